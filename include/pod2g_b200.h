@@ -1,0 +1,205 @@
+/*
+ * pod2g_b200.h -- C-ABI of the B200-native POD-2G solve path.
+ *
+ * This is the drop-in boundary for the reference's solve phase
+ * (/root/reference/proj/include/pod2g/, cited as file:line below):
+ *
+ *   reference                                           this ABI
+ *   CsrMatrix (core/csr.hpp:14-59)                      p2g_set_pattern + p2g_set_values
+ *   PodBasis::phi_r (pod.hpp:19-25)                     p2g_set_basis
+ *   Pod2gPreconditioner ctor (pod.hpp:261-263)          p2g_setup   (A_c = Phi^T K Phi + factor)
+ *     -> Pod2gOperator ctor (pod.hpp:186-189)
+ *     -> reduced_operator (pod.hpp:152-165), DenseLu (core/dense_solve.hpp:15-38)
+ *   reduced_solve (pod.hpp:167-179)                     p2g_initial_guess
+ *   pcg_solve (krylov.hpp:243-297) + SolveReport        p2g_solve
+ *     (core/report.hpp:13-23)
+ *   spmv (core/csr.hpp:83-93)                           p2g_spmv        (test hook)
+ *   Pod2gPreconditioner::apply (pod.hpp:264-267)        p2g_precond_apply (test hook)
+ *   gauss_seidel_sweep[_backward] (smoothers.hpp:26-72) p2g_smooth      (test hook)
+ *
+ * One handle owns one CUDA device, one stream, one sparsity pattern, one POD
+ * basis and a BATCH of B value sets sharing the pattern (the instances the
+ * reference runs one per parallel_for slot, core/parallel.hpp:16-43).  A
+ * handle is not thread-safe; many handles on many threads/devices are
+ * (the reference's reentrancy contract, krylov.hpp:12-13).
+ *
+ * Host arrays are instance-major, like B separate std::vector<double>:
+ * values [B][nnz], vectors [B][n], coarse matrices [B][k][k].  Indices use
+ * the reference's size_t (uint64_t); they are range-checked and narrowed to
+ * int32 on the device.
+ *
+ * Errors: every call returns a p2g_status.  P2G_EINVAL mirrors the
+ * reference's std::invalid_argument (require(), core/types.hpp:15-17); the
+ * per-instance codes of p2g_solve mirror its std::runtime_error cases
+ * (krylov.hpp:265-266, 274-275, 287-288, 295; core/dense_solve.hpp:25-26;
+ * smoothers.hpp:41-43).  p2g_last_error() holds the message.
+ *
+ * There is no CPU fallback: without a CUDA device p2g_create fails with
+ * P2G_ECUDA.
+ */
+#ifndef POD2G_B200_H
+#define POD2G_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define P2G_ABI_VERSION 1
+
+typedef struct p2g_handle p2g_handle;
+
+typedef enum {
+    P2G_OK = 0,
+    P2G_EINVAL = 1,      /* invalid argument / dimension mismatch (require)          */
+    P2G_EBREAKDOWN = 2,  /* r.s <= 0, p^T K p <= 0, or rs' <= 0 (krylov.hpp:265-288)  */
+    P2G_ENONFINITE = 3,  /* non-finite entries in solution (krylov.hpp:295)          */
+    P2G_ESINGULAR = 4,   /* coarse operator not SPD / singular (dense_solve.hpp:25)  */
+    P2G_EZERODIAG = 5,   /* zero diagonal in a smoother row (smoothers.hpp:41-43)    */
+    P2G_ECUDA = 6,       /* CUDA runtime error / no device                           */
+    P2G_ENCCL = 7,       /* NCCL error (row-partitioned handles)                      */
+    P2G_ESTATE = 8       /* call order violated (e.g. solve before setup)            */
+} p2g_status;
+
+typedef enum {
+    /* Symmetric Gauss-Seidel in node-colour order: forward sweep over colours
+     * 0..C-1, backward over C-1..0, the dofs of one node in ascending
+     * (forward) / descending (backward) order.  Identical to the reference's
+     * natural-order sweeps (smoothers.hpp:26-72) applied to the
+     * colour-permuted system P K P^T -- the stated reordering deviation. */
+    P2G_SMOOTHER_GS_MULTICOLOR = 0,
+    /* Damped Jacobi, exactly jacobi_sweep (smoothers.hpp:75-87): no reordering. */
+    P2G_SMOOTHER_JACOBI = 1
+} p2g_smoother;
+
+typedef enum {
+    /* t = r - K s with the reference's full row sum (csr.hpp:96-105). */
+    P2G_RESIDUAL_FULL = 0,
+    /* After ONE forward GS sweep from s = 0, (D+L) s = r holds row by row, so
+     * t = r - K s = -U s: only the strictly-upper part of each row is read
+     * (half a matrix pass).  Same value up to rounding.  Used only when
+     * smoother == GS_MULTICOLOR and r1 == 1; otherwise FULL is used. */
+    P2G_RESIDUAL_UPPER = 1
+} p2g_residual_form;
+
+typedef struct {
+    int32_t smoother;       /* p2g_smoother; reference default GS (smoothers.hpp:10-14)  */
+    int32_t pre_sweeps;     /* r1 >= 1 (pod.hpp:186, bench.hpp:122)                      */
+    int32_t post_sweeps;    /* r2 >= 1                                                   */
+    int32_t residual_form;  /* p2g_residual_form                                         */
+    double omega;           /* damped Jacobi weight in (0,1] (smoothers.hpp:79)           */
+} p2g_config;
+
+/* Initialise cfg with the defaults: GS_MULTICOLOR, r1 = r2 = 1, RESIDUAL_UPPER,
+ * omega = 0.5 (2/3, the reference default, is unsafe for these operators:
+ * see DESIGN.md). */
+void p2g_config_default(p2g_config* cfg);
+
+/* ---- lifetime ---------------------------------------------------------- */
+int p2g_create(int device, p2g_handle** out);
+int p2g_destroy(p2g_handle* h);
+const char* p2g_last_error(const p2g_handle* h);
+const char* p2g_status_string(int status);
+int p2g_abi_version(void);
+
+/* ---- data -------------------------------------------------------------- */
+/* Square CSR pattern (CsrMatrix::validate invariants, csr.hpp:33-46: offsets
+ * non-decreasing from 0 to nnz, columns strictly increasing and < n, every
+ * row holding its diagonal).  block_size = dofs per node (rows
+ * node*bs .. node*bs+bs-1 belong to one node; 1 = point colouring).  The
+ * node graph is coloured greedily in natural order. */
+int p2g_set_pattern(p2g_handle* h, int64_t n, const uint64_t* row_offsets,
+                    const uint64_t* col_indices, int32_t block_size);
+
+/* B value sets [B][nnz] in the pattern's natural order (host memory).
+ * Resets any previous setup. */
+int p2g_set_values(p2g_handle* h, int32_t batch, const double* values);
+/* Same, from device memory of the handle's device ([B][nnz]). */
+int p2g_set_values_device(p2g_handle* h, int32_t batch, const double* d_values);
+
+/* POD basis Phi, n x k row-major (PodBasis::phi_r, pod.hpp:20; rank k).
+ * k == 0 disables the coarse correction (pure symmetric smoother). */
+int p2g_set_basis(p2g_handle* h, int32_t k, const double* phi);
+
+/* Per-instance setup (Pod2gOperator ctor, pod.hpp:186-189): A_c = Phi^T K Phi
+ * and its Cholesky factor.  status (may be NULL) receives B codes
+ * (P2G_ESINGULAR for a singular coarse operator, P2G_EZERODIAG for a zero
+ * smoother diagonal).  Returns the worst code. */
+int p2g_setup(p2g_handle* h, const p2g_config* cfg, int32_t* status);
+
+/* ---- solve ------------------------------------------------------------- */
+/* x0 = Phi A_c^{-1} Phi^T b per instance (reduced_solve, pod.hpp:167-179).
+ * b, x0: host [B][n]. */
+int p2g_initial_guess(p2g_handle* h, const double* b, double* x0);
+
+enum {
+    P2G_X0_ZERO = 0,     /* u0 empty => zero (krylov.hpp:247)                  */
+    P2G_X0_GIVEN = 1,    /* x0 argument                                        */
+    P2G_X0_REDUCED = 2   /* x0 = reduced_solve(K, b, Phi), computed on device  */
+};
+
+/* pcg_solve per instance (krylov.hpp:243-297) with the POD-2G preconditioner.
+ *   b        [B][n]   right-hand sides
+ *   x0       [B][n]   initial guesses (x0_mode == P2G_X0_GIVEN), else ignored
+ *   tol, max_iter     delta and max_iter of pcg_solve
+ *   x        [B][n]   solutions (output)
+ *   iters    [B]      SolveReport::cycles
+ *   converged[B]      SolveReport::converged
+ *   status   [B]      P2G_OK or the error the reference would have thrown
+ *   hist     [B][hist_cap] relative residual history incl. the initial entry
+ *                     (SolveReport::residual_history); may be NULL
+ * Any output pointer may be NULL.  Returns the worst per-instance status. */
+int p2g_solve(p2g_handle* h, const double* b, const double* x0, int32_t x0_mode, double tol,
+              int64_t max_iter, double* x, int64_t* iters, int32_t* converged, int32_t* status,
+              double* hist, int64_t hist_cap);
+
+/* Same with b / x0 / x in DEVICE memory ([B][n]); iters/converged/status/hist
+ * stay host pointers. */
+int p2g_solve_device(p2g_handle* h, const double* d_b, const double* d_x0, int32_t x0_mode,
+                     double tol, int64_t max_iter, double* d_x, int64_t* iters,
+                     int32_t* converged, int32_t* status, double* hist, int64_t hist_cap);
+
+/* Device time of the last p2g_solve / p2g_solve_device in ms (CUDA events on
+ * the handle's stream): [0] = setup-free solve incl. x0, [1] = iteration loop. */
+int p2g_last_solve_ms(const p2g_handle* h, double* ms2);
+
+/* ---- test / measurement hooks ---------------------------------------------- */
+/* y = K x per instance (spmv, csr.hpp:83-93).  x, y host [B][n]. */
+int p2g_spmv(p2g_handle* h, const double* x, double* y);
+/* s = B r (Pod2gPreconditioner::apply, pod.hpp:264-267).  host [B][n]. */
+int p2g_precond_apply(p2g_handle* h, const double* r, double* s);
+/* One smoother sweep in place: direction 0 forward, 1 backward
+ * (gauss_seidel_sweep / _backward, smoothers.hpp:26-72, in colour order;
+ * jacobi_sweep for the Jacobi smoother).  f, u host [B][n]. */
+int p2g_smooth(p2g_handle* h, int32_t direction, const double* f, double* u);
+/* Coarse operators A_c [B][k][k] as assembled on the device (before
+ * symmetrisation). */
+int p2g_coarse_operator(p2g_handle* h, double* Ac);
+
+/* Colour permutation: perm[new] = old (n entries); color_offsets receives
+ * ncolors+1 node-row offsets (cap entries at most). */
+int p2g_get_permutation(p2g_handle* h, int64_t* perm, int32_t* ncolors, int64_t* color_offsets,
+                        int32_t cap);
+
+/* Host-only (no device needed): the colouring p2g_set_pattern would use. */
+int p2g_analyze_pattern(int64_t n, const uint64_t* row_offsets, const uint64_t* col_indices,
+                        int32_t block_size, int64_t* perm, int32_t* ncolors,
+                        int64_t* color_offsets, int32_t cap, char* errbuf, int32_t errcap);
+
+/* Per-kernel-class timing of the iteration loop: runs `reps` eager
+ * iterations (no graph) with CUDA events between kernel classes on the
+ * handle's stream, on the current state of the last solve.  ms receives the
+ * mean time per iteration of each class, bytes the algorithmic HBM bytes per
+ * iteration of each class, names the class names (static). */
+#define P2G_NUM_KCLASS 9
+int p2g_profile_iteration(p2g_handle* h, int32_t reps, double* ms, double* bytes,
+                          const char** names);
+
+/* Number of kernel launches per loop iteration and in the setup/prologue. */
+int p2g_launch_counts(const p2g_handle* h, int64_t* per_iteration, int64_t* last_solve_total);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

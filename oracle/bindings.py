@@ -1,0 +1,368 @@
+"""ctypes bindings for the two CPU oracles -- TEST INFRASTRUCTURE ONLY.
+
+* ``Oracle``    -> oracle/_build/libpod2g_oracle.so, the C restatement
+                   (oracle/pod2g_oracle.c) of the reference path.
+* ``Reference`` -> oracle/_ref/libpod2g_ref.so, the unmodified reference headers
+                   (/root/reference/proj/include/pod2g) compiled by
+                   oracle/Makefile behind oracle/ref_shim.cpp.
+
+Both take CSR matrices with int64 indices (the reference's size_t) and
+row-major n x k bases, and return numpy arrays.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "_build", "libpod2g_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libpod2g_ref.so")
+
+_D = C.POINTER(C.c_double)
+_I64 = C.POINTER(C.c_int64)
+_I32 = C.POINTER(C.c_int)
+
+SMOOTHER_GS = 0
+SMOOTHER_JACOBI = 1
+
+
+def _d(a):
+    return None if a is None else a.ctypes.data_as(_D)
+
+
+def _i64(a):
+    return None if a is None else a.ctypes.data_as(_I64)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _ix(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+@dataclass
+class SolveResult:
+    u: np.ndarray
+    iters: int
+    converged: bool
+    history: np.ndarray
+    status: int
+    wall_s: float = float("nan")
+
+
+class _Csr(C.Structure):
+    _fields_ = [("n", C.c_int64), ("rp", _I64), ("ci", _I64), ("v", _D)]
+
+
+class Oracle:
+    """The C restatement of krylov.hpp/pod.hpp/smoothers.hpp/csr.hpp."""
+
+    def __init__(self, path: str = ORACLE_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"oracle not built: {path} (run make -C oracle)")
+        self.lib = L = C.CDLL(path)
+        L.or_dot.restype = C.c_double
+        L.or_dot.argtypes = [C.c_int64, _D, _D]
+        for name in ("or_spmv",):
+            getattr(L, name).argtypes = [C.POINTER(_Csr), _D, _D]
+        L.or_residual.argtypes = [C.POINTER(_Csr), _D, _D, _D]
+        L.or_gs_forward.argtypes = [C.POINTER(_Csr), _D, _D, C.c_int64]
+        L.or_gs_backward.argtypes = [C.POINTER(_Csr), _D, _D, C.c_int64]
+        L.or_jacobi_sweep.argtypes = [C.POINTER(_Csr), _D, _D, C.c_double, C.c_int64]
+        L.or_project.argtypes = [C.c_int64, C.c_int64, _D, _D, _D]
+        L.or_lift.argtypes = [C.c_int64, C.c_int64, _D, _D, _D]
+        L.or_lu_factor.argtypes = [C.c_int64, _D, _I64]
+        L.or_lu_solve.argtypes = [C.c_int64, _D, _I64, _D, _D]
+        L.or_reduced_operator.argtypes = [C.POINTER(_Csr), C.c_int64, _D, _D]
+        L.or_reduced_solve.argtypes = [C.POINTER(_Csr), _D, C.c_int64, _D, _D, _D]
+        L.or_pcg_pod2g.argtypes = [C.POINTER(_Csr), _D, C.c_int64, _D, _D, C.c_double, C.c_int64,
+                                   C.c_int, C.c_double, C.c_int64, C.c_int64, _D, _I64, _I32,
+                                   _D, C.c_int64, _I64]
+        L.or_pcg_pod2g_batch.argtypes = [C.c_int64, _I64, _I64, C.c_int64, _D, C.c_int64, _D,
+                                         C.c_int64, _D, _D, C.c_double, C.c_int64, C.c_int,
+                                         C.c_double, _D, _I64, _I32, _I32, C.c_int]
+
+    @staticmethod
+    def _csr(rp, ci, v):
+        keep = (_ix(rp), _ix(ci), _f64(v))
+        return _Csr(len(keep[0]) - 1, _i64(keep[0]), _i64(keep[1]), _d(keep[2])), keep
+
+    def spmv(self, rp, ci, v, x):
+        A, keep = self._csr(rp, ci, v)
+        x = _f64(x)
+        y = np.empty(A.n)
+        self.lib.or_spmv(C.byref(A), _d(x), _d(y))
+        return y
+
+    def residual(self, rp, ci, v, f, u):
+        A, keep = self._csr(rp, ci, v)
+        f, u = _f64(f), _f64(u)
+        r = np.empty(A.n)
+        self.lib.or_residual(C.byref(A), _d(f), _d(u), _d(r))
+        return r
+
+    def gauss_seidel(self, rp, ci, v, f, u, sweeps=1, backward=False):
+        A, keep = self._csr(rp, ci, v)
+        f = _f64(f)
+        u = _f64(u).copy()
+        fn = self.lib.or_gs_backward if backward else self.lib.or_gs_forward
+        st = fn(C.byref(A), _d(f), _d(u), sweeps)
+        return u, st
+
+    def jacobi_sweep(self, rp, ci, v, f, u, omega, sweeps=1):
+        A, keep = self._csr(rp, ci, v)
+        f = _f64(f)
+        u = _f64(u).copy()
+        st = self.lib.or_jacobi_sweep(C.byref(A), _d(f), _d(u), omega, sweeps)
+        return u, st
+
+    def project(self, phi, u):
+        phi, u = _f64(phi), _f64(u)
+        n, k = phi.shape
+        z = np.empty(k)
+        self.lib.or_project(n, k, _d(phi), _d(u), _d(z))
+        return z
+
+    def lift(self, phi, z):
+        phi, z = _f64(phi), _f64(z)
+        n, k = phi.shape
+        u = np.empty(n)
+        self.lib.or_lift(n, k, _d(phi), _d(z), _d(u))
+        return u
+
+    def dense_solve(self, A, b):
+        A = _f64(A).copy()
+        k = A.shape[0]
+        perm = np.empty(k, dtype=np.int64)
+        st = self.lib.or_lu_factor(k, _d(A), _i64(perm))
+        if st != 0:
+            return None, st
+        x = np.empty(k)
+        self.lib.or_lu_solve(k, _d(A), _i64(perm), _d(_f64(b)), _d(x))
+        return x, 0
+
+    def reduced_operator(self, rp, ci, v, phi):
+        A, keep = self._csr(rp, ci, v)
+        phi = _f64(phi)
+        k = phi.shape[1]
+        Ac = np.empty((k, k))
+        self.lib.or_reduced_operator(C.byref(A), k, _d(phi), _d(Ac))
+        return Ac
+
+    def reduced_solve(self, rp, ci, v, f, phi):
+        A, keep = self._csr(rp, ci, v)
+        phi, f = _f64(phi), _f64(f)
+        k = phi.shape[1]
+        x0 = np.empty(A.n)
+        ur = np.empty(k)
+        st = self.lib.or_reduced_solve(C.byref(A), _d(f), k, _d(phi), _d(x0), _d(ur))
+        return x0, ur, st
+
+    def pcg_pod2g(self, rp, ci, v, f, phi, u0=None, delta=1e-8, max_iter=100000,
+                  smoother=SMOOTHER_GS, omega=2.0 / 3.0, r1=1, r2=1, hist_cap=None):
+        A, keep = self._csr(rp, ci, v)
+        f = _f64(f)
+        if phi is None:
+            k, phi_a = 0, np.zeros((1, 1))
+        else:
+            phi_a = _f64(phi)
+            k = phi_a.shape[1]
+        u0a = None if u0 is None else _f64(u0)
+        u = np.empty(A.n)
+        it = C.c_int64()
+        conv = C.c_int()
+        cap = int(hist_cap if hist_cap is not None else min(max_iter, 200000) + 1)
+        hist = np.empty(cap)
+        hl = C.c_int64()
+        st = self.lib.or_pcg_pod2g(C.byref(A), _d(f), k, _d(phi_a), _d(u0a), delta, max_iter,
+                                   smoother, omega, r1, r2, _d(u), C.byref(it), C.byref(conv),
+                                   _d(hist), cap, C.byref(hl))
+        return SolveResult(u, it.value, bool(conv.value), hist[: min(hl.value, cap)].copy(), st)
+
+    def pcg_pod2g_batch(self, rp, ci, values, f, phi, u0=None, delta=1e-8, max_iter=100000,
+                        smoother=SMOOTHER_GS, omega=2.0 / 3.0, nthreads=1):
+        rp, ci = _ix(rp), _ix(ci)
+        values = _f64(values)
+        B, nnz = values.shape
+        n = len(rp) - 1
+        f = _f64(f)
+        phi = _f64(phi)
+        k = phi.shape[1]
+        u0a = None if u0 is None else _f64(u0)
+        u = np.empty((B, n))
+        it = np.empty(B, dtype=np.int64)
+        conv = np.empty(B, dtype=np.int32)
+        status = np.empty(B, dtype=np.int32)
+        self.lib.or_pcg_pod2g_batch(n, _i64(rp), _i64(ci), nnz, _d(values), B, _d(f), k, _d(phi),
+                                    _d(u0a), delta, max_iter, smoother, omega, _d(u), _i64(it),
+                                    conv.ctypes.data_as(_I32), status.ctypes.data_as(_I32),
+                                    nthreads)
+        return u, it, conv, status
+
+
+class Reference:
+    """The unmodified reference, compiled from /root/reference (oracle/_ref)."""
+
+    def __init__(self, path: str = REF_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"reference not built: {path} (run make -C oracle ref)")
+        self.lib = L = C.CDLL(path)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_spmv.argtypes = [C.c_int64, _I64, _I64, _D, _D, _D]
+        L.ref_residual.argtypes = [C.c_int64, _I64, _I64, _D, _D, _D, _D]
+        L.ref_gauss_seidel.argtypes = [C.c_int64, _I64, _I64, _D, _D, _D, C.c_int64, C.c_int]
+        L.ref_jacobi_sweep.argtypes = [C.c_int64, _I64, _I64, _D, _D, _D, C.c_double, C.c_int64]
+        L.ref_reduced_operator.argtypes = [C.c_int64, _I64, _I64, _D, C.c_int64, _D, _D]
+        L.ref_reduced_solve.argtypes = [C.c_int64, _I64, _I64, _D, _D, C.c_int64, _D, _D, _D]
+        L.ref_dense_solve.argtypes = [C.c_int64, _D, _D, _D]
+        L.ref_pod2g_apply.argtypes = [C.c_int64, _I64, _I64, _D, C.c_int64, _D, C.c_int,
+                                      C.c_double, _D, _D]
+        L.ref_pcg_pod2g.argtypes = [C.c_int64, _I64, _I64, _D, _D, C.c_int64, _D, _D, C.c_double,
+                                    C.c_int64, C.c_int, C.c_double, _D, _I64, _I32, _D,
+                                    C.c_int64, _I64, _D]
+        L.ref_cg_solve.argtypes = [C.c_int64, _I64, _I64, _D, _D, C.c_double, C.c_int64, _D,
+                                   _I64, _I32, _D, C.c_int64, _I64]
+        L.ref_pcg_pod2g_batch.argtypes = [C.c_int64, _I64, _I64, C.c_int64, _D, C.c_int64, _D,
+                                          C.c_int64, _D, C.c_int, C.c_double, C.c_int64, _D,
+                                          _I64, _I32, _I32, C.c_int]
+        L.ref_its_case.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
+                                   C.c_int64, _I64, _I64, _I64, _I64, _I64, _D, _D, _D,
+                                   C.c_int64]
+
+    def _check(self, st):
+        if st != 0:
+            msg = self.lib.ref_last_error().decode()
+            raise (ValueError if st == 1 else RuntimeError)(msg)
+
+    def spmv(self, rp, ci, v, x):
+        rp, ci, v, x = _ix(rp), _ix(ci), _f64(v), _f64(x)
+        y = np.empty(len(rp) - 1)
+        self._check(self.lib.ref_spmv(len(rp) - 1, _i64(rp), _i64(ci), _d(v), _d(x), _d(y)))
+        return y
+
+    def residual(self, rp, ci, v, f, u):
+        rp, ci, v, f, u = _ix(rp), _ix(ci), _f64(v), _f64(f), _f64(u)
+        r = np.empty(len(rp) - 1)
+        self._check(self.lib.ref_residual(len(rp) - 1, _i64(rp), _i64(ci), _d(v), _d(f), _d(u),
+                                          _d(r)))
+        return r
+
+    def gauss_seidel(self, rp, ci, v, f, u, sweeps=1, backward=False):
+        rp, ci, v, f = _ix(rp), _ix(ci), _f64(v), _f64(f)
+        u = _f64(u).copy()
+        self._check(self.lib.ref_gauss_seidel(len(rp) - 1, _i64(rp), _i64(ci), _d(v), _d(f),
+                                              _d(u), sweeps, 1 if backward else 0))
+        return u
+
+    def jacobi_sweep(self, rp, ci, v, f, u, omega, sweeps=1):
+        rp, ci, v, f = _ix(rp), _ix(ci), _f64(v), _f64(f)
+        u = _f64(u).copy()
+        self._check(self.lib.ref_jacobi_sweep(len(rp) - 1, _i64(rp), _i64(ci), _d(v), _d(f),
+                                              _d(u), omega, sweeps))
+        return u
+
+    def reduced_operator(self, rp, ci, v, phi):
+        rp, ci, v, phi = _ix(rp), _ix(ci), _f64(v), _f64(phi)
+        k = phi.shape[1]
+        Ac = np.empty((k, k))
+        self._check(self.lib.ref_reduced_operator(len(rp) - 1, _i64(rp), _i64(ci), _d(v), k,
+                                                  _d(phi), _d(Ac)))
+        return Ac
+
+    def reduced_solve(self, rp, ci, v, f, phi):
+        rp, ci, v, f, phi = _ix(rp), _ix(ci), _f64(v), _f64(f), _f64(phi)
+        k = phi.shape[1]
+        x0 = np.empty(len(rp) - 1)
+        ur = np.empty(k)
+        self._check(self.lib.ref_reduced_solve(len(rp) - 1, _i64(rp), _i64(ci), _d(v), _d(f), k,
+                                               _d(phi), _d(x0), _d(ur)))
+        return x0, ur
+
+    def dense_solve(self, A, b):
+        A, b = _f64(A), _f64(b)
+        x = np.empty(A.shape[0])
+        self._check(self.lib.ref_dense_solve(A.shape[0], _d(A), _d(b), _d(x)))
+        return x
+
+    def pod2g_apply(self, rp, ci, v, phi, r, smoother=SMOOTHER_GS, omega=2.0 / 3.0):
+        rp, ci, v, phi, r = _ix(rp), _ix(ci), _f64(v), _f64(phi), _f64(r)
+        s = np.empty(len(rp) - 1)
+        self._check(self.lib.ref_pod2g_apply(len(rp) - 1, _i64(rp), _i64(ci), _d(v),
+                                             phi.shape[1], _d(phi), smoother, omega, _d(r),
+                                             _d(s)))
+        return s
+
+    def pcg_pod2g(self, rp, ci, v, f, phi, u0=None, delta=1e-8, max_iter=100000,
+                  smoother=SMOOTHER_GS, omega=2.0 / 3.0, hist_cap=None):
+        rp, ci, v, f = _ix(rp), _ix(ci), _f64(v), _f64(f)
+        n = len(rp) - 1
+        if phi is None:
+            k, phi_a = 0, np.zeros((1, 1))
+        else:
+            phi_a = _f64(phi)
+            k = phi_a.shape[1]
+        u0a = None if u0 is None else _f64(u0)
+        u = np.empty(n)
+        it = C.c_int64()
+        conv = C.c_int()
+        cap = int(hist_cap if hist_cap is not None else min(max_iter, 200000) + 1)
+        hist = np.empty(cap)
+        hl = C.c_int64()
+        wall = C.c_double()
+        st = self.lib.ref_pcg_pod2g(n, _i64(rp), _i64(ci), _d(v), _d(f), k, _d(phi_a), _d(u0a),
+                                    delta, max_iter, smoother, omega, _d(u), C.byref(it),
+                                    C.byref(conv), _d(hist), cap, C.byref(hl), C.byref(wall))
+        if st != 0:
+            return SolveResult(u, 0, False, np.empty(0), st)
+        return SolveResult(u, it.value, bool(conv.value), hist[: min(hl.value, cap)].copy(), 0,
+                           wall.value)
+
+    def cg_solve(self, rp, ci, v, f, delta=1e-8, max_iter=100000):
+        rp, ci, v, f = _ix(rp), _ix(ci), _f64(v), _f64(f)
+        n = len(rp) - 1
+        u = np.empty(n)
+        it = C.c_int64()
+        conv = C.c_int()
+        cap = max_iter + 1
+        hist = np.empty(cap)
+        hl = C.c_int64()
+        self._check(self.lib.ref_cg_solve(n, _i64(rp), _i64(ci), _d(v), _d(f), delta, max_iter,
+                                          _d(u), C.byref(it), C.byref(conv), _d(hist), cap,
+                                          C.byref(hl)))
+        return SolveResult(u, it.value, bool(conv.value), hist[: min(hl.value, cap)].copy(), 0)
+
+    def pcg_pod2g_batch(self, rp, ci, values, f, phi, x0_mode=1, delta=1e-8, max_iter=100000,
+                        jobs=1):
+        rp, ci = _ix(rp), _ix(ci)
+        values, f, phi = _f64(values), _f64(f), _f64(phi)
+        B, nnz = values.shape
+        n = len(rp) - 1
+        u = np.empty((B, n))
+        it = np.empty(B, dtype=np.int64)
+        conv = np.empty(B, dtype=np.int32)
+        failed = np.empty(B, dtype=np.int32)
+        self._check(self.lib.ref_pcg_pod2g_batch(
+            n, _i64(rp), _i64(ci), nnz, _d(values), B, _d(f), phi.shape[1], _d(phi), x0_mode,
+            delta, max_iter, _d(u), _i64(it), conv.ctypes.data_as(_I32),
+            failed.ctypes.data_as(_I32), jobs))
+        return u, it, conv, failed
+
+    def its_case(self, res=32, n_snapshots=100, offline_seed=42, bench_seed=7, inst=0, jobs=8):
+        n, nnz, rank = C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(self.lib.ref_its_case(res, n_snapshots, offline_seed, bench_seed, inst, jobs,
+                                          C.byref(n), C.byref(nnz), C.byref(rank), None, None,
+                                          None, None, None, 0))
+        rp = np.empty(n.value + 1, dtype=np.int64)
+        ci = np.empty(nnz.value, dtype=np.int64)
+        v = np.empty(nnz.value)
+        f = np.empty(n.value)
+        phi = np.empty((n.value, rank.value))
+        self._check(self.lib.ref_its_case(res, n_snapshots, offline_seed, bench_seed, inst, jobs,
+                                          C.byref(n), C.byref(nnz), C.byref(rank), _i64(rp),
+                                          _i64(ci), _d(v), _d(f), _d(phi), phi.size))
+        return rp, ci, v, f, phi

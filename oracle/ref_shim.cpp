@@ -1,0 +1,307 @@
+// ref_shim.cpp -- extern "C" entry points over the UNMODIFIED reference
+// headers (/root/reference/proj/include/pod2g, read-only, compiled in place by
+// oracle/Makefile into oracle/_ref/libpod2g_ref.so).
+//
+// TEST INFRASTRUCTURE ONLY: used by tests/ to pin the C restatement
+// (oracle/pod2g_oracle.c) and the CUDA path, and by bench.py --impl reference
+// as the reference CPU arm.  No reference source is copied: this file only
+// marshals plain arrays into pod2g::CsrMatrix / PodBasis and calls the
+// reference's own functions.
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+
+#include "pod2g/bench.hpp"
+#include "pod2g/core/parallel.hpp"
+#include "pod2g/krylov.hpp"
+#include "pod2g/pod.hpp"
+#include "pod2g/problems.hpp"
+#include "pod2g/smoothers.hpp"
+
+using namespace pod2g;
+
+namespace {
+
+thread_local std::string g_err;
+
+enum { RS_OK = 0, RS_EINVAL = 1, RS_ERUNTIME = 2 };
+
+CsrMatrix make_csr(int64_t n, const int64_t* rp, const int64_t* ci, const double* v) {
+    CsrMatrix K(static_cast<index_t>(n), static_cast<index_t>(n));
+    const index_t nnz = static_cast<index_t>(rp[n]);
+    for (int64_t i = 0; i <= n; ++i) K.row_offsets[i] = static_cast<index_t>(rp[i]);
+    K.col_indices.assign(ci, ci + nnz);
+    K.values.assign(v, v + nnz);
+    K.symmetric_hint = true;
+    return K;
+}
+
+PodBasis make_basis(int64_t n, int64_t k, const double* phi) {
+    PodBasis b;
+    b.rank = static_cast<index_t>(k);
+    b.phi_r = DenseMatrix(static_cast<index_t>(n), static_cast<index_t>(k));
+    std::memcpy(b.phi_r.data.data(), phi, sizeof(double) * static_cast<size_t>(n * k));
+    return b;
+}
+
+// The damped-Jacobi variant of the POD-2G preconditioner: the public
+// Pod2gOperator (pod.hpp:184-215) with SmootherConfig{DampedJacobi,1,omega},
+// applied exactly like Pod2gPreconditioner::apply (pod.hpp:264-267).
+class Pod2gJacobiPreconditioner final : public Preconditioner {
+public:
+    Pod2gJacobiPreconditioner(const CsrMatrix& K, const PodBasis& basis, double omega)
+        : op_(K, basis, 1, 1, SmootherConfig{SmootherKind::DampedJacobi, 1, omega}) {}
+    void apply(const Vector& r, Vector& s) const override {
+        s.assign(r.size(), 0.0);
+        op_.cycle(r, s, true);
+    }
+    std::string name() const override { return "pod2g-jacobi"; }
+
+private:
+    Pod2gOperator op_;
+};
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return RS_OK;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return RS_EINVAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return RS_ERUNTIME;
+    }
+}
+
+struct SolveOut {
+    double* u;
+    int64_t* iters;
+    int* converged;
+    double* hist;
+    int64_t hist_cap;
+    int64_t* hist_len;
+    double* wall_s;
+};
+
+void write_out(const std::pair<Vector, SolveReport>& res, const SolveOut& o) {
+    std::memcpy(o.u, res.first.data(), sizeof(double) * res.first.size());
+    *o.iters = static_cast<int64_t>(res.second.cycles);
+    *o.converged = res.second.converged ? 1 : 0;
+    const auto& h = res.second.residual_history;
+    if (o.hist)
+        for (size_t i = 0; i < h.size() && static_cast<int64_t>(i) < o.hist_cap; ++i)
+            o.hist[i] = h[i];
+    if (o.hist_len) *o.hist_len = static_cast<int64_t>(h.size());
+    if (o.wall_s) *o.wall_s = res.second.wall_time_s;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_spmv(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, const double* x,
+             double* y) {
+    return guarded([&] {
+        const CsrMatrix K = make_csr(n, rp, ci, v);
+        const Vector out = spmv(K, Vector(x, x + n));
+        std::memcpy(y, out.data(), sizeof(double) * n);
+    });
+}
+
+int ref_residual(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                 const double* f, const double* u, double* r) {
+    return guarded([&] {
+        const CsrMatrix K = make_csr(n, rp, ci, v);
+        Vector out;
+        residual(K, Vector(f, f + n), Vector(u, u + n), out);
+        std::memcpy(r, out.data(), sizeof(double) * n);
+    });
+}
+
+// direction: 0 forward, 1 backward
+int ref_gauss_seidel(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                     const double* f, double* u, int64_t sweeps, int direction) {
+    return guarded([&] {
+        const CsrMatrix K = make_csr(n, rp, ci, v);
+        Vector uu(u, u + n);
+        if (direction == 0)
+            gauss_seidel_sweep(K, Vector(f, f + n), uu, static_cast<index_t>(sweeps));
+        else
+            gauss_seidel_sweep_backward(K, Vector(f, f + n), uu, static_cast<index_t>(sweeps));
+        std::memcpy(u, uu.data(), sizeof(double) * n);
+    });
+}
+
+int ref_jacobi_sweep(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                     const double* f, double* u, double omega, int64_t sweeps) {
+    return guarded([&] {
+        const CsrMatrix K = make_csr(n, rp, ci, v);
+        Vector uu(u, u + n);
+        jacobi_sweep(K, Vector(f, f + n), uu, omega, static_cast<index_t>(sweeps));
+        std::memcpy(u, uu.data(), sizeof(double) * n);
+    });
+}
+
+int ref_reduced_operator(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                         int64_t k, const double* phi, double* Ac) {
+    return guarded([&] {
+        const CsrMatrix K = make_csr(n, rp, ci, v);
+        const DenseMatrix A = reduced_operator(K, make_basis(n, k, phi));
+        std::memcpy(Ac, A.data.data(), sizeof(double) * k * k);
+    });
+}
+
+int ref_reduced_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                      const double* f, int64_t k, const double* phi, double* x0, double* ur) {
+    return guarded([&] {
+        const CsrMatrix K = make_csr(n, rp, ci, v);
+        const auto res = reduced_solve(K, Vector(f, f + n), make_basis(n, k, phi));
+        std::memcpy(x0, res.first.data(), sizeof(double) * n);
+        if (ur) std::memcpy(ur, res.second.data(), sizeof(double) * k);
+    });
+}
+
+int ref_dense_solve(int64_t k, const double* A, const double* b, double* x) {
+    return guarded([&] {
+        DenseMatrix M(static_cast<index_t>(k), static_cast<index_t>(k));
+        std::memcpy(M.data.data(), A, sizeof(double) * k * k);
+        const Vector out = dense_solve(M, Vector(b, b + k));
+        std::memcpy(x, out.data(), sizeof(double) * k);
+    });
+}
+
+// smoother: 0 = reference Pod2gPreconditioner (GS), 1 = damped Jacobi variant
+int ref_pod2g_apply(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, int64_t k,
+                    const double* phi, int smoother, double omega, const double* r, double* s) {
+    return guarded([&] {
+        auto K = std::make_shared<const CsrMatrix>(make_csr(n, rp, ci, v));
+        auto basis = std::make_shared<const PodBasis>(make_basis(n, k, phi));
+        Vector out;
+        if (smoother == 0) {
+            Pod2gPreconditioner T(K, basis, 1, 1);
+            T.apply(Vector(r, r + n), out);
+        } else {
+            Pod2gJacobiPreconditioner T(*K, *basis, omega);
+            T.apply(Vector(r, r + n), out);
+        }
+        std::memcpy(s, out.data(), sizeof(double) * n);
+    });
+}
+
+// pcg_solve (krylov.hpp:243-297) with Pod2gPreconditioner (smoother 0),
+// the damped-Jacobi POD-2G variant (smoother 1), or identity (k == 0).
+int ref_pcg_pod2g(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                  const double* f, int64_t k, const double* phi, const double* u0, double delta,
+                  int64_t max_iter, int smoother, double omega, double* u, int64_t* iters,
+                  int* converged, double* hist, int64_t hist_cap, int64_t* hist_len,
+                  double* wall_s) {
+    return guarded([&] {
+        auto K = std::make_shared<const CsrMatrix>(make_csr(n, rp, ci, v));
+        const Vector ff(f, f + n);
+        Vector uu0 = u0 ? Vector(u0, u0 + n) : Vector{};
+        const SolveOut o{u, iters, converged, hist, hist_cap, hist_len, wall_s};
+        if (k == 0) {
+            IdentityPreconditioner T;
+            write_out(pcg_solve(*K, ff, T, uu0, delta, static_cast<index_t>(max_iter)), o);
+        } else if (smoother == 0) {
+            auto basis = std::make_shared<const PodBasis>(make_basis(n, k, phi));
+            Pod2gPreconditioner T(K, basis, 1, 1);
+            write_out(pcg_solve(*K, ff, T, uu0, delta, static_cast<index_t>(max_iter)), o);
+        } else {
+            const PodBasis basis = make_basis(n, k, phi);
+            Pod2gJacobiPreconditioner T(*K, basis, omega);
+            write_out(pcg_solve(*K, ff, T, uu0, delta, static_cast<index_t>(max_iter)), o);
+        }
+    });
+}
+
+int ref_cg_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                 const double* f, double delta, int64_t max_iter, double* u, int64_t* iters,
+                 int* converged, double* hist, int64_t hist_cap, int64_t* hist_len) {
+    return guarded([&] {
+        const CsrMatrix K = make_csr(n, rp, ci, v);
+        const SolveOut o{u, iters, converged, hist, hist_cap, hist_len, nullptr};
+        write_out(cg_solve(K, Vector(f, f + n), {}, delta, static_cast<index_t>(max_iter)), o);
+    });
+}
+
+// The reference CPU arm: B instances of one pattern, each a fresh
+// Pod2gPreconditioner (A_c + LU, pod.hpp:261-263) + reduced_solve x0
+// (pod.hpp:167-179, when x0_mode == 1) + pcg_solve, run over worker threads
+// with the reference's own parallel_for (core/parallel.hpp:16-43) exactly as
+// run_pcg_benchmark does (bench.hpp:290-330).
+int ref_pcg_pod2g_batch(int64_t n, const int64_t* rp, const int64_t* ci, int64_t nnz,
+                        const double* values, int64_t B, const double* f, int64_t k,
+                        const double* phi, int x0_mode, double delta, int64_t max_iter,
+                        double* u, int64_t* iters, int* converged, int* failed, int jobs) {
+    return guarded([&] {
+        auto basis = std::make_shared<const PodBasis>(make_basis(n, k, phi));
+        parallel_for(static_cast<index_t>(B), static_cast<index_t>(jobs), [&](index_t b) {
+            auto K = std::make_shared<const CsrMatrix>(make_csr(n, rp, ci, values + b * nnz));
+            const Vector ff(f + b * n, f + (b + 1) * n);
+            try {
+                Vector u0;
+                if (x0_mode == 1) u0 = reduced_solve(*K, ff, *basis).first;
+                Pod2gPreconditioner T(K, basis, 1, 1);
+                auto res = pcg_solve(*K, ff, T, u0, delta, static_cast<index_t>(max_iter));
+                std::memcpy(u + b * n, res.first.data(), sizeof(double) * n);
+                iters[b] = static_cast<int64_t>(res.second.cycles);
+                converged[b] = res.second.converged ? 1 : 0;
+                failed[b] = 0;
+            } catch (const std::runtime_error&) {
+                failed[b] = 1;
+                iters[b] = 0;
+                converged[b] = 0;
+            }
+        });
+    });
+}
+
+// Known-answer case from the reference's own acceptance run: the `its`
+// problem (problems.hpp:99-177, make_its_problem :399-407) at resolution `res`,
+// offline basis exactly as run_offline builds it (bench.hpp:58-64: LHS seed,
+// generate_snapshots at 1e-10, compute_pod EnergyTarget{0.9999}), and test
+// instance `inst` of run_pcg_benchmark's sampler (bench.hpp:275-279, seed).
+// Call with null outputs to query sizes (n, nnz, rank).
+int ref_its_case(int64_t res, int64_t n_snapshots, uint64_t offline_seed, uint64_t bench_seed,
+                 int64_t inst, int64_t jobs, int64_t* n_out, int64_t* nnz_out,
+                 int64_t* rank_out, int64_t* rp, int64_t* ci, double* v, double* f,
+                 double* phi, int64_t phi_cap) {
+    return guarded([&] {
+        static std::map<std::tuple<int64_t, int64_t, uint64_t>, PodBasis> cache;
+        const ParametricProblem prob = make_its_problem(static_cast<index_t>(res));
+        const auto key = std::make_tuple(res, n_snapshots, offline_seed);
+        if (!cache.count(key)) {
+            const auto params = latin_hypercube_lognormal(static_cast<index_t>(n_snapshots),
+                                                          prob.parameters, offline_seed);
+            const SnapshotSet snaps =
+                generate_snapshots(prob, params, 1e-10, static_cast<index_t>(jobs));
+            cache[key] = compute_pod(snaps.solutions, EnergyTarget{0.9999});
+        }
+        const PodBasis& basis = cache[key];
+        Rng sampler(bench_seed);
+        Vector theta;
+        for (int64_t i = 0; i <= inst; ++i) theta = sample_lognormal(prob.parameters, sampler);
+        const AssembledSystem sys = prob.assemble(theta);
+        *n_out = static_cast<int64_t>(sys.K.nrows);
+        *nnz_out = static_cast<int64_t>(sys.K.nnz());
+        *rank_out = static_cast<int64_t>(basis.rank);
+        if (!rp) return;
+        for (index_t i = 0; i <= sys.K.nrows; ++i) rp[i] = static_cast<int64_t>(sys.K.row_offsets[i]);
+        for (index_t i = 0; i < sys.K.nnz(); ++i) {
+            ci[i] = static_cast<int64_t>(sys.K.col_indices[i]);
+            v[i] = sys.K.values[i];
+        }
+        std::memcpy(f, sys.f.data(), sizeof(double) * sys.f.size());
+        const int64_t cnt = static_cast<int64_t>(basis.phi_r.data.size());
+        std::memcpy(phi, basis.phi_r.data.data(), sizeof(double) * std::min(cnt, phi_cap));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,1045 @@
+// p2g_kernels.cuh -- sm_100a kernels of the batched POD-2G PCG solve path.
+//
+// Data layout in HBM:
+//   * rows are in colour-major node order (p2g_pattern.cpp), int32 CSR
+//     (rp, ci) shared by all instances, dpos = diagonal position per row;
+//   * values  vals[nnz][Bp]   -- the B instances of one nonzero are adjacent,
+//     so a warp streams one row with 32*V consecutive doubles per load and
+//     the column index is read once for the whole tile (4/B bytes per value);
+//   * vectors X[n][Bp]        -- same interleaving, so the x-gathers of a row
+//     are also 256/512-byte contiguous;
+//   * basis   phi[n][k]       -- PodBasis::phi_r row-major (pod.hpp:20).
+//
+// Warp tiling (Shape<R,S,W,V>): a warp covers R rows (nodes) x S slot lanes
+// per row x W instance lanes, each instance lane owning V instances.
+//   B == 1  : R=4,S=8,W=1  (2D rows, ~18 nnz)   or R=1,S=32,W=1 (3D rows, ~81 nnz)
+//   B <= 8  : R=1,S=4,W=8
+//   B <= 32 : R=1,S=1,W=32
+//   B  > 32 : R=1,S=1,W=32,V=2 (double2 per lane, 64 instances per tile)
+// With S == 1 every lane walks its row sequentially in column order with
+// separately rounded multiply and add, i.e. exactly the reference's row sums
+// (csr.hpp:83-105, smoothers.hpp:26-72); with S > 1 the row is split over
+// slot lanes and combined by a fixed xor-shuffle tree.
+//
+// All reductions (dot products, Phi^T t) are deterministic: per-block partials
+// in a fixed order, then fixed-order warp sums.  No floating-point atomics.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace p2g {
+
+constexpr int kWarps = 8;
+constexpr int kBlock = kWarps * 32;
+
+template <int R_, int S_, int W_, int V_>
+struct Shape {
+    static constexpr int R = R_, S = S_, W = W_, V = V_, T = W_ * V_;
+};
+using ShB1a = Shape<4, 8, 1, 1>;
+using ShB1b = Shape<1, 32, 1, 1>;
+using ShB8 = Shape<1, 4, 8, 1>;
+using ShB32 = Shape<1, 1, 32, 1>;
+using ShB64 = Shape<1, 1, 32, 2>;
+
+// shape used by kernels that keep k accumulators per lane (restriction,
+// K*Phi): one instance per lane to bound registers
+template <class Sh>
+struct AccShape {
+    using type = Sh;
+};
+template <>
+struct AccShape<ShB64> {
+    using type = ShB32;
+};
+
+struct Mat {
+    int n;           // rows
+    int bs;          // dofs per node
+    const int* rp;   // n+1
+    const int* ci;   // nnz
+    const int* dpos; // n
+    const double* vals;  // [nnz][Bp]
+    int Bp;
+};
+
+enum : int { ST_OK = 0, ST_EBREAKDOWN = 2, ST_ENONFINITE = 3, ST_ESINGULAR = 4, ST_EZERODIAG = 5 };
+
+struct SolveParams {
+    double tol;
+    long long max_iter;
+    long long hist_cap;
+};
+
+// ---------------------------------------------------------------- helpers
+template <class Sh>
+struct LaneGeo {
+    int lane, warp, w, s, r;
+    __device__ __forceinline__ LaneGeo() {
+        lane = threadIdx.x & 31;
+        warp = threadIdx.x >> 5;
+        w = lane % Sh::W;
+        s = (lane / Sh::W) % Sh::S;
+        r = lane / (Sh::W * Sh::S);
+    }
+};
+
+template <int V>
+__device__ __forceinline__ void ldv(double (&d)[V], const double* p) {
+    if constexpr (V == 1) {
+        d[0] = *p;
+    } else {
+        const double2 t = *reinterpret_cast<const double2*>(p);
+        d[0] = t.x;
+        d[1] = t.y;
+    }
+}
+// streamed (evict-first) load for the matrix values: read once per pass
+template <int V>
+__device__ __forceinline__ void ldv_stream(double (&d)[V], const double* p) {
+    if constexpr (V == 1) {
+        d[0] = __ldcs(p);
+    } else {
+        const double2 t = __ldcs(reinterpret_cast<const double2*>(p));
+        d[0] = t.x;
+        d[1] = t.y;
+    }
+}
+template <int V>
+__device__ __forceinline__ void stv(double* p, const double (&d)[V], const bool (&m)[V]) {
+    if constexpr (V == 1) {
+        if (m[0]) *p = d[0];
+    } else {
+        if (m[0] && m[1]) {
+            *reinterpret_cast<double2*>(p) = make_double2(d[0], d[1]);
+        } else {
+            if (m[0]) p[0] = d[0];
+            if (m[1]) p[1] = d[1];
+        }
+    }
+}
+
+template <class Sh>
+__device__ __forceinline__ double slot_sum(double x) {
+#pragma unroll
+    for (int o = Sh::W; o < Sh::W * Sh::S; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+// sum over the (s, r) lanes that share an instance lane w; result in lanes < W
+template <class Sh>
+__device__ __forceinline__ double inst_sum(double x) {
+#pragma unroll
+    for (int o = Sh::W; o < 32; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+// acc[v] += sum_{k in [k0,k1), k = k0+s (mod S)} vals[k][b] * X[ci[k]][b]
+// (separately rounded multiply and add: the reference's `s += v * x`)
+template <class Sh>
+__device__ __forceinline__ void row_dot(const Mat& A, const double* X, int b0, int k0, int k1,
+                                        int s, double (&acc)[Sh::V]) {
+#pragma unroll 4
+    for (int k = k0 + s; k < k1; k += Sh::S) {
+        const int c = __ldg(A.ci + k);
+        double a[Sh::V], x[Sh::V];
+        ldv_stream<Sh::V>(a, A.vals + (size_t)k * A.Bp + b0);
+        ldv<Sh::V>(x, X + (size_t)c * A.Bp + b0);
+#pragma unroll
+        for (int v = 0; v < Sh::V; ++v) acc[v] = __dadd_rn(acc[v], __dmul_rn(a[v], x[v]));
+    }
+}
+
+// acc[v] -= vals*X sequentially (gauss_seidel_sweep's `sum -= K_ij u_j`, S == 1 only)
+template <class Sh>
+__device__ __forceinline__ void row_sub(const Mat& A, const double* X, int b0, int k0, int k1,
+                                        double (&acc)[Sh::V]) {
+#pragma unroll 4
+    for (int k = k0; k < k1; ++k) {
+        const int c = __ldg(A.ci + k);
+        double a[Sh::V], x[Sh::V];
+        ldv_stream<Sh::V>(a, A.vals + (size_t)k * A.Bp + b0);
+        ldv<Sh::V>(x, X + (size_t)c * A.Bp + b0);
+#pragma unroll
+        for (int v = 0; v < Sh::V; ++v) acc[v] = __dsub_rn(acc[v], __dmul_rn(a[v], x[v]));
+    }
+}
+
+// One Gauss-Seidel row update (smoothers.hpp:31-44):
+//   s_i = (f_i - sum_{j != i} K_ij s_j) / K_ii
+// upper == false: only the L part is read (first forward sweep from s = 0:
+// the U-part entries of s are still zero, and subtracting zeros is exact).
+template <class Sh>
+__device__ __forceinline__ void gs_row(const Mat& A, const double* f, double* s, int i, int b0,
+                                       int lane_s, bool upper, const bool (&m)[Sh::V], bool any) {
+    double out[Sh::V];
+    if constexpr (Sh::S == 1) {
+        if (any) {
+            const int kb = __ldg(A.rp + i), kd = __ldg(A.dpos + i), ke = __ldg(A.rp + i + 1);
+            double acc[Sh::V], d[Sh::V];
+            ldv<Sh::V>(acc, f + (size_t)i * A.Bp + b0);
+            row_sub<Sh>(A, s, b0, kb, kd, acc);
+            if (upper) row_sub<Sh>(A, s, b0, kd + 1, ke, acc);
+            ldv<Sh::V>(d, A.vals + (size_t)kd * A.Bp + b0);
+#pragma unroll
+            for (int v = 0; v < Sh::V; ++v) out[v] = __ddiv_rn(acc[v], d[v]);
+            stv<Sh::V>(s + (size_t)i * A.Bp + b0, out, m);
+        }
+    } else {
+        double acc[Sh::V];
+#pragma unroll
+        for (int v = 0; v < Sh::V; ++v) acc[v] = 0.0;
+        int kd = 0;
+        if (any) {
+            const int kb = __ldg(A.rp + i), ke = __ldg(A.rp + i + 1);
+            kd = __ldg(A.dpos + i);
+            row_dot<Sh>(A, s, b0, kb, kd, lane_s, acc);
+            if (upper) row_dot<Sh>(A, s, b0, kd + 1, ke, lane_s, acc);
+        }
+#pragma unroll
+        for (int v = 0; v < Sh::V; ++v) acc[v] = slot_sum<Sh>(acc[v]);
+        if (any && lane_s == 0) {
+            double fi[Sh::V], d[Sh::V];
+            ldv<Sh::V>(fi, f + (size_t)i * A.Bp + b0);
+            ldv<Sh::V>(d, A.vals + (size_t)kd * A.Bp + b0);
+#pragma unroll
+            for (int v = 0; v < Sh::V; ++v) out[v] = __ddiv_rn(__dsub_rn(fi[v], acc[v]), d[v]);
+            stv<Sh::V>(s + (size_t)i * A.Bp + b0, out, m);
+        }
+        __syncwarp();  // the next dof of this node reads s_i
+    }
+}
+
+// block-level deterministic partial: lanes -> warps (fixed order) -> part[T]
+template <class Sh>
+__device__ __forceinline__ void block_partial(double (&acc)[Sh::V], double* part_row) {
+    __shared__ double sm[kWarps][Sh::T];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int v = 0; v < Sh::V; ++v) acc[v] = inst_sum<Sh>(acc[v]);
+    if (lane < Sh::W) {
+#pragma unroll
+        for (int v = 0; v < Sh::V; ++v) sm[warp][lane * Sh::V + v] = acc[v];
+    }
+    __syncthreads();
+    if (threadIdx.x < Sh::T) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) t += sm[w][threadIdx.x];
+        part_row[threadIdx.x] = t;
+    }
+}
+
+template <class Sh>
+__device__ __forceinline__ void lane_mask(const int* active, int b0, bool (&m)[Sh::V], bool& any) {
+    any = false;
+#pragma unroll
+    for (int v = 0; v < Sh::V; ++v) {
+        m[v] = active[b0 + v] != 0;
+        any |= m[v];
+    }
+}
+
+// grid-stride over nodes [nb, ne): node g handled by sub-group r of a warp
+#define P2G_NODE_LOOP(Sh, nb, ne, G)                                                         \
+    for (int base_ = (nb) + (blockIdx.x * kWarps + (G).warp) * Sh::R; base_ < (ne);        \
+         base_ += gridDim.x * kWarps * Sh::R)
+
+// ================================================================ kernels
+
+// y = K x (csr.hpp:83-93) on all rows; DOT: partial of x.y per instance
+// (krylov.hpp:272-273: Kp = spmv(K,p); pKp = dot(p, Kp)).
+template <class Sh, bool DOT>
+__global__ void __launch_bounds__(kBlock) k_spmv(Mat A, const double* __restrict__ x,
+                                                 double* __restrict__ y, const int* active,
+                                                 double* part) {
+    LaneGeo<Sh> G;
+    const int b0 = blockIdx.y * Sh::T + G.w * Sh::V;
+    bool m[Sh::V], any;
+    lane_mask<Sh>(active, b0, m, any);
+    double dacc[Sh::V];
+#pragma unroll
+    for (int v = 0; v < Sh::V; ++v) dacc[v] = 0.0;
+    const int nn = A.n / A.bs;
+    P2G_NODE_LOOP(Sh, 0, nn, G) {
+        const int node = base_ + G.r;
+        const bool valid = node < nn;
+        for (int c = 0; c < A.bs; ++c) {
+            const int i = node * A.bs + c;
+            double acc[Sh::V];
+#pragma unroll
+            for (int v = 0; v < Sh::V; ++v) acc[v] = 0.0;
+            if (valid && any) row_dot<Sh>(A, x, b0, __ldg(A.rp + i), __ldg(A.rp + i + 1), G.s, acc);
+#pragma unroll
+            for (int v = 0; v < Sh::V; ++v) acc[v] = slot_sum<Sh>(acc[v]);
+            if (valid && any && G.s == 0) {
+                stv<Sh::V>(y + (size_t)i * A.Bp + b0, acc, m);
+                if constexpr (DOT) {
+                    double xi[Sh::V];
+                    ldv<Sh::V>(xi, x + (size_t)i * A.Bp + b0);
+#pragma unroll
+                    for (int v = 0; v < Sh::V; ++v)
+                        dacc[v] = __dadd_rn(dacc[v], __dmul_rn(xi[v], acc[v]));
+                }
+            }
+        }
+    }
+    if constexpr (DOT) block_partial<Sh>(dacc, part + (size_t)blockIdx.x * A.Bp + blockIdx.y * Sh::T);
+}
+
+// r = f - K u (csr.hpp:96-105) with partials of r.r and f.f (for ||r0||, ||f||)
+template <class Sh>
+__global__ void __launch_bounds__(kBlock) k_residual(Mat A, const double* __restrict__ f,
+                                                     const double* __restrict__ u,
+                                                     double* __restrict__ r, const int* active,
+                                                     double* part_rr, double* part_ff) {
+    LaneGeo<Sh> G;
+    const int b0 = blockIdx.y * Sh::T + G.w * Sh::V;
+    bool m[Sh::V], any;
+    lane_mask<Sh>(active, b0, m, any);
+    double rr[Sh::V], ff[Sh::V];
+#pragma unroll
+    for (int v = 0; v < Sh::V; ++v) rr[v] = ff[v] = 0.0;
+    const int nn = A.n / A.bs;
+    P2G_NODE_LOOP(Sh, 0, nn, G) {
+        const int node = base_ + G.r;
+        const bool valid = node < nn;
+        for (int c = 0; c < A.bs; ++c) {
+            const int i = node * A.bs + c;
+            double acc[Sh::V];
+#pragma unroll
+            for (int v = 0; v < Sh::V; ++v) acc[v] = 0.0;
+            if (valid && any) row_dot<Sh>(A, u, b0, __ldg(A.rp + i), __ldg(A.rp + i + 1), G.s, acc);
+#pragma unroll
+            for (int v = 0; v < Sh::V; ++v) acc[v] = slot_sum<Sh>(acc[v]);
+            if (valid && any && G.s == 0) {
+                double fi[Sh::V], ri[Sh::V];
+                ldv<Sh::V>(fi, f + (size_t)i * A.Bp + b0);
+#pragma unroll
+                for (int v = 0; v < Sh::V; ++v) {
+                    ri[v] = __dsub_rn(fi[v], acc[v]);
+                    rr[v] = __dadd_rn(rr[v], __dmul_rn(ri[v], ri[v]));
+                    ff[v] = __dadd_rn(ff[v], __dmul_rn(fi[v], fi[v]));
+                }
+                stv<Sh::V>(r + (size_t)i * A.Bp + b0, ri, m);
+            }
+        }
+    }
+    if (part_rr) {
+        block_partial<Sh>(rr, part_rr + (size_t)blockIdx.x * A.Bp + blockIdx.y * Sh::T);
+        __syncthreads();
+        block_partial<Sh>(ff, part_ff + (size_t)blockIdx.x * A.Bp + blockIdx.y * Sh::T);
+    }
+}
+
+enum : int { PRE_NONE = 0, PRE_GS = 1, PRE_JACOBI = 2 };
+
+// PCG update fused with the first pre-smoothing step (krylov.hpp:277-279):
+//   UPDATE:  u += alpha p ; r += (-alpha) Kp ; partial r.r
+//   then     GS: colour-0 nodes' first forward sweep rows (L part only)
+//            JACOBI: s_i = omega * r_i / d_i on every row (first sweep from 0,
+//            smoothers.hpp:84-85 with u = 0)
+template <class Sh, bool UPDATE, int PRE>
+__global__ void __launch_bounds__(kBlock)
+    k_update_pre(Mat A, double* __restrict__ u, double* __restrict__ r, const double* __restrict__ p,
+                 const double* __restrict__ Kp, double* __restrict__ s, const double* alpha,
+                 const int* active, double* part_rr, int color0_nodes, double omega) {
+    LaneGeo<Sh> G;
+    const int b0 = blockIdx.y * Sh::T + G.w * Sh::V;
+    bool m[Sh::V], any;
+    lane_mask<Sh>(active, b0, m, any);
+    double al[Sh::V], rr[Sh::V];
+#pragma unroll
+    for (int v = 0; v < Sh::V; ++v) {
+        al[v] = UPDATE ? alpha[b0 + v] : 0.0;
+        rr[v] = 0.0;
+    }
+    const int nn = A.n / A.bs;
+    P2G_NODE_LOOP(Sh, 0, nn, G) {
+        const int node = base_ + G.r;
+        const bool valid = node < nn;
+        for (int c = 0; c < A.bs; ++c) {
+            const int i = node * A.bs + c;
+            if constexpr (UPDATE) {
+                if (valid && any && G.s == 0) {
+                    double ui[Sh::V], pi[Sh::V], ri[Sh::V], kpi[Sh::V];
+                    const size_t o = (size_t)i * A.Bp + b0;
+                    ldv<Sh::V>(ui, u + o);
+                    ldv<Sh::V>(pi, p + o);
+                    ldv<Sh::V>(ri, r + o);
+                    ldv<Sh::V>(kpi, Kp + o);
+#pragma unroll
+                    for (int v = 0; v < Sh::V; ++v) {
+                        ui[v] = __dadd_rn(ui[v], __dmul_rn(al[v], pi[v]));
+                        ri[v] = __dadd_rn(ri[v], __dmul_rn(-al[v], kpi[v]));
+                        rr[v] = __dadd_rn(rr[v], __dmul_rn(ri[v], ri[v]));
+                    }
+                    stv<Sh::V>(u + o, ui, m);
+                    stv<Sh::V>(r + o, ri, m);
+                }
+                if constexpr (Sh::S > 1) __syncwarp();
+            }
+            if constexpr (PRE == PRE_GS) {
+                // every lane participates (S > 1 shuffles); only colour-0 rows work
+                const bool work = any && valid && node < color0_nodes;
+                gs_row<Sh>(A, r, s, work ? i : 0, b0, G.s, false, m, work);
+            } else if constexpr (PRE == PRE_JACOBI) {
+                if (valid && any && G.s == 0) {
+                    double ri[Sh::V], d[Sh::V], si[Sh::V];
+                    const size_t o = (size_t)i * A.Bp + b0;
+                    ldv<Sh::V>(ri, r + o);
+                    ldv<Sh::V>(d, A.vals + (size_t)__ldg(A.dpos + i) * A.Bp + b0);
+#pragma unroll
+                    for (int v = 0; v < Sh::V; ++v)
+                        si[v] = __ddiv_rn(__dmul_rn(omega, ri[v]), d[v]);
+                    stv<Sh::V>(s + o, si, m);
+                }
+            }
+        }
+    }
+    if constexpr (UPDATE) block_partial<Sh>(rr, part_rr + (size_t)blockIdx.x * A.Bp + blockIdx.y * Sh::T);
+}
+
+// Forward GS colour phase: nodes [nb, ne) of one colour, dofs ascending.
+template <class Sh, bool FIRST>
+__global__ void __launch_bounds__(kBlock) k_gs_forward(Mat A, const double* __restrict__ f,
+                                                       double* s, const int* active, int nb,
+                                                       int ne) {
+    LaneGeo<Sh> G;
+    const int b0 = blockIdx.y * Sh::T + G.w * Sh::V;
+    bool m[Sh::V], any;
+    lane_mask<Sh>(active, b0, m, any);
+    P2G_NODE_LOOP(Sh, nb, ne, G) {
+        const int node = base_ + G.r;
+        const bool valid = node < ne;
+        for (int c = 0; c < A.bs; ++c)
+            gs_row<Sh>(A, f, s, valid ? node * A.bs + c : 0, b0, G.s, !FIRST, m, any && valid);
+    }
+}
+
+// Backward GS colour phase: nodes of one colour, dofs descending
+// (gauss_seidel_sweep_backward, smoothers.hpp:56-70); LAST: partial of r.s
+// over this colour's rows (krylov.hpp:280 rs_new = dot(r, s)).
+template <class Sh, bool LAST>
+__global__ void __launch_bounds__(kBlock) k_gs_backward(Mat A, const double* __restrict__ f,
+                                                        double* s, const int* active, int nb,
+                                                        int ne, double* part_rs) {
+    LaneGeo<Sh> G;
+    const int b0 = blockIdx.y * Sh::T + G.w * Sh::V;
+    bool m[Sh::V], any;
+    lane_mask<Sh>(active, b0, m, any);
+    double rs[Sh::V];
+#pragma unroll
+    for (int v = 0; v < Sh::V; ++v) rs[v] = 0.0;
+    P2G_NODE_LOOP(Sh, nb, ne, G) {
+        const int node = base_ + G.r;
+        const bool valid = node < ne;
+        for (int c = A.bs - 1; c >= 0; --c) {
+            const int i = valid ? node * A.bs + c : 0;
+            gs_row<Sh>(A, f, s, i, b0, G.s, true, m, any && valid);
+            if constexpr (LAST) {
+                if (valid && any && G.s == 0) {
+                    double fi[Sh::V], si[Sh::V];
+                    ldv<Sh::V>(fi, f + (size_t)i * A.Bp + b0);
+                    ldv<Sh::V>(si, s + (size_t)i * A.Bp + b0);
+#pragma unroll
+                    for (int v = 0; v < Sh::V; ++v) rs[v] = __dadd_rn(rs[v], __dmul_rn(fi[v], si[v]));
+                }
+            }
+        }
+    }
+    if constexpr (LAST)
+        block_partial<Sh>(rs, part_rs + (size_t)blockIdx.x * A.Bp + blockIdx.y * Sh::T);
+}
+
+// Damped Jacobi sweep, out of place (smoothers.hpp:83-86):
+//   s_out_i = s_i + omega * (f_i - (K s)_i) / d_i ; LAST: partial of f.s_out
+template <class Sh, bool LAST>
+__global__ void __launch_bounds__(kBlock) k_jacobi(Mat A, const double* __restrict__ f,
+                                                   const double* __restrict__ s,
+                                                   double* __restrict__ s_out, const int* active,
+                                                   double omega, double* part_rs) {
+    LaneGeo<Sh> G;
+    const int b0 = blockIdx.y * Sh::T + G.w * Sh::V;
+    bool m[Sh::V], any;
+    lane_mask<Sh>(active, b0, m, any);
+    double rs[Sh::V];
+#pragma unroll
+    for (int v = 0; v < Sh::V; ++v) rs[v] = 0.0;
+    const int nn = A.n / A.bs;
+    P2G_NODE_LOOP(Sh, 0, nn, G) {
+        const int node = base_ + G.r;
+        const bool valid = node < nn;
+        for (int c = 0; c < A.bs; ++c) {
+            const int i = node * A.bs + c;
+            double acc[Sh::V];
+#pragma unroll
+            for (int v = 0; v < Sh::V; ++v) acc[v] = 0.0;
+            if (valid && any) row_dot<Sh>(A, s, b0, __ldg(A.rp + i), __ldg(A.rp + i + 1), G.s, acc);
+#pragma unroll
+            for (int v = 0; v < Sh::V; ++v) acc[v] = slot_sum<Sh>(acc[v]);
+            if (valid && any && G.s == 0) {
+                const size_t o = (size_t)i * A.Bp + b0;
+                double fi[Sh::V], si[Sh::V], d[Sh::V], out[Sh::V];
+                ldv<Sh::V>(fi, f + o);
+                ldv<Sh::V>(si, s + o);
+                ldv<Sh::V>(d, A.vals + (size_t)__ldg(A.dpos + i) * A.Bp + b0);
+#pragma unroll
+                for (int v = 0; v < Sh::V; ++v) {
+                    const double res = __dsub_rn(fi[v], acc[v]);
+                    out[v] = __dadd_rn(si[v], __ddiv_rn(__dmul_rn(omega, res), d[v]));
+                    if (LAST) rs[v] = __dadd_rn(rs[v], __dmul_rn(fi[v], out[v]));
+                }
+                stv<Sh::V>(s_out + o, out, m);
+            }
+        }
+    }
+    if constexpr (LAST)
+        block_partial<Sh>(rs, part_rs + (size_t)blockIdx.x * A.Bp + blockIdx.y * Sh::T);
+}
+
+enum : int { RES_UPPER = 0, RES_FULL = 1, RES_VECTOR = 2 };
+
+// Fused residual + restriction (pod.hpp:198-200: t = f - K s; c = Phi^T t),
+// t never stored.  FORM: RES_FULL  t_i = f_i - sum_j K_ij s_j (reference form)
+//                        RES_UPPER t_i = -sum_{j>i} K_ij s_j (after the first
+//                                  forward sweep from zero, see header)
+//                        RES_VECTOR t_i = f_i (restriction of f itself:
+//                                  reduced_solve's project(f), pod.hpp:171)
+// part[blk][a][b] = sum over the block's rows of phi[i][a] * t_i.
+template <class Sh, int KMAX, int FORM>
+__global__ void __launch_bounds__(kBlock) k_restrict(Mat A, const double* __restrict__ f,
+                                                     const double* __restrict__ s,
+                                                     const double* __restrict__ phi, int k,
+                                                     const int* active, double* part) {
+    LaneGeo<Sh> G;
+    const int b0 = blockIdx.y * Sh::T + G.w * Sh::V;
+    bool m[Sh::V], any;
+    lane_mask<Sh>(active, b0, m, any);
+    double acc[KMAX][Sh::V];
+#pragma unroll
+    for (int a = 0; a < KMAX; ++a)
+#pragma unroll
+        for (int v = 0; v < Sh::V; ++v) acc[a][v] = 0.0;
+    const int nn = A.n / A.bs;
+    P2G_NODE_LOOP(Sh, 0, nn, G) {
+        const int node = base_ + G.r;
+        const bool valid = node < nn;
+        for (int c = 0; c < A.bs; ++c) {
+            const int i = node * A.bs + c;
+            double t[Sh::V];
+#pragma unroll
+            for (int v = 0; v < Sh::V; ++v) t[v] = 0.0;
+            if constexpr (FORM != RES_VECTOR) {
+                if (valid && any) {
+                    const int kb = __ldg(A.rp + i), ke = __ldg(A.rp + i + 1);
+                    if (FORM == RES_UPPER)
+                        row_dot<Sh>(A, s, b0, __ldg(A.dpos + i) + 1, ke, G.s, t);
+                    else
+                        row_dot<Sh>(A, s, b0, kb, ke, G.s, t);
+                }
+#pragma unroll
+                for (int v = 0; v < Sh::V; ++v) t[v] = slot_sum<Sh>(t[v]);
+            }
+            if (valid && any && G.s == 0) {
+                if constexpr (FORM == RES_UPPER) {
+#pragma unroll
+                    for (int v = 0; v < Sh::V; ++v) t[v] = -t[v];
+                } else {
+                    double fi[Sh::V];
+                    ldv<Sh::V>(fi, f + (size_t)i * A.Bp + b0);
+#pragma unroll
+                    for (int v = 0; v < Sh::V; ++v)
+                        t[v] = FORM == RES_FULL ? __dsub_rn(fi[v], t[v]) : fi[v];
+                }
+                const double* ph = phi + (size_t)i * k;
+#pragma unroll
+                for (int a = 0; a < KMAX; ++a) {
+                    if (a < k) {
+                        const double pa = __ldg(ph + a);
+#pragma unroll
+                        for (int v = 0; v < Sh::V; ++v) acc[a][v] = fma(pa, t[v], acc[a][v]);
+                    }
+                }
+            }
+        }
+    }
+    // block reduction in chunks of 8 coefficients (bounded shared memory)
+    __shared__ double sm[kWarps][8][Sh::T];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* prow = part + (size_t)blockIdx.x * k * A.Bp + blockIdx.y * Sh::T;
+#pragma unroll
+    for (int a0 = 0; a0 < KMAX; a0 += 8) {
+        if (a0 >= k) break;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+#pragma unroll
+            for (int v = 0; v < Sh::V; ++v) {
+                const double x = inst_sum<Sh>(acc[a0 + j][v]);
+                if (lane < Sh::W) sm[warp][j][lane * Sh::V + v] = x;
+            }
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < 8 * Sh::T; e += kBlock) {
+            const int j = e / Sh::T, bt = e % Sh::T;
+            if (a0 + j < k) {
+                double tot = 0.0;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) tot += sm[w][j][bt];
+                prow[(size_t)(a0 + j) * A.Bp + bt] = tot;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Coarse correction (pod.hpp:200): c = sum of the restriction partials
+// (fixed order), e = A_c^{-1} c by the Cholesky factor L (lower, row-major
+// [Bp][k][k]).  One block per instance.
+__global__ void __launch_bounds__(kBlock) k_coarse(int Bp, int k, int nblk, const double* part,
+                                                   const double* L, double* e, const int* active) {
+    const int b = blockIdx.x;
+    if (!active[b]) return;
+    __shared__ double c[64];
+    __shared__ double Ls[64 * 64];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int a = warp; a < k; a += kWarps) {
+        double t = 0.0;
+        for (int blk = lane; blk < nblk; blk += 32) t += part[((size_t)blk * k + a) * Bp + b];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) c[a] = t;
+    }
+    const double* Lb = L + (size_t)b * k * k;
+    for (int e2 = threadIdx.x; e2 < k * k; e2 += kBlock) Ls[e2] = Lb[e2];
+    __syncthreads();
+    if (warp == 0) {
+        // forward: L y = c (lane j owns y_j, y_{j+32})
+        double y0 = lane < k ? c[lane] : 0.0, y1 = lane + 32 < k ? c[lane + 32] : 0.0;
+        for (int j = 0; j < k; ++j) {
+            const double yj_owner = (j < 32) ? y0 : y1;
+            double yj = __shfl_sync(0xffffffffu, yj_owner, j & 31);
+            yj = yj / Ls[j * k + j];
+            if (lane == (j & 31)) {
+                if (j < 32) y0 = yj; else y1 = yj;
+            }
+            if (lane > j && lane < k) y0 -= Ls[lane * k + j] * yj;
+            if (lane + 32 > j && lane + 32 < k) y1 -= Ls[(lane + 32) * k + j] * yj;
+        }
+        // backward: L^T x = y
+        for (int j = k - 1; j >= 0; --j) {
+            const double xj_owner = (j < 32) ? y0 : y1;
+            double xj = __shfl_sync(0xffffffffu, xj_owner, j & 31);
+            xj = xj / Ls[j * k + j];
+            if (lane == (j & 31)) {
+                if (j < 32) y0 = xj; else y1 = xj;
+            }
+            if (lane < j) y0 -= Ls[j * k + lane] * xj;
+            if (lane + 32 < j) y1 -= Ls[j * k + lane + 32] * xj;
+        }
+        if (lane < k) e[(size_t)lane * Bp + b] = y0;
+        if (lane + 32 < k) e[(size_t)(lane + 32) * Bp + b] = y1;
+    }
+}
+
+// Prolongation + add (pod.hpp:201-202: corr = lift(e); u += 1.0 * corr), the
+// lift sum in ascending coefficient order like PodBasis::lift (pod.hpp:40-44).
+// ASSIGN: s = corr (reduced_solve's lift into a fresh vector, pod.hpp:178).
+template <class Sh, int KMAX, bool ASSIGN>
+__global__ void __launch_bounds__(kBlock) k_prolong(Mat A, double* s, const double* __restrict__ phi,
+                                                    int k, const double* __restrict__ e,
+                                                    const int* active) {
+    LaneGeo<Sh> G;
+    const int b0 = blockIdx.y * Sh::T + G.w * Sh::V;
+    bool m[Sh::V], any;
+    lane_mask<Sh>(active, b0, m, any);
+    if (!any || G.s != 0) return;
+    double ev[KMAX][Sh::V];
+#pragma unroll
+    for (int a = 0; a < KMAX; ++a)
+        if (a < k) ldv<Sh::V>(ev[a], e + (size_t)a * A.Bp + b0);
+    const int nn = A.n / A.bs;
+    P2G_NODE_LOOP(Sh, 0, nn, G) {
+        const int node = base_ + G.r;
+        if (node >= nn) continue;
+        for (int c = 0; c < A.bs; ++c) {
+            const int i = node * A.bs + c;
+            const double* ph = phi + (size_t)i * k;
+            double corr[Sh::V];
+#pragma unroll
+            for (int v = 0; v < Sh::V; ++v) corr[v] = 0.0;
+#pragma unroll
+            for (int a = 0; a < KMAX; ++a) {
+                if (a < k) {
+                    const double pa = __ldg(ph + a);
+#pragma unroll
+                    for (int v = 0; v < Sh::V; ++v) corr[v] = __dadd_rn(corr[v], __dmul_rn(pa, ev[a][v]));
+                }
+            }
+            const size_t o = (size_t)i * A.Bp + b0;
+            if constexpr (!ASSIGN) {
+                double si[Sh::V];
+                ldv<Sh::V>(si, s + o);
+#pragma unroll
+                for (int v = 0; v < Sh::V; ++v) corr[v] = __dadd_rn(si[v], corr[v]);
+            }
+            stv<Sh::V>(s + o, corr, m);
+        }
+    }
+}
+
+// p = s + beta p (krylov.hpp:282); INIT: p = s (krylov.hpp:263)
+template <class Sh, bool INIT>
+__global__ void __launch_bounds__(kBlock) k_pupdate(int n, int Bp, const double* __restrict__ s,
+                                                    double* __restrict__ p, const double* beta,
+                                                    const int* active) {
+    const int lane = threadIdx.x & 31, w = lane % Sh::W;
+    const int sl = lane / Sh::W;  // remaining lanes stride over rows
+    constexpr int RL = 32 / Sh::W;
+    const int b0 = blockIdx.y * Sh::T + w * Sh::V;
+    bool m[Sh::V], any;
+    lane_mask<Sh>(active, b0, m, any);
+    if (!any) return;
+    double bt[Sh::V];
+#pragma unroll
+    for (int v = 0; v < Sh::V; ++v) bt[v] = INIT ? 0.0 : beta[b0 + v];
+    for (int i = (blockIdx.x * kWarps + (threadIdx.x >> 5)) * RL + sl; i < n;
+         i += gridDim.x * kWarps * RL) {
+        const size_t o = (size_t)i * Bp + b0;
+        double si[Sh::V], pi[Sh::V];
+        ldv<Sh::V>(si, s + o);
+        if constexpr (!INIT) {
+            ldv<Sh::V>(pi, p + o);
+#pragma unroll
+            for (int v = 0; v < Sh::V; ++v) si[v] = __dadd_rn(si[v], __dmul_rn(bt[v], pi[v]));
+        }
+        stv<Sh::V>(p + o, si, m);
+    }
+}
+
+// warp-level fixed-order sum of column b over `rows` partial rows
+__device__ __forceinline__ double warp_col_sum(const double* part, int rows, int Bp, int b) {
+    const int lane = threadIdx.x & 31;
+    double t = 0.0;
+    for (int q = lane; q < rows; q += 32) t += part[(size_t)q * Bp + b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    return t;
+}
+
+// alpha = rs_old / pKp with the pKp <= 0 breakdown (krylov.hpp:273-276)
+__global__ void k_alpha(int Bp, int nrows, const double* part, const double* rs_old,
+                        double* alpha, int* active, int* status) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (b >= Bp) return;
+    if (!active[b]) return;
+    const double pKp = warp_col_sum(part, nrows, Bp, b);
+    if (lane == 0) {
+        if (pKp <= 0.0) {
+            status[b] = ST_EBREAKDOWN;
+            active[b] = 0;
+        } else {
+            alpha[b] = rs_old[b] / pKp;
+        }
+    }
+}
+
+// End of one PCG iteration (krylov.hpp:280-288): rs_new, beta, k++, rel,
+// history, breakdown, convergence; sets the graph's while-condition.
+__global__ void __launch_bounds__(1024) k_finalize(int Bp, int nrs, const double* part_rs,
+                                                   int nrr, const double* part_rr,
+                                                   const double* fnorm, double* rs_old,
+                                                   double* beta, double* rel, int* iters,
+                                                   int* active, int* status, double* hist,
+                                                   const SolveParams* prm,
+                                                   cudaGraphConditionalHandle cond, int set_cond) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    int any = 0;
+    for (int b = warp; b < Bp; b += nw) {
+        if (!active[b]) continue;
+        const double rs_new = warp_col_sum(part_rs, nrs, Bp, b);
+        const double rr = warp_col_sum(part_rr, nrr, Bp, b);
+        if (lane == 0) {
+            const double bt = rs_new / rs_old[b];
+            beta[b] = bt;
+            rs_old[b] = rs_new;
+            const int it = iters[b] + 1;
+            iters[b] = it;
+            const double fn = fnorm[b];
+            const double rn = sqrt(rr);
+            const double rl = fn > 0.0 ? rn / fn : rn;  // krylov.hpp:235-237
+            rel[b] = rl;
+            if (it < prm->hist_cap) hist[(size_t)b * prm->hist_cap + it] = rl;
+            if (rs_new <= 0.0 && rl > prm->tol) {
+                status[b] = ST_EBREAKDOWN;
+                active[b] = 0;
+            } else if (!(rl > prm->tol) || it >= prm->max_iter) {
+                active[b] = 0;
+            } else {
+                any = 1;
+            }
+        }
+    }
+    any = __syncthreads_or(any);
+    if (set_cond && threadIdx.x == 0) cudaGraphSetConditional(cond, any ? 1u : 0u);
+}
+
+// Initial residual bookkeeping (krylov.hpp:252-260): fnorm, rel0, hist[0],
+// the loop-entry test.  Instances with a setup error are not entered.
+__global__ void k_init_rel(int Bp, int B, int nrows, const double* part_rr, const double* part_ff,
+                           double* fnorm, double* rel, int* iters, int* active, int* status,
+                           const int* setup_status, double* hist, const SolveParams* prm) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (b >= Bp) return;
+    const double rr = warp_col_sum(part_rr, nrows, Bp, b);
+    const double ff = warp_col_sum(part_ff, nrows, Bp, b);
+    if (lane == 0) {
+        iters[b] = 0;
+        if (b >= B) {
+            active[b] = 0;
+            status[b] = ST_OK;
+            return;
+        }
+        const double fn = sqrt(ff);
+        const double rn = sqrt(rr);
+        const double rl = fn > 0.0 ? rn / fn : rn;
+        fnorm[b] = fn;
+        rel[b] = rl;
+        if (prm->hist_cap > 0) hist[(size_t)b * prm->hist_cap] = rl;
+        const bool enter = rl > prm->tol && prm->max_iter > 0;
+        status[b] = ST_OK;
+        if (enter && setup_status[b] != ST_OK) {
+            // the reference throws when the preconditioner is first applied
+            status[b] = setup_status[b];
+            active[b] = 0;
+        } else {
+            active[b] = enter ? 1 : 0;
+        }
+    }
+}
+
+// rs_old = r.s after the first preconditioner application (krylov.hpp:262-266)
+__global__ void k_init_rs(int Bp, int nrows, const double* part_rs, double* rs_old, int* active,
+                          int* status) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (b >= Bp || !active[b]) return;
+    const double rs = warp_col_sum(part_rs, nrows, Bp, b);
+    if (lane == 0) {
+        rs_old[b] = rs;
+        if (rs <= 0.0) {
+            status[b] = ST_EBREAKDOWN;
+            active[b] = 0;
+        }
+    }
+}
+
+__global__ void k_set_cond(const int* active, int Bp, cudaGraphConditionalHandle cond) {
+    int any = 0;
+    for (int b = threadIdx.x; b < Bp; b += blockDim.x) any |= active[b];
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) cudaGraphSetConditional(cond, any ? 1u : 0u);
+}
+
+// ---------------------------------------------------------------- layout kernels
+// dst[new][Bp] (b < B) <- src[b][old] with old = map[new] ; padded columns = pad
+__global__ void k_gather_interleave(const double* __restrict__ src, int64_t src_stride, int B,
+                                    const int64_t* __restrict__ map, int64_t nnew,
+                                    double* __restrict__ dst, int Bp, int b_off, double pad) {
+    __shared__ double tile[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    const int64_t j0 = (int64_t)blockIdx.x * 32;
+    const int bb = blockIdx.y * 32;
+    for (int q = ty; q < 32; q += 8) {
+        const int b = bb + q;
+        const int64_t j = j0 + tx;
+        double v = pad;
+        if (j < nnew && b < Bp) {
+            if (b - b_off >= 0 && b - b_off < B) v = src[(int64_t)(b - b_off) * src_stride + map[j]];
+        }
+        tile[q][tx] = v;
+    }
+    __syncthreads();
+    for (int q = ty; q < 32; q += 8) {
+        const int64_t j = j0 + q;
+        const int b = bb + tx;
+        if (j < nnew && b < Bp && b - b_off >= 0 && b - b_off < B) dst[j * Bp + b] = tile[tx][q];
+    }
+}
+
+// dst[b][map[i]] <- src[i][Bp] for b < B (inverse of the above for vectors)
+__global__ void k_scatter_deinterleave(const double* __restrict__ src, int Bp, int64_t n,
+                                       const int64_t* __restrict__ map, int B,
+                                       double* __restrict__ dst) {
+    __shared__ double tile[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t i0 = (int64_t)blockIdx.x * 32;
+    const int bb = blockIdx.y * 32;
+    for (int q = ty; q < 32; q += 8) {
+        const int64_t i = i0 + q;
+        const int b = bb + tx;
+        tile[q][tx] = (i < n && b < Bp) ? src[i * Bp + b] : 0.0;
+    }
+    __syncthreads();
+    for (int q = ty; q < 32; q += 8) {
+        const int b = bb + q;
+        const int64_t i = i0 + tx;
+        if (i < n && b < B) dst[(int64_t)b * n + map[i]] = tile[tx][q];
+    }
+}
+
+// zero diagonal check (smoothers.hpp:41-43) -> setup status
+__global__ void k_check_diag(Mat A, int B, int* status) {
+    const int b = blockIdx.y;
+    if (b >= B) return;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x) {
+        if (A.vals[(size_t)A.dpos[i] * A.Bp + b] == 0.0) status[b] = ST_EZERODIAG;
+    }
+}
+
+// non-finite solution check (krylov.hpp:295) for instances without an error
+__global__ void k_check_finite(int n, int Bp, const double* u, int* status) {
+    const int b = blockIdx.y;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (!isfinite(u[(size_t)i * Bp + b]) && status[b] == ST_OK) status[b] = ST_ENONFINITE;
+    }
+}
+
+// ---------------------------------------------------------------- setup kernels
+// Y[i][a][bt] = sum_j K_ij Phi[j][a] for the instance chunk [bofs, bofs+Bt)
+// (reduced_operator's spmv(K, phi_j), pod.hpp:157, for all k columns at once)
+template <class Sh, int KMAX>
+__global__ void __launch_bounds__(kBlock) k_spmm_phi(Mat A, const double* __restrict__ phi, int k,
+                                                     int bofs, int Bt, double* __restrict__ Y) {
+    LaneGeo<Sh> G;
+    const int bt = blockIdx.y * Sh::T + G.w;  // V == 1 here
+    const int b0 = bofs + bt;
+    const int nn = A.n / A.bs;
+    P2G_NODE_LOOP(Sh, 0, nn, G) {
+        const int node = base_ + G.r;
+        const bool valid = node < nn && bt < Bt;
+        for (int c = 0; c < A.bs; ++c) {
+            const int i = node * A.bs + c;
+            double acc[KMAX];
+#pragma unroll
+            for (int a = 0; a < KMAX; ++a) acc[a] = 0.0;
+            if (valid) {
+                const int kb = __ldg(A.rp + i), ke = __ldg(A.rp + i + 1);
+                for (int q = kb + G.s; q < ke; q += Sh::S) {
+                    const int col = __ldg(A.ci + q);
+                    const double v = __ldcs(A.vals + (size_t)q * A.Bp + b0);
+                    const double* ph = phi + (size_t)col * k;
+#pragma unroll
+                    for (int a = 0; a < KMAX; ++a)
+                        if (a < k) acc[a] = fma(v, __ldg(ph + a), acc[a]);
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < KMAX; ++a) acc[a] = slot_sum<Sh>(acc[a]);
+            if (valid && G.s == 0) {
+                double* y = Y + ((size_t)i * k) * Bt + bt;
+#pragma unroll
+                for (int a = 0; a < KMAX; ++a)
+                    if (a < k) y[(size_t)a * Bt] = acc[a];
+            }
+        }
+    }
+}
+
+// part[blk][a][j] = sum_{i in block rows} phi[i][a] * X[i][j], j < ncol
+template <int KMAX>
+__global__ void __launch_bounds__(kBlock) k_restrict_cols(int n, int ncol, const double* __restrict__ X,
+                                                          const double* __restrict__ phi, int k,
+                                                          double* part) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int j = blockIdx.y * 32 + lane;
+    double acc[KMAX];
+#pragma unroll
+    for (int a = 0; a < KMAX; ++a) acc[a] = 0.0;
+    for (int i = blockIdx.x * kWarps + warp; i < n; i += gridDim.x * kWarps) {
+        const double x = j < ncol ? X[(size_t)i * ncol + j] : 0.0;
+        const double* ph = phi + (size_t)i * k;
+#pragma unroll
+        for (int a = 0; a < KMAX; ++a)
+            if (a < k) acc[a] = fma(__ldg(ph + a), x, acc[a]);
+    }
+    __shared__ double sm[kWarps][8][32];
+#pragma unroll
+    for (int a0 = 0; a0 < KMAX; a0 += 8) {
+        if (a0 >= k) break;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sm[warp][q][lane] = acc[a0 + q];
+        __syncthreads();
+        {
+            const int q = threadIdx.x / 32, l = threadIdx.x % 32;  // 8 x 32
+            const int jj = blockIdx.y * 32 + l;
+            if (a0 + q < k && jj < ncol) {
+                double t = 0.0;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) t += sm[w][q][l];
+                part[((size_t)blockIdx.x * k + a0 + q) * ncol + jj] = t;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Ac[bofs+bt][a][c] = sum_blk part[blk][a][c*Bt+bt]
+__global__ void k_reduce_ac(int nblk, int k, int Bt, int bofs, const double* part, double* Ac) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int e = blockIdx.x * (blockDim.x >> 5) + warp;  // (bt, a, c)
+    const int total = Bt * k * k;
+    if (e >= total) return;
+    const int bt = e / (k * k), a = (e / k) % k, c = e % k;
+    const int ncol = k * Bt;
+    double t = 0.0;
+    for (int blk = lane; blk < nblk; blk += 32) t += part[((size_t)blk * k + a) * ncol + c * Bt + bt];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) Ac[((size_t)(bofs + bt) * k + a) * k + c] = t;
+}
+
+// Cholesky of the symmetrised A_c, one warp per instance (row-major lower L).
+// Singular (dense_solve.hpp:20,25-26 analogue): pivot <= 1e-14 * max|a| or
+// non-positive.
+__global__ void k_cholesky(int B, int k, const double* Ac, double* L, int* status) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (b >= B) return;
+    const double* A = Ac + (size_t)b * k * k;
+    double* Lb = L + (size_t)b * k * k;
+    double mx = 0.0;
+    for (int e = lane; e < k * k; e += 32) mx = fmax(mx, fabs(A[e]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const double floor_ = 1e-14 * mx;
+    for (int e = lane; e < k * k; e += 32) {
+        const int i = e / k, j = e % k;
+        Lb[e] = j <= i ? 0.5 * (A[i * k + j] + A[j * k + i]) : 0.0;
+    }
+    __syncwarp();
+    bool bad = false;
+    for (int j = 0; j < k; ++j) {
+        // L[j][j]
+        double d = Lb[j * k + j];
+        for (int q = 0; q < j; ++q) d -= Lb[j * k + q] * Lb[j * k + q];
+        if (!(d > floor_)) bad = true;
+        const double ljj = sqrt(fmax(d, 1e-300));
+        __syncwarp();
+        for (int i = j + 1 + lane; i < k; i += 32) {
+            double v = Lb[i * k + j];
+            for (int q = 0; q < j; ++q) v -= Lb[i * k + q] * Lb[j * k + q];
+            Lb[i * k + j] = v / ljj;
+        }
+        __syncwarp();
+        if (lane == 0) Lb[j * k + j] = ljj;
+        __syncwarp();
+    }
+    if (lane == 0 && bad && status[b] == ST_OK) status[b] = ST_ESINGULAR;
+}
+
+}  // namespace p2g

@@ -1,0 +1,31 @@
+// p2g_pattern.h -- host-side pattern analysis for the B200 POD-2G path:
+// validation (CsrMatrix::validate, core/csr.hpp:33-46), greedy node colouring
+// and the colour-major permutation the multicolour smoother runs in.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace p2g {
+
+struct ColouredPattern {
+    int64_t n = 0, nnz = 0;
+    int bs = 1;                           // dofs per node
+    int ncolors = 0;
+    std::vector<int64_t> perm;            // new row -> old row
+    std::vector<int64_t> iperm;           // old row -> new row
+    std::vector<int64_t> color_rows;      // ncolors+1 row offsets (new numbering)
+    std::vector<int32_t> rp;              // new CSR row offsets (n+1)
+    std::vector<int32_t> ci;              // new CSR columns (sorted ascending)
+    std::vector<int32_t> dpos;            // new: position of the diagonal in each row
+    std::vector<int64_t> vperm;           // new nnz position -> old nnz position
+};
+
+// Returns "" on success, else the require()-style message.  Validates the
+// reference invariants, the presence of every diagonal, the int32 range, the
+// node blocking (n % bs == 0) and structural symmetry of the node graph.
+std::string build_coloured_pattern(int64_t n, const uint64_t* row_offsets,
+                                   const uint64_t* col_indices, int bs, ColouredPattern& out);
+
+}  // namespace p2g

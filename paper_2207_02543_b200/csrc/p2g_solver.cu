@@ -1,0 +1,1201 @@
+// p2g_solver.cu -- host orchestration and the C-ABI (include/pod2g_b200.h) of
+// the batched POD-2G PCG solve path on B200 (sm_100a).
+//
+// One PCG iteration (krylov.hpp:272-286 with Pod2gPreconditioner::apply,
+// pod.hpp:264-267 -> Pod2gOperator::cycle, pod.hpp:196-207) is the kernel
+// sequence
+//   spmv+dot | alpha | update+pre-smooth(colour 0) | fwd colours 1..C-1 |
+//   residual+restrict | coarse solve | prolong | bwd colours C-1..0 (+r.s) |
+//   finalize (beta, rel, history, convergence) | p-update
+// captured once into a CUDA graph whose body sits in a conditional WHILE node:
+// the loop runs entirely on the device until every instance has converged,
+// broken down or hit max_iter (the finalize kernel sets the condition).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pod2g_b200.h"
+#include "p2g_kernels.cuh"
+#include "p2g_pattern.h"
+
+using namespace p2g;
+
+namespace {
+
+enum Kclass {
+    KC_SPMV = 0,
+    KC_UPDATE,
+    KC_FWD,
+    KC_RESTRICT,
+    KC_COARSE,
+    KC_PROLONG,
+    KC_BWD,
+    KC_REDUCE,
+    KC_PUPDATE
+};
+const char* kKclassNames[P2G_NUM_KCLASS] = {"spmv_dot", "update_presmooth", "gs_forward",
+                                            "residual_restrict", "coarse_solve", "prolong",
+                                            "gs_backward", "scalar_reduce", "p_update"};
+
+enum ShapeId { SH_B1A = 0, SH_B1B, SH_B8, SH_B32, SH_B64 };
+
+}  // namespace
+
+struct p2g_handle {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    std::string err;
+
+    // pattern
+    ColouredPattern pat;
+    bool have_pattern = false;
+    int *d_rp = nullptr, *d_ci = nullptr, *d_dpos = nullptr;
+    int64_t *d_vperm = nullptr, *d_perm = nullptr;
+
+    // batch
+    int B = 0, Bp = 0, shape = SH_B64;
+    double* d_vals = nullptr;
+    bool have_values = false;
+
+    // basis
+    int k = -1;
+    double* d_phi = nullptr;
+
+    // vectors [n][Bp]
+    double *d_u = nullptr, *d_r = nullptr, *d_s = nullptr, *d_s2 = nullptr, *d_p = nullptr,
+           *d_Kp = nullptr, *d_b = nullptr;
+    // per-instance
+    double *d_alpha = nullptr, *d_beta = nullptr, *d_rsold = nullptr, *d_fnorm = nullptr,
+           *d_rel = nullptr, *d_e = nullptr, *d_L = nullptr, *d_Ac = nullptr;
+    int *d_active = nullptr, *d_iters = nullptr, *d_status = nullptr, *d_setup_status = nullptr,
+        *d_all = nullptr;
+    double* d_hist = nullptr;
+    int64_t hist_cap_alloc = 0;
+    SolveParams* d_prm = nullptr;
+    // partials
+    int nb_cap = 0;
+    double *d_part_dot = nullptr, *d_part_rr = nullptr, *d_part_ff = nullptr,
+           *d_part_rs = nullptr, *d_part_c = nullptr;
+    int part_rs_rows = 0;
+    // staging
+    double* d_stage = nullptr;
+    size_t stage_bytes = 0;
+
+    // setup
+    p2g_config cfg{};
+    bool setup_done = false;
+    double* s_final = nullptr;  // buffer holding B r after the post-smoother
+
+    // graph
+    cudaGraphExec_t loop_exec = nullptr;
+    cudaGraphConditionalHandle cond = 0;
+
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    double last_ms[2] = {0, 0};
+    int64_t launches_per_iter = 0, launches_last_solve = 0, launch_counter = 0;
+    // profiling
+    bool profiling = false;
+    cudaEvent_t kev[64];
+    int kev_n = 0;
+    int kev_class[64];
+};
+
+namespace {
+
+#define CU(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess) {                                                          \
+            h->err = std::string(#call) + ": " + cudaGetErrorString(e_);                  \
+            return static_cast<int>(P2G_ECUDA);                                          \
+        }                                                                                 \
+    } while (0)
+
+#define REQ(cond, code, msg)           \
+    do {                                \
+        if (!(cond)) {                  \
+            h->err = (msg);             \
+            return static_cast<int>(code); \
+        }                               \
+    } while (0)
+
+#define TRY(expr)                       \
+    do {                                \
+        int st_ = (expr);               \
+        if (st_ != P2G_OK) return st_;  \
+    } while (0)
+
+template <class T>
+void dfree(T*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+template <class T>
+int dalloc(p2g_handle* h, T*& p, size_t count) {
+    dfree(p);
+    if (count == 0) count = 1;
+    CU(cudaMalloc(&p, count * sizeof(T)));
+    return P2G_OK;
+}
+
+int kbucket(int k) {
+    if (k <= 8) return 8;
+    if (k <= 16) return 16;
+    if (k <= 24) return 24;
+    if (k <= 32) return 32;
+    if (k <= 40) return 40;
+    return 64;
+}
+
+#define KSWITCH(kv, ...)                                            \
+    switch (kbucket(kv)) {                                          \
+        case 8: { constexpr int KM = 8; __VA_ARGS__; } break;      \
+        case 16: { constexpr int KM = 16; __VA_ARGS__; } break;    \
+        case 24: { constexpr int KM = 24; __VA_ARGS__; } break;    \
+        case 32: { constexpr int KM = 32; __VA_ARGS__; } break;    \
+        case 40: { constexpr int KM = 40; __VA_ARGS__; } break;    \
+        default: { constexpr int KM = 64; __VA_ARGS__; } break;    \
+    }
+
+Mat mat_of(p2g_handle* h) {
+    Mat A;
+    A.n = static_cast<int>(h->pat.n);
+    A.bs = h->pat.bs;
+    A.rp = h->d_rp;
+    A.ci = h->d_ci;
+    A.dpos = h->d_dpos;
+    A.vals = h->d_vals;
+    A.Bp = h->Bp;
+    return A;
+}
+
+void count_launch(p2g_handle* h, int kclass) {
+    ++h->launch_counter;
+    if (h->profiling && h->kev_n < 63) {
+        h->kev_class[h->kev_n] = kclass;
+        cudaEventRecord(h->kev[h->kev_n + 1], h->stream);
+        ++h->kev_n;
+    }
+}
+
+// grid for a node-range kernel: one wave of resident blocks at most
+template <class Sh>
+dim3 node_grid(p2g_handle* h, int64_t units, const void* fn) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, 0);
+    occ = std::max(occ, 1);
+    const int64_t need = (units + kWarps * Sh::R - 1) / (kWarps * Sh::R);
+    int64_t gx = std::min<int64_t>(need, (int64_t)h->num_sms * occ);
+    gx = std::max<int64_t>(gx, 1);
+    gx = std::min<int64_t>(gx, h->nb_cap);
+    return dim3(static_cast<unsigned>(gx), static_cast<unsigned>(h->Bp / Sh::T));
+}
+
+// ----------------------------------------------------------------------------
+// Shape-specialised launch sequence
+template <class Sh>
+struct Run {
+    using ASh = typename AccShape<Sh>::type;
+
+    static int nnodes(p2g_handle* h) { return static_cast<int>(h->pat.n / h->pat.bs); }
+
+    static int spmv(p2g_handle* h, const double* x, double* y, bool dot, int* nb_out) {
+        Mat A = mat_of(h);
+        if (dot) {
+            auto fn = k_spmv<Sh, true>;
+            dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn);
+            fn<<<g, kBlock, 0, h->stream>>>(A, x, y, h->d_active, h->d_part_dot);
+            if (nb_out) *nb_out = g.x;
+        } else {
+            auto fn = k_spmv<Sh, false>;
+            dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn);
+            fn<<<g, kBlock, 0, h->stream>>>(A, x, y, h->d_active, nullptr);
+        }
+        count_launch(h, KC_SPMV);
+        CU(cudaGetLastError());
+        return P2G_OK;
+    }
+
+    static int residual(p2g_handle* h, const double* f, const double* u, double* r, int* nb_out) {
+        Mat A = mat_of(h);
+        auto fn = k_residual<Sh>;
+        dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn);
+        fn<<<g, kBlock, 0, h->stream>>>(A, f, u, r, h->d_active, h->d_part_rr, h->d_part_ff);
+        *nb_out = g.x;
+        count_launch(h, KC_SPMV);
+        CU(cudaGetLastError());
+        return P2G_OK;
+    }
+
+    // pre-smoothing (+ optional PCG update) ; returns the row count of the rr partials
+    static int update_pre(p2g_handle* h, bool update, const double* f_r, int* nb_rr) {
+        Mat A = mat_of(h);
+        const int pre = h->cfg.smoother == P2G_SMOOTHER_JACOBI ? PRE_JACOBI : PRE_GS;
+        const int c0 = static_cast<int>(h->pat.color_rows[1] / h->pat.bs);
+        double* r = update ? h->d_r : const_cast<double*>(f_r);
+#define P2G_UP(U, P)                                                                         \
+    {                                                                                        \
+        auto fn = k_update_pre<Sh, U, P>;                                                    \
+        dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn);                               \
+        fn<<<g, kBlock, 0, h->stream>>>(A, h->d_u, r, h->d_p, h->d_Kp, h->d_s, h->d_alpha,   \
+                                        h->d_active, h->d_part_rr, c0, h->cfg.omega);        \
+        if (nb_rr) *nb_rr = g.x;                                                             \
+    }
+        if (update) {
+            if (pre == PRE_GS) P2G_UP(true, PRE_GS) else P2G_UP(true, PRE_JACOBI)
+        } else {
+            if (pre == PRE_GS) P2G_UP(false, PRE_GS) else P2G_UP(false, PRE_JACOBI)
+        }
+#undef P2G_UP
+        count_launch(h, KC_UPDATE);
+        CU(cudaGetLastError());
+        return P2G_OK;
+    }
+
+    static int gs_forward(p2g_handle* h, const double* f, double* s, int c, bool first) {
+        Mat A = mat_of(h);
+        const int nb = static_cast<int>(h->pat.color_rows[c] / h->pat.bs);
+        const int ne = static_cast<int>(h->pat.color_rows[c + 1] / h->pat.bs);
+        if (ne <= nb) return P2G_OK;
+        if (first) {
+            auto fn = k_gs_forward<Sh, true>;
+            dim3 g = node_grid<Sh>(h, ne - nb, (const void*)fn);
+            fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_active, nb, ne);
+        } else {
+            auto fn = k_gs_forward<Sh, false>;
+            dim3 g = node_grid<Sh>(h, ne - nb, (const void*)fn);
+            fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_active, nb, ne);
+        }
+        count_launch(h, KC_FWD);
+        CU(cudaGetLastError());
+        return P2G_OK;
+    }
+
+    static int gs_backward(p2g_handle* h, const double* f, double* s, int c, bool last,
+                           int* rs_row) {
+        Mat A = mat_of(h);
+        const int nb = static_cast<int>(h->pat.color_rows[c] / h->pat.bs);
+        const int ne = static_cast<int>(h->pat.color_rows[c + 1] / h->pat.bs);
+        if (ne <= nb) return P2G_OK;
+        if (last) {
+            auto fn = k_gs_backward<Sh, true>;
+            dim3 g = node_grid<Sh>(h, ne - nb, (const void*)fn);
+            fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_active, nb, ne,
+                                            h->d_part_rs + (size_t)(*rs_row) * h->Bp);
+            *rs_row += g.x;
+        } else {
+            auto fn = k_gs_backward<Sh, false>;
+            dim3 g = node_grid<Sh>(h, ne - nb, (const void*)fn);
+            fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_active, nb, ne, nullptr);
+        }
+        count_launch(h, KC_BWD);
+        CU(cudaGetLastError());
+        return P2G_OK;
+    }
+
+    static int jacobi(p2g_handle* h, const double* f, const double* s, double* s_out, bool last,
+                      int* rs_row, int kclass) {
+        Mat A = mat_of(h);
+        if (last) {
+            auto fn = k_jacobi<Sh, true>;
+            dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn);
+            fn<<<g, kBlock, 0, h->stream>>>(A, f, s, s_out, h->d_active, h->cfg.omega,
+                                            h->d_part_rs + (size_t)(*rs_row) * h->Bp);
+            *rs_row += g.x;
+        } else {
+            auto fn = k_jacobi<Sh, false>;
+            dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn);
+            fn<<<g, kBlock, 0, h->stream>>>(A, f, s, s_out, h->d_active, h->cfg.omega, nullptr);
+        }
+        count_launch(h, kclass);
+        CU(cudaGetLastError());
+        return P2G_OK;
+    }
+
+    static int restrict_(p2g_handle* h, int form, const double* f, const double* s, int* nb_out) {
+        Mat A = mat_of(h);
+        const int k = h->k;
+        KSWITCH(k, {
+            if (form == RES_UPPER) {
+                auto fn = k_restrict<ASh, KM, RES_UPPER>;
+                dim3 g = node_grid<ASh>(h, nnodes(h), (const void*)fn);
+                fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_phi, k, h->d_active, h->d_part_c);
+                *nb_out = g.x;
+            } else if (form == RES_FULL) {
+                auto fn = k_restrict<ASh, KM, RES_FULL>;
+                dim3 g = node_grid<ASh>(h, nnodes(h), (const void*)fn);
+                fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_phi, k, h->d_active, h->d_part_c);
+                *nb_out = g.x;
+            } else {
+                auto fn = k_restrict<ASh, KM, RES_VECTOR>;
+                dim3 g = node_grid<ASh>(h, nnodes(h), (const void*)fn);
+                fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_phi, k, h->d_active, h->d_part_c);
+                *nb_out = g.x;
+            }
+        });
+        count_launch(h, KC_RESTRICT);
+        CU(cudaGetLastError());
+        return P2G_OK;
+    }
+
+    static int coarse(p2g_handle* h, int nblk) {
+        k_coarse<<<h->Bp, kBlock, 0, h->stream>>>(h->Bp, h->k, nblk, h->d_part_c, h->d_L, h->d_e,
+                                                   h->d_active);
+        count_launch(h, KC_COARSE);
+        CU(cudaGetLastError());
+        return P2G_OK;
+    }
+
+    static int prolong(p2g_handle* h, double* s, bool assign) {
+        Mat A = mat_of(h);
+        const int k = h->k;
+        KSWITCH(k, {
+            if (assign) {
+                auto fn = k_prolong<ASh, KM, true>;
+                dim3 g = node_grid<ASh>(h, nnodes(h), (const void*)fn);
+                fn<<<g, kBlock, 0, h->stream>>>(A, s, h->d_phi, k, h->d_e, h->d_active);
+            } else {
+                auto fn = k_prolong<ASh, KM, false>;
+                dim3 g = node_grid<ASh>(h, nnodes(h), (const void*)fn);
+                fn<<<g, kBlock, 0, h->stream>>>(A, s, h->d_phi, k, h->d_e, h->d_active);
+            }
+        });
+        count_launch(h, KC_PROLONG);
+        CU(cudaGetLastError());
+        return P2G_OK;
+    }
+
+    static int pupdate(p2g_handle* h, const double* s, bool init) {
+        const int n = static_cast<int>(h->pat.n);
+        constexpr int RL = 32 / Sh::W;
+        const int64_t need = (n + kWarps * RL - 1) / (kWarps * RL);
+        dim3 g(static_cast<unsigned>(std::min<int64_t>(need, (int64_t)h->num_sms * 8)),
+               h->Bp / Sh::T);
+        if (init)
+            k_pupdate<Sh, true><<<g, kBlock, 0, h->stream>>>(n, h->Bp, s, h->d_p, h->d_beta,
+                                                             h->d_active);
+        else
+            k_pupdate<Sh, false><<<g, kBlock, 0, h->stream>>>(n, h->Bp, s, h->d_p, h->d_beta,
+                                                              h->d_active);
+        count_launch(h, KC_PUPDATE);
+        CU(cudaGetLastError());
+        return P2G_OK;
+    }
+
+    // s = B r, B the POD-2G preconditioner (pod.hpp:264-267).  When `update`,
+    // the PCG update of u and r precedes it in the same kernel (r = d_r).
+    // *rs_rows receives the number of r.s partial rows written (post-smoother).
+    static int precond(p2g_handle* h, bool update, const double* r, int* nb_rr, int* rs_rows) {
+        const p2g_config& cfg = h->cfg;
+        const int C = h->pat.ncolors;
+        const double* rr = update ? h->d_r : r;
+        double* cur = h->d_s;
+        TRY(update_pre(h, update, rr, nb_rr));
+        if (cfg.smoother == P2G_SMOOTHER_GS_MULTICOLOR) {
+            for (int c = 1; c < C; ++c) TRY(gs_forward(h, rr, cur, c, true));
+            for (int sw = 1; sw < cfg.pre_sweeps; ++sw)
+                for (int c = 0; c < C; ++c) TRY(gs_forward(h, rr, cur, c, false));
+        } else {
+            for (int sw = 1; sw < cfg.pre_sweeps; ++sw) {
+                double* nxt = cur == h->d_s ? h->d_s2 : h->d_s;
+                int dummy = 0;
+                TRY(jacobi(h, rr, cur, nxt, false, &dummy, KC_FWD));
+                cur = nxt;
+            }
+        }
+        if (h->k > 0) {
+            const bool upper = cfg.smoother == P2G_SMOOTHER_GS_MULTICOLOR && cfg.pre_sweeps == 1 &&
+                               cfg.residual_form == P2G_RESIDUAL_UPPER;
+            int nbc = 0;
+            TRY(restrict_(h, upper ? RES_UPPER : RES_FULL, rr, cur, &nbc));
+            TRY(coarse(h, nbc));
+            TRY(prolong(h, cur, false));
+        }
+        int rs_row = 0;
+        if (cfg.smoother == P2G_SMOOTHER_GS_MULTICOLOR) {
+            for (int sw = 0; sw < cfg.post_sweeps; ++sw) {
+                const bool last = sw + 1 == cfg.post_sweeps;
+                for (int c = C - 1; c >= 0; --c) TRY(gs_backward(h, rr, cur, c, last, &rs_row));
+            }
+        } else {
+            for (int sw = 0; sw < cfg.post_sweeps; ++sw) {
+                const bool last = sw + 1 == cfg.post_sweeps;
+                double* nxt = cur == h->d_s ? h->d_s2 : h->d_s;
+                TRY(jacobi(h, rr, cur, nxt, last, &rs_row, KC_BWD));
+                cur = nxt;
+            }
+        }
+        h->s_final = cur;
+        if (rs_rows) *rs_rows = rs_row;
+        return P2G_OK;
+    }
+
+    // one PCG iteration (krylov.hpp:272-288)
+    static int iteration(p2g_handle* h, bool in_graph) {
+        int nb_dot = 0, nb_rr = 0, rs_rows = 0;
+        TRY(spmv(h, h->d_p, h->d_Kp, true, &nb_dot));
+        const int wb = 8;  // warps per block for the per-instance reducers
+        k_alpha<<<(h->Bp + wb - 1) / wb, wb * 32, 0, h->stream>>>(h->Bp, nb_dot, h->d_part_dot,
+                                                                  h->d_rsold, h->d_alpha,
+                                                                  h->d_active, h->d_status);
+        count_launch(h, KC_REDUCE);
+        TRY(precond(h, true, nullptr, &nb_rr, &rs_rows));
+        k_finalize<<<1, 1024, 0, h->stream>>>(h->Bp, rs_rows, h->d_part_rs, nb_rr, h->d_part_rr,
+                                              h->d_fnorm, h->d_rsold, h->d_beta, h->d_rel,
+                                              h->d_iters, h->d_active, h->d_status, h->d_hist,
+                                              h->d_prm, h->cond, in_graph ? 1 : 0);
+        count_launch(h, KC_REDUCE);
+        TRY(pupdate(h, h->s_final, false));
+        CU(cudaGetLastError());
+        return P2G_OK;
+    }
+
+    // ---- setup: A_c = Phi^T K Phi per instance, then Cholesky
+    static int coarse_setup(p2g_handle* h) {
+        const int k = h->k;
+        const int n = static_cast<int>(h->pat.n);
+        Mat A = mat_of(h);
+        using MSh = ASh;  // one instance per lane
+        // instance chunk so that Y = n*k*Bt doubles stays below ~4 GiB
+        int Bt = h->Bp;
+        while (Bt > MSh::T && (size_t)n * k * Bt * 8 > ((size_t)4 << 30)) Bt /= 2;
+        Bt = std::max(Bt, MSh::T);
+        double* Y = nullptr;
+        double* part = nullptr;
+        CU(cudaMalloc(&Y, (size_t)n * k * Bt * sizeof(double)));
+        const int ncol = k * Bt;
+        int occ_blocks = h->num_sms * 2;
+        const size_t part_count = (size_t)occ_blocks * k * ncol;
+        if (cudaMalloc(&part, part_count * sizeof(double)) != cudaSuccess) {
+            cudaFree(Y);
+            h->err = "coarse_setup: out of device memory";
+            return P2G_ECUDA;
+        }
+        int st = P2G_OK;
+        for (int bofs = 0; bofs < h->Bp && st == P2G_OK; bofs += Bt) {
+            KSWITCH(k, {
+                auto fn = k_spmm_phi<MSh, KM>;
+                int occ = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, kBlock, 0);
+                occ = std::max(occ, 1);
+                const int64_t need = (n / h->pat.bs + kWarps * MSh::R - 1) / (kWarps * MSh::R);
+                dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)h->num_sms * occ)),
+                       (unsigned)((Bt + MSh::T - 1) / MSh::T));
+                fn<<<g, kBlock, 0, h->stream>>>(A, h->d_phi, k, bofs, Bt, Y);
+                auto fr = k_restrict_cols<KM>;
+                dim3 g2((unsigned)std::min<int64_t>(occ_blocks, (n + kWarps - 1) / kWarps),
+                        (unsigned)((ncol + 31) / 32));
+                fr<<<g2, kBlock, 0, h->stream>>>(n, ncol, Y, h->d_phi, k, part);
+                const int total = Bt * k * k;
+                k_reduce_ac<<<(total + 7) / 8, 256, 0, h->stream>>>(g2.x, k, Bt, bofs, part, h->d_Ac);
+            });
+            if (cudaGetLastError() != cudaSuccess) st = P2G_ECUDA;
+        }
+        cudaStreamSynchronize(h->stream);
+        cudaFree(Y);
+        cudaFree(part);
+        if (st != P2G_OK) {
+            h->err = "coarse_setup: kernel launch failed";
+            return st;
+        }
+        k_cholesky<<<(h->B + 7) / 8, 256, 0, h->stream>>>(h->B, k, h->d_Ac, h->d_L,
+                                                          h->d_setup_status);
+        CU(cudaGetLastError());
+        return P2G_OK;
+    }
+};
+
+template <class F>
+int dispatch(p2g_handle* h, F&& f) {
+    switch (h->shape) {
+        case SH_B1A: return f(Run<ShB1a>{});
+        case SH_B1B: return f(Run<ShB1b>{});
+        case SH_B8: return f(Run<ShB8>{});
+        case SH_B32: return f(Run<ShB32>{});
+        default: return f(Run<ShB64>{});
+    }
+}
+
+// ---------------------------------------------------------------- layout helpers
+// host [B][len] (natural order) -> device [len][Bp] (permuted by map)
+int upload_interleaved(p2g_handle* h, const double* src_host, const double* src_dev, int64_t len,
+                       const int64_t* d_map, double* dst) {
+    const int B = h->B;
+    // instance chunk that fits the staging buffer
+    if (src_dev) {
+        dim3 g((unsigned)((len + 31) / 32), (unsigned)((h->Bp + 31) / 32));
+        k_gather_interleave<<<g, 256, 0, h->stream>>>(src_dev, len, B, d_map, len, dst, h->Bp, 0,
+                                                      0.0);
+        CU(cudaGetLastError());
+        return P2G_OK;
+    }
+    const size_t per = (size_t)len * sizeof(double);
+    size_t want = std::min<size_t>((size_t)B * per, (size_t)1 << 31);
+    want = std::max(want, per);
+    if (h->stage_bytes < want) {
+        dfree(h->d_stage);
+        CU(cudaMalloc(&h->d_stage, want));
+        h->stage_bytes = want;
+    }
+    const int chunk = static_cast<int>(std::max<size_t>(1, h->stage_bytes / per));
+    for (int b0 = 0; b0 < B; b0 += chunk) {
+        const int nb = std::min(chunk, B - b0);
+        CU(cudaMemcpyAsync(h->d_stage, src_host + (size_t)b0 * len, (size_t)nb * per,
+                           cudaMemcpyHostToDevice, h->stream));
+        // rows of this chunk: columns [b0, b0+nb)
+        dim3 g((unsigned)((len + 31) / 32), (unsigned)((h->Bp + 31) / 32));
+        k_gather_interleave<<<g, 256, 0, h->stream>>>(h->d_stage, len, nb, d_map, len, dst, h->Bp,
+                                                      b0, 0.0);
+        CU(cudaGetLastError());
+        CU(cudaStreamSynchronize(h->stream));  // staging buffer reuse
+    }
+    return P2G_OK;
+}
+
+int download_interleaved(p2g_handle* h, const double* src, double* dst_host, double* dst_dev) {
+    const int64_t n = h->pat.n;
+    dim3 g((unsigned)((n + 31) / 32), (unsigned)((h->Bp + 31) / 32));
+    if (dst_dev) {
+        k_scatter_deinterleave<<<g, 256, 0, h->stream>>>(src, h->Bp, n, h->d_perm, h->B, dst_dev);
+        CU(cudaGetLastError());
+        return P2G_OK;
+    }
+    const size_t bytes = (size_t)h->B * n * sizeof(double);
+    if (h->stage_bytes < bytes) {
+        dfree(h->d_stage);
+        CU(cudaMalloc(&h->d_stage, bytes));
+        h->stage_bytes = bytes;
+    }
+    k_scatter_deinterleave<<<g, 256, 0, h->stream>>>(src, h->Bp, n, h->d_perm, h->B, h->d_stage);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(dst_host, h->d_stage, bytes, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    return P2G_OK;
+}
+
+void destroy_graph(p2g_handle* h) {
+    if (h->loop_exec) cudaGraphExecDestroy(h->loop_exec);
+    h->loop_exec = nullptr;
+}
+
+int alloc_batch(p2g_handle* h) {
+    const size_t nv = (size_t)h->pat.n * h->Bp;
+    TRY(dalloc(h, h->d_vals, (size_t)h->pat.nnz * h->Bp));
+    CU(cudaMemsetAsync(h->d_vals, 0, (size_t)h->pat.nnz * h->Bp * sizeof(double), h->stream));
+    for (double** p : {&h->d_u, &h->d_r, &h->d_s, &h->d_s2, &h->d_p, &h->d_Kp, &h->d_b}) {
+        TRY(dalloc(h, *p, nv));
+        CU(cudaMemsetAsync(*p, 0, nv * sizeof(double), h->stream));
+    }
+    for (double** p : {&h->d_alpha, &h->d_beta, &h->d_rsold, &h->d_fnorm, &h->d_rel})
+        TRY(dalloc(h, *p, h->Bp));
+    for (int** p : {&h->d_active, &h->d_iters, &h->d_status, &h->d_setup_status, &h->d_all})
+        TRY(dalloc(h, *p, h->Bp));
+    std::vector<int> ones(h->Bp, 0);
+    for (int b = 0; b < h->B; ++b) ones[b] = 1;
+    CU(cudaMemcpy(h->d_all, ones.data(), sizeof(int) * h->Bp, cudaMemcpyHostToDevice));
+    // partials: up to nb_cap blocks per kernel
+    h->nb_cap = h->num_sms * 8;
+    TRY(dalloc(h, h->d_part_dot, (size_t)h->nb_cap * h->Bp));
+    TRY(dalloc(h, h->d_part_rr, (size_t)h->nb_cap * h->Bp));
+    TRY(dalloc(h, h->d_part_ff, (size_t)h->nb_cap * h->Bp));
+    h->part_rs_rows = h->nb_cap * std::max(1, h->pat.ncolors);
+    TRY(dalloc(h, h->d_part_rs, (size_t)h->part_rs_rows * h->Bp));
+    return P2G_OK;
+}
+
+int choose_shape(p2g_handle* h, int B) {
+    const double avg = (double)h->pat.nnz / (double)h->pat.n;
+    if (B == 1) {
+        h->shape = avg > 32.0 ? SH_B1B : SH_B1A;
+        h->Bp = 1;
+    } else if (B <= 8) {
+        h->shape = SH_B8;
+        h->Bp = 8;
+    } else if (B <= 32) {
+        h->shape = SH_B32;
+        h->Bp = 32;
+    } else {
+        h->shape = SH_B64;
+        h->Bp = (B + 63) / 64 * 64;
+    }
+    return P2G_OK;
+}
+
+int set_values_impl(p2g_handle* h, int32_t batch, const double* host, const double* dev) {
+    REQ(h->have_pattern, P2G_ESTATE, "p2g_set_values: pattern not set");
+    REQ(batch >= 1, P2G_EINVAL, "p2g_set_values: batch must be >= 1");
+    REQ(host || dev, P2G_EINVAL, "p2g_set_values: null values");
+    destroy_graph(h);
+    h->setup_done = false;
+    const int oldBp = h->Bp;
+    const int oldB = h->B;
+    h->B = batch;
+    choose_shape(h, batch);
+    if (h->Bp != oldBp || oldB != batch || !h->d_vals) TRY(alloc_batch(h));
+    if (h->k >= 0) {
+        TRY(dalloc(h, h->d_e, (size_t)std::max(h->k, 1) * h->Bp));
+        TRY(dalloc(h, h->d_L, (size_t)std::max(h->k * h->k, 1) * h->Bp));
+        TRY(dalloc(h, h->d_Ac, (size_t)std::max(h->k * h->k, 1) * h->Bp));
+        TRY(dalloc(h, h->d_part_c, (size_t)h->nb_cap * std::max(h->k, 1) * h->Bp));
+    }
+    TRY(upload_interleaved(h, host, dev, h->pat.nnz, h->d_vperm, h->d_vals));
+    CU(cudaStreamSynchronize(h->stream));
+    h->have_values = true;
+    return P2G_OK;
+}
+
+int build_loop_graph(p2g_handle* h) {
+    destroy_graph(h);
+    cudaGraph_t outer = nullptr;
+    CU(cudaGraphCreate(&outer, 0));
+    cudaGraphConditionalHandle cond;
+    CU(cudaGraphConditionalHandleCreate(&cond, outer, 0, 0));
+    h->cond = cond;
+    // upstream kernel: condition := any instance active
+    cudaKernelNodeParams kp = {};
+    int Bp = h->Bp;
+    int* act = h->d_active;
+    void* args[] = {&act, &Bp, &cond};
+    kp.func = (void*)k_set_cond;
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(256);
+    kp.sharedMemBytes = 0;
+    kp.kernelParams = args;
+    cudaGraphNode_t setn;
+    CU(cudaGraphAddKernelNode(&setn, outer, nullptr, 0, &kp));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    CU(cudaGraphAddNode(&wnode, outer, &setn, 1, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CU(cudaStreamBeginCaptureToGraph(h->stream, body, nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeRelaxed));
+    const int64_t before = h->launch_counter;
+    int st = dispatch(h, [&](auto R) -> int { return decltype(R)::iteration(h, true); });
+    cudaGraph_t captured = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(h->stream, &captured);
+    if (st != P2G_OK) {
+        cudaGraphDestroy(outer);
+        return st;
+    }
+    if (ce != cudaSuccess) {
+        cudaGraphDestroy(outer);
+        h->err = std::string("graph capture: ") + cudaGetErrorString(ce);
+        return P2G_ECUDA;
+    }
+    h->launches_per_iter = h->launch_counter - before;
+    cudaError_t ie = cudaGraphInstantiate(&h->loop_exec, outer, 0);
+    cudaGraphDestroy(outer);
+    if (ie != cudaSuccess) {
+        h->err = std::string("graph instantiate: ") + cudaGetErrorString(ie);
+        return P2G_ECUDA;
+    }
+    return P2G_OK;
+}
+
+int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const double* x0_host,
+               const double* x0_dev, int32_t x0_mode, double tol, int64_t max_iter,
+               double* x_host, double* x_dev, int64_t* iters, int32_t* converged, int32_t* status,
+               double* hist, int64_t hist_cap) {
+    REQ(h->setup_done, P2G_ESTATE, "p2g_solve: p2g_setup not called");
+    REQ(b_host || b_dev, P2G_EINVAL, "p2g_solve: null right-hand side");
+    REQ(x0_mode >= 0 && x0_mode <= 2, P2G_EINVAL, "p2g_solve: bad x0_mode");
+    REQ(x0_mode != P2G_X0_GIVEN || x0_host || x0_dev, P2G_EINVAL, "p2g_solve: null x0");
+    REQ(x0_mode != P2G_X0_REDUCED || h->k > 0, P2G_EINVAL,
+        "p2g_solve: reduced initial guess needs a basis");
+    REQ(max_iter >= 0 && hist_cap >= 0, P2G_EINVAL, "p2g_solve: negative max_iter/hist_cap");
+    const int64_t cap_dev = std::max<int64_t>(hist_cap, 1);
+    if (cap_dev > h->hist_cap_alloc || !h->d_hist) {
+        TRY(dalloc(h, h->d_hist, (size_t)cap_dev * h->Bp));
+        h->hist_cap_alloc = cap_dev;
+    }
+    if (!h->loop_exec) TRY(build_loop_graph(h));
+    const int64_t lc0 = h->launch_counter;
+    SolveParams prm{tol, (long long)max_iter, (long long)hist_cap};
+    CU(cudaMemcpyAsync(h->d_prm, &prm, sizeof(prm), cudaMemcpyHostToDevice, h->stream));
+
+    // inputs: b, x0 (H2D inside the caller's timed region for e2e)
+    CU(cudaEventRecord(h->ev[0], h->stream));
+    TRY(upload_interleaved(h, b_host, b_dev, h->pat.n, h->d_perm, h->d_b));
+    CU(cudaMemcpyAsync(h->d_active, h->d_all, sizeof(int) * h->Bp, cudaMemcpyDeviceToDevice,
+                       h->stream));
+    int st = dispatch(h, [&](auto R) -> int {
+        using Rn = decltype(R);
+        if (x0_mode == P2G_X0_GIVEN) {
+            TRY(upload_interleaved(h, x0_host, x0_dev, h->pat.n, h->d_perm, h->d_u));
+        } else if (x0_mode == P2G_X0_REDUCED) {
+            int nbc = 0;
+            TRY(Rn::restrict_(h, RES_VECTOR, h->d_b, nullptr, &nbc));
+            TRY(Rn::coarse(h, nbc));
+            TRY(Rn::prolong(h, h->d_u, true));
+        } else {
+            CU(cudaMemsetAsync(h->d_u, 0, (size_t)h->pat.n * h->Bp * sizeof(double), h->stream));
+        }
+        int nb = 0;
+        TRY(Rn::residual(h, h->d_b, h->d_u, h->d_r, &nb));
+        k_init_rel<<<(h->Bp + 7) / 8, 256, 0, h->stream>>>(
+            h->Bp, h->B, nb, h->d_part_rr, h->d_part_ff, h->d_fnorm, h->d_rel, h->d_iters,
+            h->d_active, h->d_status, h->d_setup_status, h->d_hist, h->d_prm);
+        count_launch(h, KC_REDUCE);
+        // s = T r0 ; rs_old = r.s ; p = s   (krylov.hpp:262-266)
+        int rs_rows = 0;
+        TRY(Rn::precond(h, false, h->d_r, nullptr, &rs_rows));
+        k_init_rs<<<(h->Bp + 7) / 8, 256, 0, h->stream>>>(h->Bp, rs_rows, h->d_part_rs,
+                                                           h->d_rsold, h->d_active, h->d_status);
+        count_launch(h, KC_REDUCE);
+        TRY(Rn::pupdate(h, h->s_final, true));
+        return P2G_OK;
+    });
+    if (st != P2G_OK) return st;
+    CU(cudaEventRecord(h->ev[1], h->stream));
+    CU(cudaGraphLaunch(h->loop_exec, h->stream));
+    CU(cudaEventRecord(h->ev[2], h->stream));
+    {
+        const dim3 g((unsigned)std::min<int64_t>((h->pat.n + 255) / 256, 1024), h->B);
+        k_check_finite<<<g, 256, 0, h->stream>>>(static_cast<int>(h->pat.n), h->Bp, h->d_u,
+                                                  h->d_status);
+        CU(cudaGetLastError());
+    }
+    if (x_host || x_dev) TRY(download_interleaved(h, h->d_u, x_host, x_dev));
+    CU(cudaEventRecord(h->ev[3], h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    std::vector<int> it(h->Bp), stt(h->Bp);
+    std::vector<double> rel(h->Bp);
+    CU(cudaMemcpy(it.data(), h->d_iters, sizeof(int) * h->Bp, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(stt.data(), h->d_status, sizeof(int) * h->Bp, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(rel.data(), h->d_rel, sizeof(double) * h->Bp, cudaMemcpyDeviceToHost));
+    int worst = P2G_OK;
+    for (int b = 0; b < h->B; ++b) {
+        if (iters) iters[b] = it[b];
+        if (converged) converged[b] = rel[b] <= tol ? 1 : 0;
+        if (status) status[b] = stt[b];
+        if (stt[b] != P2G_OK) worst = stt[b];
+    }
+    if (hist && hist_cap > 0) {
+        CU(cudaMemcpy(hist, h->d_hist, sizeof(double) * hist_cap * h->B,
+                      cudaMemcpyDeviceToHost));
+        for (int b = 0; b < h->B; ++b) {
+            const int64_t len = std::min<int64_t>(it[b] + 1, hist_cap);
+            for (int64_t q = len; q < hist_cap; ++q) hist[b * hist_cap + q] = NAN;
+        }
+    }
+    float ms_all = 0, ms_loop = 0;
+    cudaEventElapsedTime(&ms_all, h->ev[0], h->ev[3]);
+    cudaEventElapsedTime(&ms_loop, h->ev[1], h->ev[2]);
+    h->last_ms[0] = ms_all;
+    h->last_ms[1] = ms_loop;
+    int64_t maxit = 0;
+    for (int b = 0; b < h->B; ++b) maxit = std::max<int64_t>(maxit, it[b]);
+    h->launches_last_solve = (h->launch_counter - lc0) + 1 /*set_cond*/ +
+                             maxit * h->launches_per_iter + 1 /*finite*/ + 1 /*download*/;
+    if (worst != P2G_OK) h->err = "p2g_solve: at least one instance failed (see status)";
+    return worst;
+}
+
+}  // namespace
+
+// ============================================================================ C-ABI
+extern "C" {
+
+void p2g_config_default(p2g_config* cfg) {
+    if (!cfg) return;
+    cfg->smoother = P2G_SMOOTHER_GS_MULTICOLOR;
+    cfg->pre_sweeps = 1;
+    cfg->post_sweeps = 1;
+    cfg->residual_form = P2G_RESIDUAL_UPPER;
+    cfg->omega = 0.5;
+}
+
+int p2g_abi_version(void) { return P2G_ABI_VERSION; }
+
+const char* p2g_status_string(int s) {
+    switch (s) {
+        case P2G_OK: return "ok";
+        case P2G_EINVAL: return "invalid argument";
+        case P2G_EBREAKDOWN: return "PCG breakdown (preconditioner or matrix not SPD)";
+        case P2G_ENONFINITE: return "non-finite entries in solution";
+        case P2G_ESINGULAR: return "coarse operator singular";
+        case P2G_EZERODIAG: return "zero diagonal";
+        case P2G_ECUDA: return "CUDA error";
+        case P2G_ENCCL: return "NCCL error";
+        case P2G_ESTATE: return "call order violated";
+        default: return "unknown";
+    }
+}
+
+int p2g_create(int device, p2g_handle** out) {
+    if (!out) return P2G_EINVAL;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return P2G_ECUDA;
+    if (device < 0 || device >= ndev) return P2G_EINVAL;
+    if (cudaSetDevice(device) != cudaSuccess) return P2G_ECUDA;
+    p2g_handle* h = new p2g_handle();
+    h->device = device;
+    cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete h;
+        return P2G_ECUDA;
+    }
+    for (auto& e : h->ev) cudaEventCreate(&e);
+    for (auto& e : h->kev) cudaEventCreate(&e);
+    if (cudaMalloc(&h->d_prm, sizeof(SolveParams)) != cudaSuccess) {
+        delete h;
+        return P2G_ECUDA;
+    }
+    p2g_config_default(&h->cfg);
+    *out = h;
+    return P2G_OK;
+}
+
+int p2g_destroy(p2g_handle* h) {
+    if (!h) return P2G_EINVAL;
+    cudaSetDevice(h->device);
+    cudaStreamSynchronize(h->stream);
+    destroy_graph(h);
+    dfree(h->d_rp);
+    dfree(h->d_ci);
+    dfree(h->d_dpos);
+    dfree(h->d_vperm);
+    dfree(h->d_perm);
+    dfree(h->d_vals);
+    dfree(h->d_phi);
+    for (double** p : {&h->d_u, &h->d_r, &h->d_s, &h->d_s2, &h->d_p, &h->d_Kp, &h->d_b, &h->d_alpha,
+                       &h->d_beta, &h->d_rsold, &h->d_fnorm, &h->d_rel, &h->d_e, &h->d_L, &h->d_Ac,
+                       &h->d_hist, &h->d_part_dot, &h->d_part_rr, &h->d_part_ff, &h->d_part_rs,
+                       &h->d_part_c, &h->d_stage})
+        dfree(*p);
+    for (int** p : {&h->d_active, &h->d_iters, &h->d_status, &h->d_setup_status, &h->d_all})
+        dfree(*p);
+    dfree(h->d_prm);
+    for (auto& e : h->ev) cudaEventDestroy(e);
+    for (auto& e : h->kev) cudaEventDestroy(e);
+    cudaStreamDestroy(h->stream);
+    delete h;
+    return P2G_OK;
+}
+
+const char* p2g_last_error(const p2g_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+int p2g_set_pattern(p2g_handle* h, int64_t n, const uint64_t* row_offsets,
+                    const uint64_t* col_indices, int32_t block_size) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    ColouredPattern pat;
+    const std::string msg = build_coloured_pattern(n, row_offsets, col_indices, block_size, pat);
+    REQ(msg.empty(), P2G_EINVAL, msg);
+    destroy_graph(h);
+    h->pat = std::move(pat);
+    h->have_pattern = true;
+    h->have_values = false;
+    h->setup_done = false;
+    h->B = 0;
+    h->Bp = 0;
+    h->k = -1;
+    dfree(h->d_vals);
+    TRY(dalloc(h, h->d_rp, h->pat.rp.size()));
+    TRY(dalloc(h, h->d_ci, h->pat.ci.size()));
+    TRY(dalloc(h, h->d_dpos, h->pat.dpos.size()));
+    TRY(dalloc(h, h->d_vperm, h->pat.vperm.size()));
+    TRY(dalloc(h, h->d_perm, h->pat.perm.size()));
+    CU(cudaMemcpy(h->d_rp, h->pat.rp.data(), sizeof(int) * h->pat.rp.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_ci, h->pat.ci.data(), sizeof(int) * h->pat.ci.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_dpos, h->pat.dpos.data(), sizeof(int) * h->pat.dpos.size(),
+                  cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_vperm, h->pat.vperm.data(), sizeof(int64_t) * h->pat.vperm.size(),
+                  cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_perm, h->pat.perm.data(), sizeof(int64_t) * h->pat.perm.size(),
+                  cudaMemcpyHostToDevice));
+    return P2G_OK;
+}
+
+int p2g_set_values(p2g_handle* h, int32_t batch, const double* values) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    return set_values_impl(h, batch, values, nullptr);
+}
+
+int p2g_set_values_device(p2g_handle* h, int32_t batch, const double* d_values) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    return set_values_impl(h, batch, nullptr, d_values);
+}
+
+int p2g_set_basis(p2g_handle* h, int32_t k, const double* phi) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    REQ(h->have_pattern, P2G_ESTATE, "p2g_set_basis: pattern not set");
+    REQ(k >= 0 && k <= 64, P2G_EINVAL, "p2g_set_basis: rank must lie in [0, 64]");
+    REQ(k == 0 || phi, P2G_EINVAL, "p2g_set_basis: null basis");
+    destroy_graph(h);
+    h->setup_done = false;
+    h->k = k;
+    const int64_t n = h->pat.n;
+    std::vector<double> perm_phi((size_t)n * std::max(k, 1), 0.0);
+    for (int64_t i = 0; i < n; ++i)
+        for (int a = 0; a < k; ++a) perm_phi[i * k + a] = phi[h->pat.perm[i] * k + a];
+    TRY(dalloc(h, h->d_phi, perm_phi.size()));
+    CU(cudaMemcpy(h->d_phi, perm_phi.data(), sizeof(double) * perm_phi.size(),
+                  cudaMemcpyHostToDevice));
+    if (h->Bp > 0) {
+        TRY(dalloc(h, h->d_e, (size_t)std::max(k, 1) * h->Bp));
+        TRY(dalloc(h, h->d_L, (size_t)std::max(k * k, 1) * h->Bp));
+        TRY(dalloc(h, h->d_Ac, (size_t)std::max(k * k, 1) * h->Bp));
+        TRY(dalloc(h, h->d_part_c, (size_t)h->nb_cap * std::max(k, 1) * h->Bp));
+    }
+    return P2G_OK;
+}
+
+int p2g_setup(p2g_handle* h, const p2g_config* cfg, int32_t* status) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    REQ(h->have_values, P2G_ESTATE, "p2g_setup: values not set");
+    REQ(h->k >= 0, P2G_ESTATE, "p2g_setup: basis not set");
+    p2g_config c;
+    if (cfg) c = *cfg; else p2g_config_default(&c);
+    REQ(c.smoother == P2G_SMOOTHER_GS_MULTICOLOR || c.smoother == P2G_SMOOTHER_JACOBI, P2G_EINVAL,
+        "p2g_setup: unknown smoother");
+    REQ(c.pre_sweeps >= 1 && c.post_sweeps >= 1 && c.pre_sweeps <= 16 && c.post_sweeps <= 16,
+        P2G_EINVAL, "p2g_setup: sweeps must lie in [1,16]");
+    REQ(c.smoother != P2G_SMOOTHER_JACOBI || (c.omega > 0.0 && c.omega <= 1.0), P2G_EINVAL,
+        "jacobi_sweep: omega outside (0,1]");
+    REQ(c.residual_form == P2G_RESIDUAL_FULL || c.residual_form == P2G_RESIDUAL_UPPER, P2G_EINVAL,
+        "p2g_setup: unknown residual form");
+    destroy_graph(h);
+    h->cfg = c;
+    CU(cudaMemsetAsync(h->d_setup_status, 0, sizeof(int) * h->Bp, h->stream));
+    {
+        Mat A = mat_of(h);
+        dim3 g(std::max(1, std::min(1024, (int)((h->pat.n + 255) / 256))), h->B);
+        k_check_diag<<<g, 256, 0, h->stream>>>(A, h->B, h->d_setup_status);
+        CU(cudaGetLastError());
+    }
+    if (h->k > 0) TRY(dispatch(h, [&](auto R) -> int { return decltype(R)::coarse_setup(h); }));
+    CU(cudaStreamSynchronize(h->stream));
+    std::vector<int> st(h->Bp);
+    CU(cudaMemcpy(st.data(), h->d_setup_status, sizeof(int) * h->Bp, cudaMemcpyDeviceToHost));
+    int worst = P2G_OK;
+    for (int b = 0; b < h->B; ++b) {
+        if (status) status[b] = st[b];
+        if (st[b] != P2G_OK) worst = st[b];
+    }
+    h->setup_done = true;
+    if (worst != P2G_OK) h->err = "p2g_setup: at least one instance failed (see status)";
+    return worst;
+}
+
+int p2g_initial_guess(p2g_handle* h, const double* b, double* x0) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    REQ(h->setup_done, P2G_ESTATE, "p2g_initial_guess: p2g_setup not called");
+    REQ(h->k > 0, P2G_EINVAL, "reduced_solve: basis has rank 0");
+    REQ(b && x0, P2G_EINVAL, "p2g_initial_guess: null argument");
+    TRY(upload_interleaved(h, b, nullptr, h->pat.n, h->d_perm, h->d_b));
+    CU(cudaMemcpyAsync(h->d_active, h->d_all, sizeof(int) * h->Bp, cudaMemcpyDeviceToDevice,
+                       h->stream));
+    TRY(dispatch(h, [&](auto R) -> int {
+        using Rn = decltype(R);
+        int nbc = 0;
+        TRY(Rn::restrict_(h, RES_VECTOR, h->d_b, nullptr, &nbc));
+        TRY(Rn::coarse(h, nbc));
+        TRY(Rn::prolong(h, h->d_u, true));
+        return P2G_OK;
+    }));
+    TRY(download_interleaved(h, h->d_u, x0, nullptr));
+    return P2G_OK;
+}
+
+int p2g_solve(p2g_handle* h, const double* b, const double* x0, int32_t x0_mode, double tol,
+              int64_t max_iter, double* x, int64_t* iters, int32_t* converged, int32_t* status,
+              double* hist, int64_t hist_cap) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    return solve_impl(h, b, nullptr, x0, nullptr, x0_mode, tol, max_iter, x, nullptr, iters,
+                      converged, status, hist, hist_cap);
+}
+
+int p2g_solve_device(p2g_handle* h, const double* d_b, const double* d_x0, int32_t x0_mode,
+                     double tol, int64_t max_iter, double* d_x, int64_t* iters,
+                     int32_t* converged, int32_t* status, double* hist, int64_t hist_cap) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    return solve_impl(h, nullptr, d_b, nullptr, d_x0, x0_mode, tol, max_iter, nullptr, d_x, iters,
+                      converged, status, hist, hist_cap);
+}
+
+int p2g_last_solve_ms(const p2g_handle* h, double* ms2) {
+    if (!h || !ms2) return P2G_EINVAL;
+    ms2[0] = h->last_ms[0];
+    ms2[1] = h->last_ms[1];
+    return P2G_OK;
+}
+
+int p2g_spmv(p2g_handle* h, const double* x, double* y) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    REQ(h->have_values, P2G_ESTATE, "p2g_spmv: values not set");
+    REQ(x && y, P2G_EINVAL, "p2g_spmv: null argument");
+    TRY(upload_interleaved(h, x, nullptr, h->pat.n, h->d_perm, h->d_p));
+    CU(cudaMemcpyAsync(h->d_active, h->d_all, sizeof(int) * h->Bp, cudaMemcpyDeviceToDevice,
+                       h->stream));
+    TRY(dispatch(h, [&](auto R) -> int { return decltype(R)::spmv(h, h->d_p, h->d_Kp, false, nullptr); }));
+    TRY(download_interleaved(h, h->d_Kp, y, nullptr));
+    return P2G_OK;
+}
+
+int p2g_precond_apply(p2g_handle* h, const double* r, double* s) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    REQ(h->setup_done, P2G_ESTATE, "p2g_precond_apply: p2g_setup not called");
+    REQ(r && s, P2G_EINVAL, "p2g_precond_apply: null argument");
+    TRY(upload_interleaved(h, r, nullptr, h->pat.n, h->d_perm, h->d_r));
+    CU(cudaMemcpyAsync(h->d_active, h->d_all, sizeof(int) * h->Bp, cudaMemcpyDeviceToDevice,
+                       h->stream));
+    TRY(dispatch(h, [&](auto R) -> int { return decltype(R)::precond(h, false, h->d_r, nullptr, nullptr); }));
+    TRY(download_interleaved(h, h->s_final, s, nullptr));
+    return P2G_OK;
+}
+
+int p2g_smooth(p2g_handle* h, int32_t direction, const double* f, double* u) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    REQ(h->have_values, P2G_ESTATE, "p2g_smooth: values not set");
+    REQ(f && u, P2G_EINVAL, "p2g_smooth: null argument");
+    REQ(direction == 0 || direction == 1, P2G_EINVAL, "p2g_smooth: direction must be 0 or 1");
+    TRY(upload_interleaved(h, f, nullptr, h->pat.n, h->d_perm, h->d_r));
+    TRY(upload_interleaved(h, u, nullptr, h->pat.n, h->d_perm, h->d_s));
+    CU(cudaMemcpyAsync(h->d_active, h->d_all, sizeof(int) * h->Bp, cudaMemcpyDeviceToDevice,
+                       h->stream));
+    double* out = h->d_s;
+    TRY(dispatch(h, [&](auto R) -> int {
+        using Rn = decltype(R);
+        const int C = h->pat.ncolors;
+        if (h->cfg.smoother == P2G_SMOOTHER_JACOBI) {
+            int dummy = 0;
+            TRY(Rn::jacobi(h, h->d_r, h->d_s, h->d_s2, false, &dummy, KC_FWD));
+            out = h->d_s2;
+        } else if (direction == 0) {
+            for (int c = 0; c < C; ++c) TRY(Rn::gs_forward(h, h->d_r, h->d_s, c, false));
+        } else {
+            int row = 0;
+            for (int c = C - 1; c >= 0; --c) TRY(Rn::gs_backward(h, h->d_r, h->d_s, c, false, &row));
+        }
+        return P2G_OK;
+    }));
+    TRY(download_interleaved(h, out, u, nullptr));
+    return P2G_OK;
+}
+
+int p2g_coarse_operator(p2g_handle* h, double* Ac) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    REQ(h->setup_done && h->k > 0, P2G_ESTATE, "p2g_coarse_operator: no coarse operator");
+    REQ(Ac, P2G_EINVAL, "p2g_coarse_operator: null argument");
+    CU(cudaMemcpy(Ac, h->d_Ac, sizeof(double) * h->k * h->k * h->B, cudaMemcpyDeviceToHost));
+    return P2G_OK;
+}
+
+int p2g_get_permutation(p2g_handle* h, int64_t* perm, int32_t* ncolors, int64_t* color_offsets,
+                        int32_t cap) {
+    if (!h) return P2G_EINVAL;
+    REQ(h->have_pattern, P2G_ESTATE, "p2g_get_permutation: pattern not set");
+    if (perm) std::memcpy(perm, h->pat.perm.data(), sizeof(int64_t) * h->pat.n);
+    if (ncolors) *ncolors = h->pat.ncolors;
+    if (color_offsets)
+        for (int c = 0; c <= h->pat.ncolors && c < cap; ++c) color_offsets[c] = h->pat.color_rows[c];
+    return P2G_OK;
+}
+
+int p2g_analyze_pattern(int64_t n, const uint64_t* row_offsets, const uint64_t* col_indices,
+                        int32_t block_size, int64_t* perm, int32_t* ncolors,
+                        int64_t* color_offsets, int32_t cap, char* errbuf, int32_t errcap) {
+    ColouredPattern pat;
+    const std::string msg = build_coloured_pattern(n, row_offsets, col_indices, block_size, pat);
+    if (!msg.empty()) {
+        if (errbuf && errcap > 0) {
+            std::strncpy(errbuf, msg.c_str(), errcap - 1);
+            errbuf[errcap - 1] = 0;
+        }
+        return P2G_EINVAL;
+    }
+    if (perm) std::memcpy(perm, pat.perm.data(), sizeof(int64_t) * n);
+    if (ncolors) *ncolors = pat.ncolors;
+    if (color_offsets)
+        for (int c = 0; c <= pat.ncolors && c < cap; ++c) color_offsets[c] = pat.color_rows[c];
+    return P2G_OK;
+}
+
+int p2g_profile_iteration(p2g_handle* h, int32_t reps, double* ms, double* bytes,
+                          const char** names) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    REQ(h->setup_done, P2G_ESTATE, "p2g_profile_iteration: p2g_setup not called");
+    REQ(reps >= 1, P2G_EINVAL, "p2g_profile_iteration: reps >= 1");
+    std::vector<double> acc(P2G_NUM_KCLASS, 0.0);
+    // every instance active: time the full batch (state is scratch)
+    for (int rep = 0; rep < reps; ++rep) {
+        CU(cudaMemcpyAsync(h->d_active, h->d_all, sizeof(int) * h->Bp, cudaMemcpyDeviceToDevice,
+                           h->stream));
+        h->profiling = true;
+        h->kev_n = 0;
+        CU(cudaEventRecord(h->kev[0], h->stream));
+        int st = dispatch(h, [&](auto R) -> int { return decltype(R)::iteration(h, false); });
+        h->profiling = false;
+        TRY(st);
+        CU(cudaStreamSynchronize(h->stream));
+        for (int q = 0; q < h->kev_n; ++q) {
+            float t = 0;
+            cudaEventElapsedTime(&t, h->kev[q], h->kev[q + 1]);
+            acc[h->kev_class[q]] += t;
+        }
+    }
+    // algorithmic bytes per iteration per class:
+    const double n = (double)h->pat.n, z = (double)h->pat.nnz, Bp = (double)h->B;
+    const double k = (double)std::max(h->k, 0);
+    const double idx = 4.0 * z + 4.0 * (n + 1);    // shared pattern, once per batch
+    const double Mv = 8.0 * z * Bp;                // values, one pass
+    const double C = h->pat.ncolors;
+    double by[P2G_NUM_KCLASS] = {0};
+    // lower/upper halves of the values (strict), diagonal
+    const double zl = 0.5 * (z - n);
+    const bool gs = h->cfg.smoother == P2G_SMOOTHER_GS_MULTICOLOR;
+    by[KC_SPMV] = Mv + idx + 16.0 * n * Bp;                    // vals, x once, y
+    by[KC_UPDATE] = 48.0 * n * Bp + (gs ? 0.0 : 24.0 * n * Bp);  // u,p,r,Kp r/w (+ s,d for Jacobi)
+    by[KC_FWD] = gs ? (8.0 * (zl + n) * Bp + 4.0 * (zl + n) + 4.0 * n + 24.0 * n * Bp * (C - 1) / C)
+                    : 0.0;
+    by[KC_RESTRICT] = (gs && h->cfg.residual_form == P2G_RESIDUAL_UPPER && h->cfg.pre_sweeps == 1
+                           ? 8.0 * zl * Bp + 4.0 * zl + 4.0 * n
+                           : Mv + idx + 8.0 * n * Bp) +
+                      8.0 * n * Bp + 8.0 * n * k;
+    by[KC_COARSE] = 0.0;
+    by[KC_PROLONG] = 16.0 * n * Bp + 8.0 * n * k;
+    by[KC_BWD] = Mv + idx + 24.0 * n * Bp;
+    by[KC_REDUCE] = 0.0;
+    by[KC_PUPDATE] = 24.0 * n * Bp;
+    if (h->k == 0) by[KC_RESTRICT] = by[KC_PROLONG] = 0.0;
+    for (int q = 0; q < P2G_NUM_KCLASS; ++q) {
+        if (ms) ms[q] = acc[q] / reps;
+        if (bytes) bytes[q] = by[q];
+        if (names) names[q] = kKclassNames[q];
+    }
+    return P2G_OK;
+}
+
+int p2g_launch_counts(const p2g_handle* h, int64_t* per_iteration, int64_t* last_solve_total) {
+    if (!h) return P2G_EINVAL;
+    if (per_iteration) *per_iteration = h->launches_per_iter;
+    if (last_solve_total) *last_solve_total = h->launches_last_solve;
+    return P2G_OK;
+}
+
+}  // extern "C"
