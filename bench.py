@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""bench.py -- PCG+POD-2G converged solves/s (fp64) on B200.
+
+Workload (BASELINE.json configs[1], "c2"): 2D Q4 plane-stress cantilever on a
+256x128 grid (66,048 dofs, 1.18M nonzeros), lognormal KL modulus, POD basis
+k=20 from 50 GPU-solved snapshots, a batch of 64 seeded instances sharing the
+CSR pattern, each solved by PCG + POD-2G to relative residual 1e-8 from
+x0 = Phi A_c^{-1} Phi^T b.  One STEP = one batch: value upload/relayout,
+per-instance setup (A_c = Phi^T K Phi + LDL^T), x0, and the PCG loop.
+
+  python bench.py [--gpus N --steps K --warmup W --config c2 --impl ours|reference]
+
+N > 1 (torchrun): instance sharding, one 64-instance batch per rank with
+disjoint seeds (weak scaling, no data-path collective); max-over-ranks time.
+--impl reference: the unmodified reference (oracle/_ref, compiled from
+/root/reference by oracle/Makefile) on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PCG+POD-2G converged solves/sec (fp64)"
+UNIT = "solves/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-instances", type=int, default=0,
+                    help="instances in the CPU sample (default: one per host core, <= batch)")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nm, v in zip(names, s[5:9]):
+                if "Active" in v and "Not" not in v:
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kclass):
+    """dram bytes per launch of the dominant kernel class from the committed
+    ncu --set full capture (profiles/ncu_summary.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d["per_iteration_dram_bytes"].get(kclass)
+    except Exception:
+        return None
+
+
+def cpu_reference_run(prob, values, F, instances, jobs):
+    """The unmodified reference (oracle/_ref): fresh Pod2gPreconditioner +
+    reduced_solve x0 + pcg_solve per instance, parallel_for over `jobs`
+    threads (bench.hpp:290-330).  Returns (seconds, iters)."""
+    from oracle.bindings import Reference
+    R = Reference()
+    t = time.perf_counter()
+    u, it, conv, failed = R.pcg_pod2g_batch(prob.rp.astype(np.int64), prob.ci.astype(np.int64),
+                                            values[:instances], F[:instances], prob.phi, 1,
+                                            prob.cfg.tol, 100000, jobs)
+    dt = time.perf_counter() - t
+    if np.any(failed) or not np.all(conv):
+        raise RuntimeError("reference CPU arm: an instance failed")
+    return dt, it
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    if args.impl == "reference" and rank != 0:
+        return 0  # the reference arm runs on rank 0 alone
+
+    from paper_2207_02543_b200 import problems as PR
+    cfg = PR.CONFIGS[args.config]
+    cores = os.cpu_count() or 1
+
+    if args.impl == "reference":
+        return reference_arm(args, cfg, PR, cores, ws)
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    from paper_2207_02543_b200 import _lib as L
+    from paper_2207_02543_b200.solver import BatchSolver
+
+    # ---- inputs (outside the timed region): basis, this rank's instances
+    t0 = time.perf_counter()
+    prob = PR.build_problem(cfg, device=local)
+    strong = cfg.batch > 64 and ws > 1          # c3/c4: split the batch
+    B = cfg.batch // ws if strong else cfg.batch
+    seeds = PR.query_seeds(cfg, B, offset=rank * B)
+    values = prob.values(seeds)                 # [B][nnz] natural order (host)
+    n, nnz = prob.mesh.n, prob.mesh.nnz
+    F = np.ascontiguousarray(np.broadcast_to(prob.f, (B, n)))
+    gen_s = time.perf_counter() - t0
+
+    dev = torch.device("cuda", local)
+    vals_d = torch.from_numpy(values).to(dev)
+    b_d = torch.from_numpy(F).to(dev)
+    x_d = torch.empty_like(b_d)
+    s = BatchSolver(local)
+    s.set_pattern(prob.rp, prob.ci, prob.mesh.block_size)
+    stream = torch.cuda.ExternalStream(s.stream(), device=dev)
+
+    def step_device():
+        s.set_values_device(vals_d.data_ptr(), B)
+        s.set_basis(prob.phi)
+        st = s.setup()
+        it, conv, status, _ = s.solve_device(b_d.data_ptr(), x_d.data_ptr(), None, L.X0_REDUCED,
+                                             cfg.tol, 100000)
+        return st, it, conv, status
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step_device()
+    barrier()
+    l0 = s.launch_counts()[1]
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    iters_all = []
+    ok = True
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            st, it, conv, status = step_device()
+            ok &= bool(np.all(conv)) and bool(np.all(status == 0)) and bool(np.all(st == 0))
+            iters_all.append(it.copy())
+        ev1.record(stream)
+        barrier()
+    launches = s.launch_counts()[1] - l0
+    ms = ev0.elapsed_time(ev1)
+    if ws > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_solves = B * args.steps * ws
+    value = total_solves / (ms / 1e3)
+    iters = np.concatenate(iters_all)
+
+    # ---- roofline: per-kernel-class time of the loop body, same state
+    prof = s.profile_iteration(5)
+    dom = max(prof.items(), key=lambda kv: kv[1][0])
+    dom_name, (dom_ms, dom_bytes) = dom
+    peak, peak_src = hbm_peak()
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    iter_ms = sum(v[0] for v in prof.values())
+    iter_bytes = sum(v[1] for v in prof.values())
+    per_iter, _ = s.launch_counts()
+
+    # ---- e2e through the C-ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        vals_h = torch.from_numpy(values).pin_memory()
+        b_h = torch.from_numpy(F).pin_memory()
+        x_h = torch.empty_like(b_h).pin_memory()
+        import ctypes as C
+        lib = L.lib()
+        Dp = L.D
+        it_h = np.zeros(B, dtype=np.int64)
+        cv_h = np.zeros(B, dtype=np.int32)
+        st_h = np.zeros(B, dtype=np.int32)
+
+        def step_e2e():
+            rc = lib.p2g_set_values(s._h, B, C.cast(vals_h.data_ptr(), Dp))
+            assert rc == 0, rc
+            s.set_basis(prob.phi)
+            s.setup()
+            rc = lib.p2g_solve(s._h, C.cast(b_h.data_ptr(), Dp), None, L.X0_REDUCED, cfg.tol,
+                               100000, C.cast(x_h.data_ptr(), Dp), it_h.ctypes.data_as(L.I64),
+                               cv_h.ctypes.data_as(L.I32), st_h.ctypes.data_as(L.I32), None, 0)
+            assert rc == 0, rc
+            return float(x_h[0, 0])  # device->host read of the result
+
+        step_e2e()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_e2e()
+        e1.record(stream)
+        barrier()
+        ems = e0.elapsed_time(e1)
+        if ws > 1:
+            t = torch.tensor([ems], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": total_solves / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(values.nbytes + F.nbytes),
+               "d2h_bytes_per_step": int(F.nbytes + 3 * 4 * B)}
+
+    # ---- CPU baseline: the reference itself on host cores, bounded sample
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        ninst = args.cpu_instances or min(B, cores)
+        try:
+            dt, cit = cpu_reference_run(prob, values, F, ninst, cores)
+            cpu = {"value": ninst / dt, "unit": UNIT, "cores": cores, "kind": "reference",
+                   "sample": f"{ninst} of the {B} {cfg.name} instances, natural-order SGS "
+                             f"(reference default), x0=reduced_solve, tol {cfg.tol:g}; "
+                             f"mean iterations {float(np.mean(cit)):.1f}; {dt:.2f} s wall"}
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": cores, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded KL lognormal modulus; generator in include/pod2g_gen.h)",
+            "config": {"workload": f"{cfg.name}: Q4 plane-stress {cfg.nx}x{cfg.ny} cantilever"
+                                   if cfg.dim == 2 else
+                                   f"{cfg.name}: hex8 {cfg.nx}^3 elasticity",
+                       "n_dofs": n, "nnz": nnz, "pod_rank": int(prob.phi.shape[1]),
+                       "instances_per_gpu": B, "tol": cfg.tol, "x0": "reduced_solve",
+                       "smoother": "multicolour symmetric GS (node colours, D1)",
+                       "l2": "inputs larger than L2 (values %.0f MB per GPU)" % (values.nbytes / 1e6),
+                       "parallelism": f"instance-sharded x{ws}",
+                       "iterations_mean": float(np.mean(iters)),
+                       "iterations_max": int(np.max(iters)),
+                       "all_converged": ok, "input_generation_s": round(gen_s, 2)},
+            "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
+                         "traffic": ncu_traffic(dom_name),
+                         "algorithmic_bytes_per_iteration": iter_bytes,
+                         "iteration_ms": iter_ms,
+                         "iteration_frac": iter_bytes / (iter_ms * 1e-3) / 1e9 / peak,
+                         "classes": {k: {"ms": v[0], "bytes": v[1]} for k, v in prof.items()}},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "launches_per_iteration": int(per_iter),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    s.close()
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def reference_arm(args, cfg, PR, cores, ws):
+    """--impl reference: the reference CPU path on this box's host cores."""
+    mesh = PR.Mesh.for_config(cfg)
+    rp, ci = mesh.pattern()
+    f = mesh.rhs()
+    prob = _basis_for_reference(cfg, PR, mesh, rp, ci, f, cores)
+    ninst = args.cpu_instances or min(cfg.batch, cores)
+    seeds = PR.query_seeds(cfg, ninst)
+    values = mesh.assemble(mesh.kl_field(seeds, cfg.kl_terms)[0])
+    F = np.ascontiguousarray(np.broadcast_to(f, (ninst, mesh.n)))
+    times = []
+    for i in range(args.warmup + args.steps):
+        dt, it = cpu_reference_run(prob, values, F, ninst, cores)
+        if i >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = ninst * args.steps / tot
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"{cfg.name}", "n_dofs": mesh.n, "nnz": mesh.nnz,
+                   "instances_per_step": ninst, "tol": cfg.tol},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"{ninst} {cfg.name} instances per step, one per host core "
+                                   f"(parallel_for), natural-order SGS, x0=reduced_solve"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _basis_for_reference(cfg, PR, mesh, rp, ci, f, jobs):
+    """The reference arm's offline basis, made by the reference itself:
+    Jacobi-PCG snapshots with generate_snapshots' tolerance ladder and
+    compute_pod(RankTarget{k}) (oracle/_ref ref_offline_basis).  Only the
+    input generator (mesh, KL field) is ours."""
+    from oracle.bindings import Reference
+    R = Reference()
+    vals = mesh.assemble(mesh.kl_field(PR.snapshot_seeds(cfg), cfg.kl_terms)[0])
+    F = np.ascontiguousarray(np.broadcast_to(f, (len(vals), mesh.n)))
+    phi = R.offline_basis(rp.astype(np.int64), ci.astype(np.int64), vals, F, cfg.k,
+                          PR.SNAP_TOL, jobs)
+    return PR.Problem(cfg, mesh, rp, ci, f, phi, np.zeros(0), np.zeros(0))
+
+
+if __name__ == "__main__":
+    sys.exit(main())

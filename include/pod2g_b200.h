@@ -196,8 +196,13 @@ int p2g_analyze_pattern(int64_t n, const uint64_t* row_offsets, const uint64_t* 
 int p2g_profile_iteration(p2g_handle* h, int32_t reps, double* ms, double* bytes,
                           const char** names);
 
-/* Number of kernel launches per loop iteration and in the setup/prologue. */
-int p2g_launch_counts(const p2g_handle* h, int64_t* per_iteration, int64_t* last_solve_total);
+/* The handle's CUDA stream (cudaStream_t) -- every kernel of the handle is
+ * launched on it; callers time with CUDA events recorded on this stream. */
+void* p2g_get_stream(const p2g_handle* h);
+
+/* Kernel launches of one loop iteration, and the running total of every
+ * kernel this handle has executed (setup, prologue and graph iterations). */
+int p2g_launch_counts(const p2g_handle* h, int64_t* per_iteration, int64_t* total_executed);
 
 #ifdef __cplusplus
 }

@@ -230,6 +230,8 @@ class Reference:
         L.ref_pcg_pod2g_batch.argtypes = [C.c_int64, _I64, _I64, C.c_int64, _D, C.c_int64, _D,
                                           C.c_int64, _D, C.c_int, C.c_double, C.c_int64, _D,
                                           _I64, _I32, _I32, C.c_int]
+        L.ref_offline_basis.argtypes = [C.c_int64, _I64, _I64, C.c_int64, _D, C.c_int64, _D,
+                                         C.c_double, C.c_int64, C.c_int, _D, _I64]
         L.ref_its_case.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
                                    C.c_int64, _I64, _I64, _I64, _I64, _I64, _D, _D, _D,
                                    C.c_int64]
@@ -351,6 +353,17 @@ class Reference:
             delta, max_iter, _d(u), _i64(it), conv.ctypes.data_as(_I32),
             failed.ctypes.data_as(_I32), jobs))
         return u, it, conv, failed
+
+    def offline_basis(self, rp, ci, values, F, rank, tol=1e-10, jobs=1):
+        """Snapshots (Jacobi-PCG ladder) + compute_pod(RankTarget{rank})."""
+        rp, ci, values, F = _ix(rp), _ix(ci), _f64(values), _f64(F)
+        N, nnz = values.shape
+        n = len(rp) - 1
+        phi = np.empty((n, rank))
+        r = C.c_int64()
+        self._check(self.lib.ref_offline_basis(n, _i64(rp), _i64(ci), nnz, _d(values), N, _d(F),
+                                               tol, rank, jobs, _d(phi), C.byref(r)))
+        return np.ascontiguousarray(phi[:, : r.value])
 
     def its_case(self, res=32, n_snapshots=100, offline_seed=42, bench_seed=7, inst=0, jobs=8):
         n, nnz, rank = C.c_int64(), C.c_int64(), C.c_int64()

@@ -263,6 +263,42 @@ int ref_pcg_pod2g_batch(int64_t n, const int64_t* rp, const int64_t* ci, int64_t
     });
 }
 
+// Offline stage with the reference's own solvers, for the reference CPU arm:
+// snapshots as generate_snapshots solves them (problems.hpp:489-519: Jacobi-PCG,
+// tolerance ladder delta, delta/10, delta/100, true-residual check,
+// parallel_for over samples) for externally assembled systems, then
+// compute_pod(RankTarget{rank}) (pod.hpp:73-148).  phi receives d x r.
+int ref_offline_basis(int64_t n, const int64_t* rp, const int64_t* ci, int64_t nnz,
+                      const double* values, int64_t N, const double* f, double tolerance,
+                      int64_t rank, int jobs, double* phi, int64_t* rank_out) {
+    return guarded([&] {
+        std::vector<Vector> sols(static_cast<size_t>(N));
+        parallel_for(static_cast<index_t>(N), static_cast<index_t>(jobs), [&](index_t i) {
+            const CsrMatrix K = make_csr(n, rp, ci, values + i * nnz);
+            const Vector ff(f + i * n, f + (i + 1) * n);
+            const JacobiPreconditioner jacobi(K);
+            const index_t max_iter = 10 * K.nrows;
+            Vector u(K.nrows, 0.0);
+            const double fnorm = norm2(ff);
+            double true_rel = std::numeric_limits<double>::infinity();
+            for (double delta : {tolerance, tolerance / 10.0, tolerance / 100.0}) {
+                auto [sol, rep] = pcg_solve(K, ff, jacobi, u, delta, max_iter);
+                u = std::move(sol);
+                Vector r;
+                residual(K, ff, u, r);
+                true_rel = fnorm > 0.0 ? norm2(r) / fnorm : norm2(r);
+                if (true_rel <= tolerance) break;
+            }
+            if (true_rel > tolerance)
+                throw std::runtime_error("snapshot " + std::to_string(i) + " failed");
+            sols[i] = std::move(u);
+        });
+        const PodBasis b = compute_pod(sols, RankTarget{static_cast<index_t>(rank)});
+        *rank_out = static_cast<int64_t>(b.rank);
+        std::memcpy(phi, b.phi_r.data.data(), sizeof(double) * b.phi_r.data.size());
+    });
+}
+
 // Known-answer case from the reference's own acceptance run: the `its`
 // problem (problems.hpp:99-177, make_its_problem :399-407) at resolution `res`,
 // offline basis exactly as run_offline builds it (bench.hpp:58-64: LHS seed,

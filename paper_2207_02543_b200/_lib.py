@@ -47,6 +47,7 @@ SIGNATURES = [
                                       C.c_char_p, C.c_int32]),
     ("p2g_profile_iteration", C.c_int, [H, C.c_int32, D, D, C.POINTER(C.c_char_p)]),
     ("p2g_launch_counts", C.c_int, [H, I64, I64]),
+    ("p2g_get_stream", C.c_void_p, [H]),
     # pod2g_gen.h
     ("p2g_mesh_create", C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_double,
                                   C.c_double, C.c_double, C.c_double, C.POINTER(H)]),

@@ -25,14 +25,22 @@
 // in a fixed order, then fixed-order warp sums.  No floating-point atomics.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
 namespace p2g {
 
+namespace cg = cooperative_groups;
+
 constexpr int kWarps = 8;
 constexpr int kBlock = kWarps * 32;
+// Reduction-producing kernels run in thread-block clusters of kCluster CTAs:
+// the per-CTA partials are combined over DSMEM, so each cluster writes ONE
+// partial row (8x fewer rows for the per-instance scalar reductions).
+constexpr int kCluster = 8;
+#define P2G_CLUSTER __cluster_dims__(kCluster, 1, 1)
 
 template <int R_, int S_, int W_, int V_>
 struct Shape {
@@ -212,10 +220,15 @@ __device__ __forceinline__ void gs_row(const Mat& A, const double* f, double* s,
     }
 }
 
-// block-level deterministic partial: lanes -> warps (fixed order) -> part[T]
+// Deterministic per-cluster partial: lanes -> warps (fixed order) -> CTA
+// total in shared memory -> the cluster's rank-0 CTA sums the kCluster CTA
+// totals over DSMEM in rank order and writes (or, ACC, adds to) one row:
+//   part[(blockIdx.x / kCluster) * Bp + blockIdx.y * T + t]
 template <class Sh>
-__device__ __forceinline__ void block_partial(double (&acc)[Sh::V], double* part_row) {
+__device__ __forceinline__ void cluster_partial(double (&acc)[Sh::V], double* part, int Bp,
+                                                bool accumulate) {
     __shared__ double sm[kWarps][Sh::T];
+    __shared__ double tot[Sh::T];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int v = 0; v < Sh::V; ++v) acc[v] = inst_sum<Sh>(acc[v]);
@@ -228,8 +241,18 @@ __device__ __forceinline__ void block_partial(double (&acc)[Sh::V], double* part
         double t = 0.0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) t += sm[w][threadIdx.x];
-        part_row[threadIdx.x] = t;
+        tot[threadIdx.x] = t;
     }
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    if (cl.block_rank() == 0 && threadIdx.x < Sh::T) {
+        double t = 0.0;
+#pragma unroll
+        for (int r = 0; r < kCluster; ++r) t += cl.map_shared_rank(tot, r)[threadIdx.x];
+        double* dst = part + (size_t)(blockIdx.x / kCluster) * Bp + blockIdx.y * Sh::T + threadIdx.x;
+        *dst = accumulate ? *dst + t : t;
+    }
+    cl.sync();
 }
 
 template <class Sh>
@@ -252,7 +275,7 @@ __device__ __forceinline__ void lane_mask(const int* active, int b0, bool (&m)[S
 // y = K x (csr.hpp:83-93) on all rows; DOT: partial of x.y per instance
 // (krylov.hpp:272-273: Kp = spmv(K,p); pKp = dot(p, Kp)).
 template <class Sh, bool DOT>
-__global__ void __launch_bounds__(kBlock) k_spmv(Mat A, const double* __restrict__ x,
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_spmv(Mat A, const double* __restrict__ x,
                                                  double* __restrict__ y, const int* active,
                                                  double* part) {
     LaneGeo<Sh> G;
@@ -286,12 +309,12 @@ __global__ void __launch_bounds__(kBlock) k_spmv(Mat A, const double* __restrict
             }
         }
     }
-    if constexpr (DOT) block_partial<Sh>(dacc, part + (size_t)blockIdx.x * A.Bp + blockIdx.y * Sh::T);
+    if constexpr (DOT) cluster_partial<Sh>(dacc, part, A.Bp, false);
 }
 
 // r = f - K u (csr.hpp:96-105) with partials of r.r and f.f (for ||r0||, ||f||)
 template <class Sh>
-__global__ void __launch_bounds__(kBlock) k_residual(Mat A, const double* __restrict__ f,
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_residual(Mat A, const double* __restrict__ f,
                                                      const double* __restrict__ u,
                                                      double* __restrict__ r, const int* active,
                                                      double* part_rr, double* part_ff) {
@@ -328,9 +351,8 @@ __global__ void __launch_bounds__(kBlock) k_residual(Mat A, const double* __rest
         }
     }
     if (part_rr) {
-        block_partial<Sh>(rr, part_rr + (size_t)blockIdx.x * A.Bp + blockIdx.y * Sh::T);
-        __syncthreads();
-        block_partial<Sh>(ff, part_ff + (size_t)blockIdx.x * A.Bp + blockIdx.y * Sh::T);
+        cluster_partial<Sh>(rr, part_rr, A.Bp, false);
+        cluster_partial<Sh>(ff, part_ff, A.Bp, false);
     }
 }
 
@@ -342,7 +364,7 @@ enum : int { PRE_NONE = 0, PRE_GS = 1, PRE_JACOBI = 2 };
 //            JACOBI: s_i = omega * r_i / d_i on every row (first sweep from 0,
 //            smoothers.hpp:84-85 with u = 0)
 template <class Sh, bool UPDATE, int PRE>
-__global__ void __launch_bounds__(kBlock)
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock)
     k_update_pre(Mat A, double* __restrict__ u, double* __restrict__ r, const double* __restrict__ p,
                  const double* __restrict__ Kp, double* __restrict__ s, const double* alpha,
                  const int* active, double* part_rr, int color0_nodes, double omega) {
@@ -399,7 +421,7 @@ __global__ void __launch_bounds__(kBlock)
             }
         }
     }
-    if constexpr (UPDATE) block_partial<Sh>(rr, part_rr + (size_t)blockIdx.x * A.Bp + blockIdx.y * Sh::T);
+    if constexpr (UPDATE) cluster_partial<Sh>(rr, part_rr, A.Bp, false);
 }
 
 // Forward GS colour phase: nodes [nb, ne) of one colour, dofs ascending.
@@ -423,9 +445,9 @@ __global__ void __launch_bounds__(kBlock) k_gs_forward(Mat A, const double* __re
 // (gauss_seidel_sweep_backward, smoothers.hpp:56-70); LAST: partial of r.s
 // over this colour's rows (krylov.hpp:280 rs_new = dot(r, s)).
 template <class Sh, bool LAST>
-__global__ void __launch_bounds__(kBlock) k_gs_backward(Mat A, const double* __restrict__ f,
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_gs_backward(Mat A, const double* __restrict__ f,
                                                         double* s, const int* active, int nb,
-                                                        int ne, double* part_rs) {
+                                                        int ne, double* part_rs, int accumulate) {
     LaneGeo<Sh> G;
     const int b0 = blockIdx.y * Sh::T + G.w * Sh::V;
     bool m[Sh::V], any;
@@ -450,14 +472,13 @@ __global__ void __launch_bounds__(kBlock) k_gs_backward(Mat A, const double* __r
             }
         }
     }
-    if constexpr (LAST)
-        block_partial<Sh>(rs, part_rs + (size_t)blockIdx.x * A.Bp + blockIdx.y * Sh::T);
+    if constexpr (LAST) cluster_partial<Sh>(rs, part_rs, A.Bp, accumulate != 0);
 }
 
 // Damped Jacobi sweep, out of place (smoothers.hpp:83-86):
 //   s_out_i = s_i + omega * (f_i - (K s)_i) / d_i ; LAST: partial of f.s_out
 template <class Sh, bool LAST>
-__global__ void __launch_bounds__(kBlock) k_jacobi(Mat A, const double* __restrict__ f,
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_jacobi(Mat A, const double* __restrict__ f,
                                                    const double* __restrict__ s,
                                                    double* __restrict__ s_out, const int* active,
                                                    double omega, double* part_rs) {
@@ -496,8 +517,7 @@ __global__ void __launch_bounds__(kBlock) k_jacobi(Mat A, const double* __restri
             }
         }
     }
-    if constexpr (LAST)
-        block_partial<Sh>(rs, part_rs + (size_t)blockIdx.x * A.Bp + blockIdx.y * Sh::T);
+    if constexpr (LAST) cluster_partial<Sh>(rs, part_rs, A.Bp, false);
 }
 
 enum : int { RES_UPPER = 0, RES_FULL = 1, RES_VECTOR = 2 };
@@ -510,7 +530,7 @@ enum : int { RES_UPPER = 0, RES_FULL = 1, RES_VECTOR = 2 };
 //                                  reduced_solve's project(f), pod.hpp:171)
 // part[blk][a][b] = sum over the block's rows of phi[i][a] * t_i.
 template <class Sh, int KMAX, int FORM>
-__global__ void __launch_bounds__(kBlock) k_restrict(Mat A, const double* __restrict__ f,
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_restrict(Mat A, const double* __restrict__ f,
                                                      const double* __restrict__ s,
                                                      const double* __restrict__ phi, int k,
                                                      const int* active, double* part) {
@@ -566,10 +586,11 @@ __global__ void __launch_bounds__(kBlock) k_restrict(Mat A, const double* __rest
             }
         }
     }
-    // block reduction in chunks of 8 coefficients (bounded shared memory)
+    // CTA reduction in chunks of 8 coefficients, then the cluster's rank-0
+    // CTA sums the kCluster CTA totals over DSMEM: one partial row per cluster
     __shared__ double sm[kWarps][8][Sh::T];
+    __shared__ double tot[KMAX][Sh::T];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double* prow = part + (size_t)blockIdx.x * k * A.Bp + blockIdx.y * Sh::T;
 #pragma unroll
     for (int a0 = 0; a0 < KMAX; a0 += 8) {
         if (a0 >= k) break;
@@ -584,20 +605,32 @@ __global__ void __launch_bounds__(kBlock) k_restrict(Mat A, const double* __rest
         __syncthreads();
         for (int e = threadIdx.x; e < 8 * Sh::T; e += kBlock) {
             const int j = e / Sh::T, bt = e % Sh::T;
-            if (a0 + j < k) {
-                double tot = 0.0;
+            double t = 0.0;
 #pragma unroll
-                for (int w = 0; w < kWarps; ++w) tot += sm[w][j][bt];
-                prow[(size_t)(a0 + j) * A.Bp + bt] = tot;
-            }
+            for (int w = 0; w < kWarps; ++w) t += sm[w][j][bt];
+            tot[a0 + j][bt] = t;
         }
         __syncthreads();
     }
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    if (cl.block_rank() == 0) {
+        double* prow = part + (size_t)(blockIdx.x / kCluster) * k * A.Bp + blockIdx.y * Sh::T;
+        for (int e = threadIdx.x; e < k * Sh::T; e += kBlock) {
+            const int a = e / Sh::T, bt = e % Sh::T;
+            double t = 0.0;
+#pragma unroll
+            for (int r = 0; r < kCluster; ++r) t += cl.map_shared_rank(&tot[0][0], r)[a * Sh::T + bt];
+            prow[(size_t)a * A.Bp + bt] = t;
+        }
+    }
+    cl.sync();
 }
 
 // Coarse correction (pod.hpp:200): c = sum of the restriction partials
-// (fixed order), e = A_c^{-1} c by the Cholesky factor L (lower, row-major
-// [Bp][k][k]).  One block per instance.
+// (fixed order), e = A_c^{-1} c with the LDL^T factor of A_c (L unit lower in
+// the strict lower triangle, D on the diagonal; row-major [Bp][k][k]).
+// One block per instance.
 __global__ void __launch_bounds__(kBlock) k_coarse(int Bp, int k, int nblk, const double* part,
                                                    const double* L, double* e, const int* active) {
     const int b = blockIdx.x;
@@ -607,6 +640,7 @@ __global__ void __launch_bounds__(kBlock) k_coarse(int Bp, int k, int nblk, cons
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int a = warp; a < k; a += kWarps) {
         double t = 0.0;
+#pragma unroll 4
         for (int blk = lane; blk < nblk; blk += 32) t += part[((size_t)blk * k + a) * Bp + b];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
@@ -616,26 +650,19 @@ __global__ void __launch_bounds__(kBlock) k_coarse(int Bp, int k, int nblk, cons
     for (int e2 = threadIdx.x; e2 < k * k; e2 += kBlock) Ls[e2] = Lb[e2];
     __syncthreads();
     if (warp == 0) {
-        // forward: L y = c (lane j owns y_j, y_{j+32})
+        // forward: L y = c (unit diagonal); lane j owns y_j, y_{j+32}
         double y0 = lane < k ? c[lane] : 0.0, y1 = lane + 32 < k ? c[lane + 32] : 0.0;
         for (int j = 0; j < k; ++j) {
-            const double yj_owner = (j < 32) ? y0 : y1;
-            double yj = __shfl_sync(0xffffffffu, yj_owner, j & 31);
-            yj = yj / Ls[j * k + j];
-            if (lane == (j & 31)) {
-                if (j < 32) y0 = yj; else y1 = yj;
-            }
+            const double yj = __shfl_sync(0xffffffffu, j < 32 ? y0 : y1, j & 31);
             if (lane > j && lane < k) y0 -= Ls[lane * k + j] * yj;
             if (lane + 32 > j && lane + 32 < k) y1 -= Ls[(lane + 32) * k + j] * yj;
         }
-        // backward: L^T x = y
+        // z = D^{-1} y
+        if (lane < k) y0 /= Ls[lane * k + lane];
+        if (lane + 32 < k) y1 /= Ls[(lane + 32) * k + lane + 32];
+        // backward: L^T x = z
         for (int j = k - 1; j >= 0; --j) {
-            const double xj_owner = (j < 32) ? y0 : y1;
-            double xj = __shfl_sync(0xffffffffu, xj_owner, j & 31);
-            xj = xj / Ls[j * k + j];
-            if (lane == (j & 31)) {
-                if (j < 32) y0 = xj; else y1 = xj;
-            }
+            const double xj = __shfl_sync(0xffffffffu, j < 32 ? y0 : y1, j & 31);
             if (lane < j) y0 -= Ls[j * k + lane] * xj;
             if (lane + 32 < j) y1 -= Ls[j * k + lane + 32] * xj;
         }
@@ -723,6 +750,7 @@ __global__ void __launch_bounds__(kBlock) k_pupdate(int n, int Bp, const double*
 __device__ __forceinline__ double warp_col_sum(const double* part, int rows, int Bp, int b) {
     const int lane = threadIdx.x & 31;
     double t = 0.0;
+#pragma unroll 4
     for (int q = lane; q < rows; q += 32) t += part[(size_t)q * Bp + b];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
@@ -748,18 +776,20 @@ __global__ void k_alpha(int Bp, int nrows, const double* part, const double* rs_
 }
 
 // End of one PCG iteration (krylov.hpp:280-288): rs_new, beta, k++, rel,
-// history, breakdown, convergence; sets the graph's while-condition.
-__global__ void __launch_bounds__(1024) k_finalize(int Bp, int nrs, const double* part_rs,
-                                                   int nrr, const double* part_rr,
-                                                   const double* fnorm, double* rs_old,
-                                                   double* beta, double* rel, int* iters,
-                                                   int* active, int* status, double* hist,
-                                                   const SolveParams* prm,
-                                                   cudaGraphConditionalHandle cond, int set_cond) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+// history, breakdown, convergence, one warp per instance.  The last CTA to
+// finish sets the graph's while-condition to "any instance still active"
+// (integer atomics only: the flag/ticket are reset by that CTA).
+__global__ void __launch_bounds__(256) k_finalize(int Bp, int nrs, const double* part_rs,
+                                                  int nrr, const double* part_rr,
+                                                  const double* fnorm, double* rs_old,
+                                                  double* beta, double* rel, int* iters,
+                                                  int* active, int* status, double* hist,
+                                                  const SolveParams* prm, unsigned* flag_ticket,
+                                                  cudaGraphConditionalHandle cond, int set_cond) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.x * (blockDim.x >> 5) + warp;
     int any = 0;
-    for (int b = warp; b < Bp; b += nw) {
-        if (!active[b]) continue;
+    if (b < Bp && active[b]) {
         const double rs_new = warp_col_sum(part_rs, nrs, Bp, b);
         const double rr = warp_col_sum(part_rr, nrr, Bp, b);
         if (lane == 0) {
@@ -784,7 +814,16 @@ __global__ void __launch_bounds__(1024) k_finalize(int Bp, int nrs, const double
         }
     }
     any = __syncthreads_or(any);
-    if (set_cond && threadIdx.x == 0) cudaGraphSetConditional(cond, any ? 1u : 0u);
+    if (set_cond && threadIdx.x == 0) {
+        if (any) atomicOr(&flag_ticket[0], 1u);
+        __threadfence();
+        const unsigned t = atomicAdd(&flag_ticket[1], 1u);
+        if (t == gridDim.x - 1) {
+            const unsigned f = atomicExch(&flag_ticket[0], 0u);
+            atomicExch(&flag_ticket[1], 0u);
+            cudaGraphSetConditional(cond, f ? 1u : 0u);
+        }
+    }
 }
 
 // Initial residual bookkeeping (krylov.hpp:252-260): fnorm, rel0, hist[0],
@@ -1003,9 +1042,11 @@ __global__ void k_reduce_ac(int nblk, int k, int Bt, int bofs, const double* par
     if (lane == 0) Ac[((size_t)(bofs + bt) * k + a) * k + c] = t;
 }
 
-// Cholesky of the symmetrised A_c, one warp per instance (row-major lower L).
-// Singular (dense_solve.hpp:20,25-26 analogue): pivot <= 1e-14 * max|a| or
-// non-positive.
+// Square-root-free Cholesky (LDL^T, no pivoting) of the symmetrised A_c,
+// one warp per instance.  Works for any symmetric matrix with nonzero leading
+// minors, so an indefinite coarse operator factors like the reference's LU
+// and surfaces later as a PCG breakdown; singular (dense_solve.hpp:20,25-26
+// analogue) when a pivot |d_j| <= 1e-14 * max|a|.
 __global__ void k_cholesky(int B, int k, const double* Ac, double* L, int* status) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int b = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -1024,19 +1065,19 @@ __global__ void k_cholesky(int B, int k, const double* Ac, double* L, int* statu
     __syncwarp();
     bool bad = false;
     for (int j = 0; j < k; ++j) {
-        // L[j][j]
+        // d_j = a_jj - sum_q l_jq^2 d_q
         double d = Lb[j * k + j];
-        for (int q = 0; q < j; ++q) d -= Lb[j * k + q] * Lb[j * k + q];
-        if (!(d > floor_)) bad = true;
-        const double ljj = sqrt(fmax(d, 1e-300));
+        for (int q = 0; q < j; ++q) d -= Lb[j * k + q] * Lb[j * k + q] * Lb[q * k + q];
+        if (!(fabs(d) > floor_)) bad = true;
+        const double dj = bad ? 1.0 : d;
         __syncwarp();
         for (int i = j + 1 + lane; i < k; i += 32) {
             double v = Lb[i * k + j];
-            for (int q = 0; q < j; ++q) v -= Lb[i * k + q] * Lb[j * k + q];
-            Lb[i * k + j] = v / ljj;
+            for (int q = 0; q < j; ++q) v -= Lb[i * k + q] * Lb[j * k + q] * Lb[q * k + q];
+            Lb[i * k + j] = v / dj;
         }
         __syncwarp();
-        if (lane == 0) Lb[j * k + j] = ljj;
+        if (lane == 0) Lb[j * k + j] = dj;
         __syncwarp();
     }
     if (lane == 0 && bad && status[b] == ST_OK) status[b] = ST_ESINGULAR;

@@ -78,6 +78,7 @@ struct p2g_handle {
     double* d_hist = nullptr;
     int64_t hist_cap_alloc = 0;
     SolveParams* d_prm = nullptr;
+    unsigned* d_flag_ticket = nullptr;  // [any-active flag, CTA ticket] of k_finalize
     // partials
     int nb_cap = 0;
     double *d_part_dot = nullptr, *d_part_rr = nullptr, *d_part_ff = nullptr,
@@ -97,8 +98,11 @@ struct p2g_handle {
     cudaGraphConditionalHandle cond = 0;
 
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    std::vector<std::pair<const void*, int>> occ_cache;
     double last_ms[2] = {0, 0};
     int64_t launches_per_iter = 0, launches_last_solve = 0, launch_counter = 0;
+    int64_t launches_executed = 0;  // every kernel this handle ran (graph iterations included)
+    bool capturing = false;
     // profiling
     bool profiling = false;
     cudaEvent_t kev[64];
@@ -178,6 +182,7 @@ Mat mat_of(p2g_handle* h) {
 
 void count_launch(p2g_handle* h, int kclass) {
     ++h->launch_counter;
+    if (!h->capturing) ++h->launches_executed;
     if (h->profiling && h->kev_n < 63) {
         h->kev_class[h->kev_n] = kclass;
         cudaEventRecord(h->kev[h->kev_n + 1], h->stream);
@@ -186,15 +191,41 @@ void count_launch(p2g_handle* h, int kclass) {
 }
 
 // grid for a node-range kernel: one wave of resident blocks at most
+// cluster == true: grid.x rounded up to a multiple of kCluster (the kernel
+// carries __cluster_dims__), one partial row per cluster
+// Resident CTAs per kernel (one full wave), cached per function.  For the
+// cluster kernels this is the number of co-resident CLUSTERS x kCluster, so
+// the grid never spills into a partial second wave.
+int resident_ctas(p2g_handle* h, const void* fn, bool cluster) {
+    for (auto& e : h->occ_cache)
+        if (e.first == fn) return e.second;
+    int ctas = 0;
+    if (cluster) {
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(kCluster * 1024, 1, 1);
+        lc.blockDim = dim3(kBlock, 1, 1);
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, fn, &lc) != cudaSuccess || ncl <= 0) {
+            cudaGetLastError();
+            ncl = h->num_sms / kCluster;
+        }
+        ctas = ncl * kCluster;
+    } else {
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, 0);
+        ctas = std::max(occ, 1) * h->num_sms;
+    }
+    h->occ_cache.emplace_back(fn, ctas);
+    return ctas;
+}
+
 template <class Sh>
-dim3 node_grid(p2g_handle* h, int64_t units, const void* fn) {
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, 0);
-    occ = std::max(occ, 1);
+dim3 node_grid(p2g_handle* h, int64_t units, const void* fn, bool cluster = false) {
     const int64_t need = (units + kWarps * Sh::R - 1) / (kWarps * Sh::R);
-    int64_t gx = std::min<int64_t>(need, (int64_t)h->num_sms * occ);
+    int64_t gx = std::min<int64_t>(need, resident_ctas(h, fn, cluster));
     gx = std::max<int64_t>(gx, 1);
     gx = std::min<int64_t>(gx, h->nb_cap);
+    if (cluster) gx = (gx + kCluster - 1) / kCluster * kCluster;
     return dim3(static_cast<unsigned>(gx), static_cast<unsigned>(h->Bp / Sh::T));
 }
 
@@ -210,12 +241,12 @@ struct Run {
         Mat A = mat_of(h);
         if (dot) {
             auto fn = k_spmv<Sh, true>;
-            dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn);
+            dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn, true);
             fn<<<g, kBlock, 0, h->stream>>>(A, x, y, h->d_active, h->d_part_dot);
-            if (nb_out) *nb_out = g.x;
+            if (nb_out) *nb_out = g.x / kCluster;
         } else {
             auto fn = k_spmv<Sh, false>;
-            dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn);
+            dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn, true);
             fn<<<g, kBlock, 0, h->stream>>>(A, x, y, h->d_active, nullptr);
         }
         count_launch(h, KC_SPMV);
@@ -226,9 +257,9 @@ struct Run {
     static int residual(p2g_handle* h, const double* f, const double* u, double* r, int* nb_out) {
         Mat A = mat_of(h);
         auto fn = k_residual<Sh>;
-        dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn);
+        dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn, true);
         fn<<<g, kBlock, 0, h->stream>>>(A, f, u, r, h->d_active, h->d_part_rr, h->d_part_ff);
-        *nb_out = g.x;
+        *nb_out = g.x / kCluster;
         count_launch(h, KC_SPMV);
         CU(cudaGetLastError());
         return P2G_OK;
@@ -243,10 +274,10 @@ struct Run {
 #define P2G_UP(U, P)                                                                         \
     {                                                                                        \
         auto fn = k_update_pre<Sh, U, P>;                                                    \
-        dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn);                               \
+        dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn, true);                         \
         fn<<<g, kBlock, 0, h->stream>>>(A, h->d_u, r, h->d_p, h->d_Kp, h->d_s, h->d_alpha,   \
                                         h->d_active, h->d_part_rr, c0, h->cfg.omega);        \
-        if (nb_rr) *nb_rr = g.x;                                                             \
+        if (nb_rr) *nb_rr = g.x / kCluster;                                                  \
     }
         if (update) {
             if (pre == PRE_GS) P2G_UP(true, PRE_GS) else P2G_UP(true, PRE_JACOBI)
@@ -278,22 +309,27 @@ struct Run {
         return P2G_OK;
     }
 
+    // one backward colour phase; every phase of a sweep uses the same grid
+    // (the largest colour's) so the LAST sweep's r.s partials accumulate into
+    // the same rows phase after phase (first phase writes, later ones add)
     static int gs_backward(p2g_handle* h, const double* f, double* s, int c, bool last,
-                           int* rs_row) {
+                           int* rs_rows, bool first_phase) {
         Mat A = mat_of(h);
         const int nb = static_cast<int>(h->pat.color_rows[c] / h->pat.bs);
         const int ne = static_cast<int>(h->pat.color_rows[c + 1] / h->pat.bs);
-        if (ne <= nb) return P2G_OK;
+        int64_t maxc = 1;
+        for (int q = 0; q < h->pat.ncolors; ++q)
+            maxc = std::max<int64_t>(maxc, (h->pat.color_rows[q + 1] - h->pat.color_rows[q]) / h->pat.bs);
         if (last) {
             auto fn = k_gs_backward<Sh, true>;
-            dim3 g = node_grid<Sh>(h, ne - nb, (const void*)fn);
-            fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_active, nb, ne,
-                                            h->d_part_rs + (size_t)(*rs_row) * h->Bp);
-            *rs_row += g.x;
+            dim3 g = node_grid<Sh>(h, maxc, (const void*)fn, true);
+            fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_active, nb, ne, h->d_part_rs,
+                                            first_phase ? 0 : 1);
+            *rs_rows = g.x / kCluster;
         } else {
             auto fn = k_gs_backward<Sh, false>;
-            dim3 g = node_grid<Sh>(h, ne - nb, (const void*)fn);
-            fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_active, nb, ne, nullptr);
+            dim3 g = node_grid<Sh>(h, maxc, (const void*)fn, true);
+            fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_active, nb, ne, nullptr, 0);
         }
         count_launch(h, KC_BWD);
         CU(cudaGetLastError());
@@ -301,17 +337,17 @@ struct Run {
     }
 
     static int jacobi(p2g_handle* h, const double* f, const double* s, double* s_out, bool last,
-                      int* rs_row, int kclass) {
+                      int* rs_rows, int kclass) {
         Mat A = mat_of(h);
         if (last) {
             auto fn = k_jacobi<Sh, true>;
-            dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn);
+            dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn, true);
             fn<<<g, kBlock, 0, h->stream>>>(A, f, s, s_out, h->d_active, h->cfg.omega,
-                                            h->d_part_rs + (size_t)(*rs_row) * h->Bp);
-            *rs_row += g.x;
+                                            h->d_part_rs);
+            *rs_rows = g.x / kCluster;
         } else {
             auto fn = k_jacobi<Sh, false>;
-            dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn);
+            dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn, true);
             fn<<<g, kBlock, 0, h->stream>>>(A, f, s, s_out, h->d_active, h->cfg.omega, nullptr);
         }
         count_launch(h, kclass);
@@ -325,19 +361,19 @@ struct Run {
         KSWITCH(k, {
             if (form == RES_UPPER) {
                 auto fn = k_restrict<ASh, KM, RES_UPPER>;
-                dim3 g = node_grid<ASh>(h, nnodes(h), (const void*)fn);
+                dim3 g = node_grid<ASh>(h, nnodes(h), (const void*)fn, true);
                 fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_phi, k, h->d_active, h->d_part_c);
-                *nb_out = g.x;
+                *nb_out = g.x / kCluster;
             } else if (form == RES_FULL) {
                 auto fn = k_restrict<ASh, KM, RES_FULL>;
-                dim3 g = node_grid<ASh>(h, nnodes(h), (const void*)fn);
+                dim3 g = node_grid<ASh>(h, nnodes(h), (const void*)fn, true);
                 fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_phi, k, h->d_active, h->d_part_c);
-                *nb_out = g.x;
+                *nb_out = g.x / kCluster;
             } else {
                 auto fn = k_restrict<ASh, KM, RES_VECTOR>;
-                dim3 g = node_grid<ASh>(h, nnodes(h), (const void*)fn);
+                dim3 g = node_grid<ASh>(h, nnodes(h), (const void*)fn, true);
                 fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_phi, k, h->d_active, h->d_part_c);
-                *nb_out = g.x;
+                *nb_out = g.x / kCluster;
             }
         });
         count_launch(h, KC_RESTRICT);
@@ -422,7 +458,8 @@ struct Run {
         if (cfg.smoother == P2G_SMOOTHER_GS_MULTICOLOR) {
             for (int sw = 0; sw < cfg.post_sweeps; ++sw) {
                 const bool last = sw + 1 == cfg.post_sweeps;
-                for (int c = C - 1; c >= 0; --c) TRY(gs_backward(h, rr, cur, c, last, &rs_row));
+                for (int c = C - 1; c >= 0; --c)
+                    TRY(gs_backward(h, rr, cur, c, last, &rs_row, c == C - 1));
             }
         } else {
             for (int sw = 0; sw < cfg.post_sweeps; ++sw) {
@@ -447,10 +484,10 @@ struct Run {
                                                                   h->d_active, h->d_status);
         count_launch(h, KC_REDUCE);
         TRY(precond(h, true, nullptr, &nb_rr, &rs_rows));
-        k_finalize<<<1, 1024, 0, h->stream>>>(h->Bp, rs_rows, h->d_part_rs, nb_rr, h->d_part_rr,
-                                              h->d_fnorm, h->d_rsold, h->d_beta, h->d_rel,
-                                              h->d_iters, h->d_active, h->d_status, h->d_hist,
-                                              h->d_prm, h->cond, in_graph ? 1 : 0);
+        k_finalize<<<(h->Bp + 7) / 8, 256, 0, h->stream>>>(
+            h->Bp, rs_rows, h->d_part_rs, nb_rr, h->d_part_rr, h->d_fnorm, h->d_rsold, h->d_beta,
+            h->d_rel, h->d_iters, h->d_active, h->d_status, h->d_hist, h->d_prm, h->d_flag_ticket,
+            h->cond, in_graph ? 1 : 0);
         count_launch(h, KC_REDUCE);
         TRY(pupdate(h, h->s_final, false));
         CU(cudaGetLastError());
@@ -488,13 +525,13 @@ struct Run {
                 const int64_t need = (n / h->pat.bs + kWarps * MSh::R - 1) / (kWarps * MSh::R);
                 dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)h->num_sms * occ)),
                        (unsigned)((Bt + MSh::T - 1) / MSh::T));
-                fn<<<g, kBlock, 0, h->stream>>>(A, h->d_phi, k, bofs, Bt, Y);
+                fn<<<g, kBlock, 0, h->stream>>>(A, h->d_phi, k, bofs, Bt, Y); ++h->launches_executed;
                 auto fr = k_restrict_cols<KM>;
                 dim3 g2((unsigned)std::min<int64_t>(occ_blocks, (n + kWarps - 1) / kWarps),
                         (unsigned)((ncol + 31) / 32));
-                fr<<<g2, kBlock, 0, h->stream>>>(n, ncol, Y, h->d_phi, k, part);
+                fr<<<g2, kBlock, 0, h->stream>>>(n, ncol, Y, h->d_phi, k, part); ++h->launches_executed;
                 const int total = Bt * k * k;
-                k_reduce_ac<<<(total + 7) / 8, 256, 0, h->stream>>>(g2.x, k, Bt, bofs, part, h->d_Ac);
+                k_reduce_ac<<<(total + 7) / 8, 256, 0, h->stream>>>(g2.x, k, Bt, bofs, part, h->d_Ac); ++h->launches_executed;
             });
             if (cudaGetLastError() != cudaSuccess) st = P2G_ECUDA;
         }
@@ -506,7 +543,7 @@ struct Run {
             return st;
         }
         k_cholesky<<<(h->B + 7) / 8, 256, 0, h->stream>>>(h->B, k, h->d_Ac, h->d_L,
-                                                          h->d_setup_status);
+                                                          h->d_setup_status); ++h->launches_executed;
         CU(cudaGetLastError());
         return P2G_OK;
     }
@@ -532,7 +569,7 @@ int upload_interleaved(p2g_handle* h, const double* src_host, const double* src_
     if (src_dev) {
         dim3 g((unsigned)((len + 31) / 32), (unsigned)((h->Bp + 31) / 32));
         k_gather_interleave<<<g, 256, 0, h->stream>>>(src_dev, len, B, d_map, len, dst, h->Bp, 0,
-                                                      0.0);
+                                                      0.0); ++h->launches_executed;
         CU(cudaGetLastError());
         return P2G_OK;
     }
@@ -552,7 +589,7 @@ int upload_interleaved(p2g_handle* h, const double* src_host, const double* src_
         // rows of this chunk: columns [b0, b0+nb)
         dim3 g((unsigned)((len + 31) / 32), (unsigned)((h->Bp + 31) / 32));
         k_gather_interleave<<<g, 256, 0, h->stream>>>(h->d_stage, len, nb, d_map, len, dst, h->Bp,
-                                                      b0, 0.0);
+                                                      b0, 0.0); ++h->launches_executed;
         CU(cudaGetLastError());
         CU(cudaStreamSynchronize(h->stream));  // staging buffer reuse
     }
@@ -563,7 +600,7 @@ int download_interleaved(p2g_handle* h, const double* src, double* dst_host, dou
     const int64_t n = h->pat.n;
     dim3 g((unsigned)((n + 31) / 32), (unsigned)((h->Bp + 31) / 32));
     if (dst_dev) {
-        k_scatter_deinterleave<<<g, 256, 0, h->stream>>>(src, h->Bp, n, h->d_perm, h->B, dst_dev);
+        k_scatter_deinterleave<<<g, 256, 0, h->stream>>>(src, h->Bp, n, h->d_perm, h->B, dst_dev); ++h->launches_executed;
         CU(cudaGetLastError());
         return P2G_OK;
     }
@@ -573,7 +610,7 @@ int download_interleaved(p2g_handle* h, const double* src, double* dst_host, dou
         CU(cudaMalloc(&h->d_stage, bytes));
         h->stage_bytes = bytes;
     }
-    k_scatter_deinterleave<<<g, 256, 0, h->stream>>>(src, h->Bp, n, h->d_perm, h->B, h->d_stage);
+    k_scatter_deinterleave<<<g, 256, 0, h->stream>>>(src, h->Bp, n, h->d_perm, h->B, h->d_stage); ++h->launches_executed;
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(dst_host, h->d_stage, bytes, cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));
@@ -681,7 +718,9 @@ int build_loop_graph(p2g_handle* h) {
     CU(cudaStreamBeginCaptureToGraph(h->stream, body, nullptr, nullptr, 0,
                                      cudaStreamCaptureModeRelaxed));
     const int64_t before = h->launch_counter;
+    h->capturing = true;
     int st = dispatch(h, [&](auto R) -> int { return decltype(R)::iteration(h, true); });
+    h->capturing = false;
     cudaGraph_t captured = nullptr;
     cudaError_t ce = cudaStreamEndCapture(h->stream, &captured);
     if (st != P2G_OK) {
@@ -720,7 +759,7 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
         h->hist_cap_alloc = cap_dev;
     }
     if (!h->loop_exec) TRY(build_loop_graph(h));
-    const int64_t lc0 = h->launch_counter;
+    const int64_t lc0 = h->launches_executed;
     SolveParams prm{tol, (long long)max_iter, (long long)hist_cap};
     CU(cudaMemcpyAsync(h->d_prm, &prm, sizeof(prm), cudaMemcpyHostToDevice, h->stream));
 
@@ -763,7 +802,7 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
     {
         const dim3 g((unsigned)std::min<int64_t>((h->pat.n + 255) / 256, 1024), h->B);
         k_check_finite<<<g, 256, 0, h->stream>>>(static_cast<int>(h->pat.n), h->Bp, h->d_u,
-                                                  h->d_status);
+                                                  h->d_status); ++h->launches_executed;
         CU(cudaGetLastError());
     }
     if (x_host || x_dev) TRY(download_interleaved(h, h->d_u, x_host, x_dev));
@@ -796,8 +835,8 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
     h->last_ms[1] = ms_loop;
     int64_t maxit = 0;
     for (int b = 0; b < h->B; ++b) maxit = std::max<int64_t>(maxit, it[b]);
-    h->launches_last_solve = (h->launch_counter - lc0) + 1 /*set_cond*/ +
-                             maxit * h->launches_per_iter + 1 /*finite*/ + 1 /*download*/;
+    h->launches_executed += 1 /*set_cond*/ + maxit * h->launches_per_iter;
+    h->launches_last_solve = h->launches_executed - lc0;
     if (worst != P2G_OK) h->err = "p2g_solve: at least one instance failed (see status)";
     return worst;
 }
@@ -849,7 +888,9 @@ int p2g_create(int device, p2g_handle** out) {
     }
     for (auto& e : h->ev) cudaEventCreate(&e);
     for (auto& e : h->kev) cudaEventCreate(&e);
-    if (cudaMalloc(&h->d_prm, sizeof(SolveParams)) != cudaSuccess) {
+    if (cudaMalloc(&h->d_prm, sizeof(SolveParams)) != cudaSuccess ||
+        cudaMalloc(&h->d_flag_ticket, 2 * sizeof(unsigned)) != cudaSuccess ||
+        cudaMemset(h->d_flag_ticket, 0, 2 * sizeof(unsigned)) != cudaSuccess) {
         delete h;
         return P2G_ECUDA;
     }
@@ -878,6 +919,7 @@ int p2g_destroy(p2g_handle* h) {
     for (int** p : {&h->d_active, &h->d_iters, &h->d_status, &h->d_setup_status, &h->d_all})
         dfree(*p);
     dfree(h->d_prm);
+    dfree(h->d_flag_ticket);
     for (auto& e : h->ev) cudaEventDestroy(e);
     for (auto& e : h->kev) cudaEventDestroy(e);
     cudaStreamDestroy(h->stream);
@@ -977,7 +1019,7 @@ int p2g_setup(p2g_handle* h, const p2g_config* cfg, int32_t* status) {
     {
         Mat A = mat_of(h);
         dim3 g(std::max(1, std::min(1024, (int)((h->pat.n + 255) / 256))), h->B);
-        k_check_diag<<<g, 256, 0, h->stream>>>(A, h->B, h->d_setup_status);
+        k_check_diag<<<g, 256, 0, h->stream>>>(A, h->B, h->d_setup_status); ++h->launches_executed;
         CU(cudaGetLastError());
     }
     if (h->k > 0) TRY(dispatch(h, [&](auto R) -> int { return decltype(R)::coarse_setup(h); }));
@@ -1088,7 +1130,8 @@ int p2g_smooth(p2g_handle* h, int32_t direction, const double* f, double* u) {
             for (int c = 0; c < C; ++c) TRY(Rn::gs_forward(h, h->d_r, h->d_s, c, false));
         } else {
             int row = 0;
-            for (int c = C - 1; c >= 0; --c) TRY(Rn::gs_backward(h, h->d_r, h->d_s, c, false, &row));
+            for (int c = C - 1; c >= 0; --c)
+                TRY(Rn::gs_backward(h, h->d_r, h->d_s, c, false, &row, c == C - 1));
         }
         return P2G_OK;
     }));
@@ -1191,10 +1234,12 @@ int p2g_profile_iteration(p2g_handle* h, int32_t reps, double* ms, double* bytes
     return P2G_OK;
 }
 
+void* p2g_get_stream(const p2g_handle* h) { return h ? (void*)h->stream : nullptr; }
+
 int p2g_launch_counts(const p2g_handle* h, int64_t* per_iteration, int64_t* last_solve_total) {
     if (!h) return P2G_EINVAL;
     if (per_iteration) *per_iteration = h->launches_per_iter;
-    if (last_solve_total) *last_solve_total = h->launches_last_solve;
+    if (last_solve_total) *last_solve_total = h->launches_executed;
     return P2G_OK;
 }
 

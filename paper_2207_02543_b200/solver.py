@@ -250,6 +250,10 @@ class BatchSolver:
                     "profile_iteration")
         return {names[i].decode(): (float(ms[i]), float(by[i])) for i in range(L.NUM_KCLASS)}
 
+    def stream(self) -> int:
+        """cudaStream_t of the handle (all its kernels run there)."""
+        return int(self._L.p2g_get_stream(self._h) or 0)
+
     def launch_counts(self):
         a, b = C.c_int64(), C.c_int64()
         self._check(self._L.p2g_launch_counts(self._h, C.byref(a), C.byref(b)))
