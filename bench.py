@@ -165,14 +165,13 @@ def main():
     if ws > 1:
         dist.init_process_group("nccl", init_method="env://")
     from paper_2207_02543_b200 import _lib as L
+    from paper_2207_02543_b200 import dist as D
     from paper_2207_02543_b200.solver import BatchSolver
 
     # ---- inputs (outside the timed region): basis, this rank's instances
     t0 = time.perf_counter()
     prob = PR.build_problem(cfg, device=local)
-    strong = cfg.batch > 64 and ws > 1          # c3/c4: split the batch
-    B = cfg.batch // ws if strong else cfg.batch
-    seeds = PR.query_seeds(cfg, B, offset=rank * B)
+    B, seeds, strong = PR.shard(cfg, ws, rank)
     values = prob.values(seeds)                 # [B][nnz] natural order (host)
     n, nnz = prob.mesh.n, prob.mesh.nnz
     F = np.ascontiguousarray(np.broadcast_to(prob.f, (B, n)))
@@ -217,12 +216,8 @@ def main():
         ev1.record(stream)
         barrier()
     launches = s.launch_counts()[1] - l0
-    ms = ev0.elapsed_time(ev1)
-    if ws > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    total_solves = B * args.steps * ws
+    ms = D.max_over_ranks(ev0.elapsed_time(ev1), dev)
+    total_solves = (cfg.batch if strong else B * ws) * args.steps
     value = total_solves / (ms / 1e3)
     iters = np.concatenate(iters_all)
 
@@ -269,11 +264,7 @@ def main():
             step_e2e()
         e1.record(stream)
         barrier()
-        ems = e0.elapsed_time(e1)
-        if ws > 1:
-            t = torch.tensor([ems], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = D.max_over_ranks(e0.elapsed_time(e1), dev)
         e2e = {"value": total_solves / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(values.nbytes + F.nbytes),
                "d2h_bytes_per_step": int(F.nbytes + 3 * 4 * B)}

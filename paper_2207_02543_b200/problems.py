@@ -53,6 +53,24 @@ CONFIGS = {
 }
 
 
+def shard(cfg: Config, world: int, rank: int):
+    """Instance sharding across `world` GPUs (BASELINE.json: independent
+    instances, no communication).  Configs with more than one 64-instance
+    tile (c3: 256) split the batch (strong scaling); otherwise every rank
+    solves its own full batch with disjoint seeds (weak scaling).
+    Returns (instances_on_rank, seeds, strong)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("shard: bad world/rank")
+    strong = cfg.batch > 64 and world > 1
+    if strong:
+        base, extra = divmod(cfg.batch, world)
+        count = base + (1 if rank < extra else 0)
+        offset = rank * base + min(rank, extra)
+    else:
+        count, offset = cfg.batch, rank * cfg.batch
+    return count, query_seeds(cfg, count, offset=offset), strong
+
+
 def snapshot_seeds(cfg: Config, count=None):
     """Seeds of the offline snapshots: disjoint from the query seeds."""
     count = cfg.n_snapshots if count is None else count

@@ -1,0 +1,58 @@
+"""World-size-2 gloo test of the instance-sharded multi-GPU path's host logic
+(bench.py under torchrun): disjoint shards, full coverage, max-over-ranks."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2207_02543_b200 import dist as D
+    from paper_2207_02543_b200 import problems as PR
+    out = {}
+    for name in ("c2", "c3"):
+        cfg = PR.CONFIGS[name]
+        n, seeds, strong = PR.shard(cfg, world, rank)
+        counts = D.gather_counts(np.array([n]))
+        allseeds = D.gather_counts(seeds.astype(np.int64)) if not strong or len(set(counts)) == 1 else None
+        out[name] = (counts.tolist(), None if allseeds is None else allseeds.tolist(), strong)
+    out["max"] = D.max_over_ranks(10.0 + rank)
+    if rank == 0:
+        q.put(out)
+    dist.destroy_process_group()
+
+
+def test_sharding_two_ranks_gloo():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from paper_2207_02543_b200 import problems as PR
+    counts, seeds, strong = out["c2"]
+    assert counts == [64, 64] and not strong and len(set(seeds)) == 128
+    counts, seeds, strong = out["c3"]
+    assert counts == [128, 128] and strong
+    assert seeds == PR.query_seeds(PR.CONFIGS["c3"]).astype(np.int64).tolist()
+    assert out["max"] == 11.0
