@@ -95,10 +95,13 @@ struct p2g_handle {
 
     // graph
     cudaGraphExec_t loop_exec = nullptr;
+    std::vector<uint64_t> graph_key;  // what the captured graph baked in
     cudaGraphConditionalHandle cond = 0;
 
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     std::vector<std::pair<const void*, int>> occ_cache;
+    std::vector<std::pair<void*, size_t>> caps;  // ensure() capacities
+    double *d_Y = nullptr, *d_part_ac = nullptr;  // setup workspaces
     double last_ms[2] = {0, 0};
     int64_t launches_per_iter = 0, launches_last_solve = 0, launch_counter = 0;
     int64_t launches_executed = 0;  // every kernel this handle ran (graph iterations included)
@@ -146,6 +149,23 @@ int dalloc(p2g_handle* h, T*& p, size_t count) {
     dfree(p);
     if (count == 0) count = 1;
     CU(cudaMalloc(&p, count * sizeof(T)));
+    return P2G_OK;
+}
+
+// grow-only workspace: reallocates only when `count` exceeds the capacity
+// (no cudaMalloc/cudaFree on the per-batch path once sizes are stable)
+template <class T>
+int ensure(p2g_handle* h, T*& p, size_t count) {
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    for (auto& c : h->caps)
+        if (c.first == (void*)&p) {
+            if (p && c.second >= bytes) return P2G_OK;
+            TRY(dalloc(h, p, std::max<size_t>(count, 1)));
+            c.second = bytes;
+            return P2G_OK;
+        }
+    TRY(dalloc(h, p, std::max<size_t>(count, 1)));
+    h->caps.emplace_back((void*)&p, bytes);
     return P2G_OK;
 }
 
@@ -504,17 +524,13 @@ struct Run {
         int Bt = h->Bp;
         while (Bt > MSh::T && (size_t)n * k * Bt * 8 > ((size_t)4 << 30)) Bt /= 2;
         Bt = std::max(Bt, MSh::T);
-        double* Y = nullptr;
-        double* part = nullptr;
-        CU(cudaMalloc(&Y, (size_t)n * k * Bt * sizeof(double)));
         const int ncol = k * Bt;
         int occ_blocks = h->num_sms * 2;
         const size_t part_count = (size_t)occ_blocks * k * ncol;
-        if (cudaMalloc(&part, part_count * sizeof(double)) != cudaSuccess) {
-            cudaFree(Y);
-            h->err = "coarse_setup: out of device memory";
-            return P2G_ECUDA;
-        }
+        TRY(ensure(h, h->d_Y, (size_t)n * k * Bt));
+        TRY(ensure(h, h->d_part_ac, part_count));
+        double* Y = h->d_Y;
+        double* part = h->d_part_ac;
         int st = P2G_OK;
         for (int bofs = 0; bofs < h->Bp && st == P2G_OK; bofs += Bt) {
             KSWITCH(k, {
@@ -536,8 +552,6 @@ struct Run {
             if (cudaGetLastError() != cudaSuccess) st = P2G_ECUDA;
         }
         cudaStreamSynchronize(h->stream);
-        cudaFree(Y);
-        cudaFree(part);
         if (st != P2G_OK) {
             h->err = "coarse_setup: kernel launch failed";
             return st;
@@ -669,7 +683,7 @@ int set_values_impl(p2g_handle* h, int32_t batch, const double* host, const doub
     REQ(h->have_pattern, P2G_ESTATE, "p2g_set_values: pattern not set");
     REQ(batch >= 1, P2G_EINVAL, "p2g_set_values: batch must be >= 1");
     REQ(host || dev, P2G_EINVAL, "p2g_set_values: null values");
-    destroy_graph(h);
+    
     h->setup_done = false;
     const int oldBp = h->Bp;
     const int oldB = h->B;
@@ -677,15 +691,24 @@ int set_values_impl(p2g_handle* h, int32_t batch, const double* host, const doub
     choose_shape(h, batch);
     if (h->Bp != oldBp || oldB != batch || !h->d_vals) TRY(alloc_batch(h));
     if (h->k >= 0) {
-        TRY(dalloc(h, h->d_e, (size_t)std::max(h->k, 1) * h->Bp));
-        TRY(dalloc(h, h->d_L, (size_t)std::max(h->k * h->k, 1) * h->Bp));
-        TRY(dalloc(h, h->d_Ac, (size_t)std::max(h->k * h->k, 1) * h->Bp));
-        TRY(dalloc(h, h->d_part_c, (size_t)h->nb_cap * std::max(h->k, 1) * h->Bp));
+        TRY(ensure(h, h->d_e, (size_t)std::max(h->k, 1) * h->Bp));
+        TRY(ensure(h, h->d_L, (size_t)std::max(h->k * h->k, 1) * h->Bp));
+        TRY(ensure(h, h->d_Ac, (size_t)std::max(h->k * h->k, 1) * h->Bp));
+        TRY(ensure(h, h->d_part_c, (size_t)h->nb_cap * std::max(h->k, 1) * h->Bp));
     }
     TRY(upload_interleaved(h, host, dev, h->pat.nnz, h->d_vperm, h->d_vals));
     CU(cudaStreamSynchronize(h->stream));
     h->have_values = true;
     return P2G_OK;
+}
+
+std::vector<uint64_t> graph_key_of(p2g_handle* h) {
+    auto u = [](const void* p) { return (uint64_t)(uintptr_t)p; };
+    return {u(h->d_vals), u(h->d_phi), u(h->d_e), u(h->d_L), u(h->d_part_c), u(h->d_u), u(h->d_r),
+            u(h->d_s), u(h->d_s2), u(h->d_p), u(h->d_Kp), u(h->d_hist), (uint64_t)h->Bp,
+            (uint64_t)h->B, (uint64_t)h->k, (uint64_t)h->shape, (uint64_t)h->cfg.smoother,
+            (uint64_t)h->cfg.pre_sweeps, (uint64_t)h->cfg.post_sweeps,
+            (uint64_t)h->cfg.residual_form, (uint64_t)std::llround(h->cfg.omega * 1e15)};
 }
 
 int build_loop_graph(p2g_handle* h) {
@@ -733,6 +756,7 @@ int build_loop_graph(p2g_handle* h) {
         return P2G_ECUDA;
     }
     h->launches_per_iter = h->launch_counter - before;
+    h->graph_key = graph_key_of(h);
     cudaError_t ie = cudaGraphInstantiate(&h->loop_exec, outer, 0);
     cudaGraphDestroy(outer);
     if (ie != cudaSuccess) {
@@ -758,7 +782,7 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
         TRY(dalloc(h, h->d_hist, (size_t)cap_dev * h->Bp));
         h->hist_cap_alloc = cap_dev;
     }
-    if (!h->loop_exec) TRY(build_loop_graph(h));
+    if (!h->loop_exec || h->graph_key != graph_key_of(h)) TRY(build_loop_graph(h));
     const int64_t lc0 = h->launches_executed;
     SolveParams prm{tol, (long long)max_iter, (long long)hist_cap};
     CU(cudaMemcpyAsync(h->d_prm, &prm, sizeof(prm), cudaMemcpyHostToDevice, h->stream));
@@ -920,6 +944,8 @@ int p2g_destroy(p2g_handle* h) {
         dfree(*p);
     dfree(h->d_prm);
     dfree(h->d_flag_ticket);
+    dfree(h->d_Y);
+    dfree(h->d_part_ac);
     for (auto& e : h->ev) cudaEventDestroy(e);
     for (auto& e : h->kev) cudaEventDestroy(e);
     cudaStreamDestroy(h->stream);
@@ -979,21 +1005,21 @@ int p2g_set_basis(p2g_handle* h, int32_t k, const double* phi) {
     REQ(h->have_pattern, P2G_ESTATE, "p2g_set_basis: pattern not set");
     REQ(k >= 0 && k <= 64, P2G_EINVAL, "p2g_set_basis: rank must lie in [0, 64]");
     REQ(k == 0 || phi, P2G_EINVAL, "p2g_set_basis: null basis");
-    destroy_graph(h);
+    
     h->setup_done = false;
     h->k = k;
     const int64_t n = h->pat.n;
     std::vector<double> perm_phi((size_t)n * std::max(k, 1), 0.0);
     for (int64_t i = 0; i < n; ++i)
         for (int a = 0; a < k; ++a) perm_phi[i * k + a] = phi[h->pat.perm[i] * k + a];
-    TRY(dalloc(h, h->d_phi, perm_phi.size()));
+    TRY(ensure(h, h->d_phi, perm_phi.size()));
     CU(cudaMemcpy(h->d_phi, perm_phi.data(), sizeof(double) * perm_phi.size(),
                   cudaMemcpyHostToDevice));
     if (h->Bp > 0) {
-        TRY(dalloc(h, h->d_e, (size_t)std::max(k, 1) * h->Bp));
-        TRY(dalloc(h, h->d_L, (size_t)std::max(k * k, 1) * h->Bp));
-        TRY(dalloc(h, h->d_Ac, (size_t)std::max(k * k, 1) * h->Bp));
-        TRY(dalloc(h, h->d_part_c, (size_t)h->nb_cap * std::max(k, 1) * h->Bp));
+        TRY(ensure(h, h->d_e, (size_t)std::max(k, 1) * h->Bp));
+        TRY(ensure(h, h->d_L, (size_t)std::max(k * k, 1) * h->Bp));
+        TRY(ensure(h, h->d_Ac, (size_t)std::max(k * k, 1) * h->Bp));
+        TRY(ensure(h, h->d_part_c, (size_t)h->nb_cap * std::max(k, 1) * h->Bp));
     }
     return P2G_OK;
 }
@@ -1013,7 +1039,7 @@ int p2g_setup(p2g_handle* h, const p2g_config* cfg, int32_t* status) {
         "jacobi_sweep: omega outside (0,1]");
     REQ(c.residual_form == P2G_RESIDUAL_FULL || c.residual_form == P2G_RESIDUAL_UPPER, P2G_EINVAL,
         "p2g_setup: unknown residual form");
-    destroy_graph(h);
+    
     h->cfg = c;
     CU(cudaMemsetAsync(h->d_setup_status, 0, sizeof(int) * h->Bp, h->stream));
     {
