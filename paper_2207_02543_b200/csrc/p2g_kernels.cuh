@@ -312,8 +312,17 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_spmv(Mat A, const double
     if constexpr (DOT) cluster_partial<Sh>(dacc, part, A.Bp, false);
 }
 
-// r = f - K u (csr.hpp:96-105) with partials of r.r and f.f (for ||r0||, ||f||)
-template <class Sh>
+enum : int { RES_UPPER = 0, RES_FULL = 1, RES_VECTOR = 2 };
+
+// Residual of the pre-smoothed correction, written to r (the restriction's
+// input t, pod.hpp:198-199):
+//   RES_FULL : r = f - K u (csr.hpp:96-105: row sum first, then subtract),
+//              optional partials of r.r and f.f (||r0||, ||f||, krylov.hpp:252-256)
+//   RES_UPPER: r = -U u -- after ONE forward GS sweep from zero,
+//              (D + L) u = f row by row, so f - K u = -U u (same value up to
+//              rounding, half the matrix traffic: only the strictly upper
+//              entries of each row are read)
+template <class Sh, int FORM>
 __global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_residual(Mat A, const double* __restrict__ f,
                                                      const double* __restrict__ u,
                                                      double* __restrict__ r, const int* active,
@@ -334,17 +343,26 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_residual(Mat A, const do
             double acc[Sh::V];
 #pragma unroll
             for (int v = 0; v < Sh::V; ++v) acc[v] = 0.0;
-            if (valid && any) row_dot<Sh>(A, u, b0, __ldg(A.rp + i), __ldg(A.rp + i + 1), G.s, acc);
+            if (valid && any) {
+                const int k0 = FORM == RES_UPPER ? __ldg(A.dpos + i) + 1 : __ldg(A.rp + i);
+                row_dot<Sh>(A, u, b0, k0, __ldg(A.rp + i + 1), G.s, acc);
+            }
 #pragma unroll
             for (int v = 0; v < Sh::V; ++v) acc[v] = slot_sum<Sh>(acc[v]);
             if (valid && any && G.s == 0) {
-                double fi[Sh::V], ri[Sh::V];
-                ldv<Sh::V>(fi, f + (size_t)i * A.Bp + b0);
+                double ri[Sh::V];
+                if constexpr (FORM == RES_UPPER) {
 #pragma unroll
-                for (int v = 0; v < Sh::V; ++v) {
-                    ri[v] = __dsub_rn(fi[v], acc[v]);
-                    rr[v] = __dadd_rn(rr[v], __dmul_rn(ri[v], ri[v]));
-                    ff[v] = __dadd_rn(ff[v], __dmul_rn(fi[v], fi[v]));
+                    for (int v = 0; v < Sh::V; ++v) ri[v] = -acc[v];
+                } else {
+                    double fi[Sh::V];
+                    ldv<Sh::V>(fi, f + (size_t)i * A.Bp + b0);
+#pragma unroll
+                    for (int v = 0; v < Sh::V; ++v) {
+                        ri[v] = __dsub_rn(fi[v], acc[v]);
+                        rr[v] = __dadd_rn(rr[v], __dmul_rn(ri[v], ri[v]));
+                        ff[v] = __dadd_rn(ff[v], __dmul_rn(fi[v], fi[v]));
+                    }
                 }
                 stv<Sh::V>(r + (size_t)i * A.Bp + b0, ri, m);
             }
@@ -520,20 +538,17 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_jacobi(Mat A, const doub
     if constexpr (LAST) cluster_partial<Sh>(rs, part_rs, A.Bp, false);
 }
 
-enum : int { RES_UPPER = 0, RES_FULL = 1, RES_VECTOR = 2 };
-
-// Fused residual + restriction (pod.hpp:198-200: t = f - K s; c = Phi^T t),
-// t never stored.  FORM: RES_FULL  t_i = f_i - sum_j K_ij s_j (reference form)
-//                        RES_UPPER t_i = -sum_{j>i} K_ij s_j (after the first
-//                                  forward sweep from zero, see header)
-//                        RES_VECTOR t_i = f_i (restriction of f itself:
-//                                  reduced_solve's project(f), pod.hpp:171)
-// part[blk][a][b] = sum over the block's rows of phi[i][a] * t_i.
-template <class Sh, int KMAX, int FORM>
-__global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_restrict(Mat A, const double* __restrict__ f,
-                                                     const double* __restrict__ s,
-                                                     const double* __restrict__ phi, int k,
-                                                     const int* active, double* part) {
+// Restriction c = Phi^T t (PodBasis::project, pod.hpp:27-35) of a vector
+// t[n][Bp] (the residual, or f itself for reduced_solve, pod.hpp:171).
+// Lanes: R = 32/W rows x W instance lanes x V instances; each lane keeps the
+// k coefficients of its V instances in registers and reads its row of Phi
+// with 16-byte vector loads.  Partials: one row per cluster (DSMEM),
+// part[cluster][a][b].
+template <class Sh, int KMAX>
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_restrict_vec(int n, int Bp,
+                                                         const double* __restrict__ t,
+                                                         const double* __restrict__ phi, int k,
+                                                         const int* active, double* part) {
     LaneGeo<Sh> G;
     const int b0 = blockIdx.y * Sh::T + G.w * Sh::V;
     bool m[Sh::V], any;
@@ -543,45 +558,33 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_restrict(Mat A, const do
     for (int a = 0; a < KMAX; ++a)
 #pragma unroll
         for (int v = 0; v < Sh::V; ++v) acc[a][v] = 0.0;
-    const int nn = A.n / A.bs;
-    P2G_NODE_LOOP(Sh, 0, nn, G) {
-        const int node = base_ + G.r;
-        const bool valid = node < nn;
-        for (int c = 0; c < A.bs; ++c) {
-            const int i = node * A.bs + c;
-            double t[Sh::V];
+    const bool keven = (k & 1) == 0;
+    for (int base = (blockIdx.x * kWarps + G.warp) * Sh::R; base < n;
+         base += gridDim.x * kWarps * Sh::R) {
+        const int i = base + G.r;
+        if (i >= n || !any) continue;
+        double tv[Sh::V];
+        ldv<Sh::V>(tv, t + (size_t)i * Bp + b0);
+        const double* ph = phi + (size_t)i * k;
+        if (keven) {
 #pragma unroll
-            for (int v = 0; v < Sh::V; ++v) t[v] = 0.0;
-            if constexpr (FORM != RES_VECTOR) {
-                if (valid && any) {
-                    const int kb = __ldg(A.rp + i), ke = __ldg(A.rp + i + 1);
-                    if (FORM == RES_UPPER)
-                        row_dot<Sh>(A, s, b0, __ldg(A.dpos + i) + 1, ke, G.s, t);
-                    else
-                        row_dot<Sh>(A, s, b0, kb, ke, G.s, t);
-                }
+            for (int a = 0; a < KMAX; a += 2) {
+                if (a < k) {
+                    const double2 p2 = __ldg(reinterpret_cast<const double2*>(ph + a));
 #pragma unroll
-                for (int v = 0; v < Sh::V; ++v) t[v] = slot_sum<Sh>(t[v]);
-            }
-            if (valid && any && G.s == 0) {
-                if constexpr (FORM == RES_UPPER) {
-#pragma unroll
-                    for (int v = 0; v < Sh::V; ++v) t[v] = -t[v];
-                } else {
-                    double fi[Sh::V];
-                    ldv<Sh::V>(fi, f + (size_t)i * A.Bp + b0);
-#pragma unroll
-                    for (int v = 0; v < Sh::V; ++v)
-                        t[v] = FORM == RES_FULL ? __dsub_rn(fi[v], t[v]) : fi[v];
-                }
-                const double* ph = phi + (size_t)i * k;
-#pragma unroll
-                for (int a = 0; a < KMAX; ++a) {
-                    if (a < k) {
-                        const double pa = __ldg(ph + a);
-#pragma unroll
-                        for (int v = 0; v < Sh::V; ++v) acc[a][v] = fma(pa, t[v], acc[a][v]);
+                    for (int v = 0; v < Sh::V; ++v) {
+                        acc[a][v] = fma(p2.x, tv[v], acc[a][v]);
+                        acc[a + 1][v] = fma(p2.y, tv[v], acc[a + 1][v]);
                     }
+                }
+            }
+        } else {
+#pragma unroll
+            for (int a = 0; a < KMAX; ++a) {
+                if (a < k) {
+                    const double pa = __ldg(ph + a);
+#pragma unroll
+                    for (int v = 0; v < Sh::V; ++v) acc[a][v] = fma(pa, tv[v], acc[a][v]);
                 }
             }
         }
@@ -605,23 +608,23 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_restrict(Mat A, const do
         __syncthreads();
         for (int e = threadIdx.x; e < 8 * Sh::T; e += kBlock) {
             const int j = e / Sh::T, bt = e % Sh::T;
-            double t = 0.0;
+            double tt = 0.0;
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) t += sm[w][j][bt];
-            tot[a0 + j][bt] = t;
+            for (int w = 0; w < kWarps; ++w) tt += sm[w][j][bt];
+            tot[a0 + j][bt] = tt;
         }
         __syncthreads();
     }
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();
     if (cl.block_rank() == 0) {
-        double* prow = part + (size_t)(blockIdx.x / kCluster) * k * A.Bp + blockIdx.y * Sh::T;
+        double* prow = part + (size_t)(blockIdx.x / kCluster) * k * Bp + blockIdx.y * Sh::T;
         for (int e = threadIdx.x; e < k * Sh::T; e += kBlock) {
             const int a = e / Sh::T, bt = e % Sh::T;
-            double t = 0.0;
+            double tt = 0.0;
 #pragma unroll
-            for (int r = 0; r < kCluster; ++r) t += cl.map_shared_rank(&tot[0][0], r)[a * Sh::T + bt];
-            prow[(size_t)a * A.Bp + bt] = t;
+            for (int r = 0; r < kCluster; ++r) tt += cl.map_shared_rank(&tot[0][0], r)[a * Sh::T + bt];
+            prow[(size_t)a * Bp + bt] = tt;
         }
     }
     cl.sync();
@@ -674,29 +677,43 @@ __global__ void __launch_bounds__(kBlock) k_coarse(int Bp, int k, int nblk, cons
 // Prolongation + add (pod.hpp:201-202: corr = lift(e); u += 1.0 * corr), the
 // lift sum in ascending coefficient order like PodBasis::lift (pod.hpp:40-44).
 // ASSIGN: s = corr (reduced_solve's lift into a fresh vector, pod.hpp:178).
+// Same lane layout as k_restrict_vec; e (k x V) lives in registers.
 template <class Sh, int KMAX, bool ASSIGN>
-__global__ void __launch_bounds__(kBlock) k_prolong(Mat A, double* s, const double* __restrict__ phi,
-                                                    int k, const double* __restrict__ e,
+__global__ void __launch_bounds__(kBlock) k_prolong(int n, int Bp, double* s,
+                                                    const double* __restrict__ phi, int k,
+                                                    const double* __restrict__ e,
                                                     const int* active) {
     LaneGeo<Sh> G;
     const int b0 = blockIdx.y * Sh::T + G.w * Sh::V;
     bool m[Sh::V], any;
     lane_mask<Sh>(active, b0, m, any);
-    if (!any || G.s != 0) return;
+    if (!any) return;
     double ev[KMAX][Sh::V];
 #pragma unroll
     for (int a = 0; a < KMAX; ++a)
-        if (a < k) ldv<Sh::V>(ev[a], e + (size_t)a * A.Bp + b0);
-    const int nn = A.n / A.bs;
-    P2G_NODE_LOOP(Sh, 0, nn, G) {
-        const int node = base_ + G.r;
-        if (node >= nn) continue;
-        for (int c = 0; c < A.bs; ++c) {
-            const int i = node * A.bs + c;
-            const double* ph = phi + (size_t)i * k;
-            double corr[Sh::V];
+        if (a < k) ldv<Sh::V>(ev[a], e + (size_t)a * Bp + b0);
+    const bool keven = (k & 1) == 0;
+    for (int base = (blockIdx.x * kWarps + G.warp) * Sh::R; base < n;
+         base += gridDim.x * kWarps * Sh::R) {
+        const int i = base + G.r;
+        if (i >= n) continue;
+        const double* ph = phi + (size_t)i * k;
+        double corr[Sh::V];
 #pragma unroll
-            for (int v = 0; v < Sh::V; ++v) corr[v] = 0.0;
+        for (int v = 0; v < Sh::V; ++v) corr[v] = 0.0;
+        if (keven) {
+#pragma unroll
+            for (int a = 0; a < KMAX; a += 2) {
+                if (a < k) {
+                    const double2 p2 = __ldg(reinterpret_cast<const double2*>(ph + a));
+#pragma unroll
+                    for (int v = 0; v < Sh::V; ++v) {
+                        corr[v] = __dadd_rn(corr[v], __dmul_rn(p2.x, ev[a][v]));
+                        corr[v] = __dadd_rn(corr[v], __dmul_rn(p2.y, ev[a + 1][v]));
+                    }
+                }
+            }
+        } else {
 #pragma unroll
             for (int a = 0; a < KMAX; ++a) {
                 if (a < k) {
@@ -705,17 +722,25 @@ __global__ void __launch_bounds__(kBlock) k_prolong(Mat A, double* s, const doub
                     for (int v = 0; v < Sh::V; ++v) corr[v] = __dadd_rn(corr[v], __dmul_rn(pa, ev[a][v]));
                 }
             }
-            const size_t o = (size_t)i * A.Bp + b0;
-            if constexpr (!ASSIGN) {
-                double si[Sh::V];
-                ldv<Sh::V>(si, s + o);
-#pragma unroll
-                for (int v = 0; v < Sh::V; ++v) corr[v] = __dadd_rn(si[v], corr[v]);
-            }
-            stv<Sh::V>(s + o, corr, m);
         }
+        const size_t o = (size_t)i * Bp + b0;
+        if constexpr (!ASSIGN) {
+            double si[Sh::V];
+            ldv<Sh::V>(si, s + o);
+#pragma unroll
+            for (int v = 0; v < Sh::V; ++v) corr[v] = __dadd_rn(si[v], corr[v]);
+        }
+        stv<Sh::V>(s + o, corr, m);
     }
 }
+
+// shape of the row-local kernels (restriction, prolongation): R = 32/W rows
+// per warp, one instance per lane unless k is small enough for two
+template <class Sh, int KMAX>
+struct LocalShape {
+    static constexpr int V = (Sh::V == 2 && KMAX <= 24) ? 2 : 1;
+    using type = Shape<32 / Sh::W, 1, Sh::W, V>;
+};
 
 // p = s + beta p (krylov.hpp:282); INIT: p = s (krylov.hpp:263)
 template <class Sh, bool INIT>

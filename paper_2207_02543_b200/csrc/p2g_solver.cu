@@ -276,7 +276,7 @@ struct Run {
 
     static int residual(p2g_handle* h, const double* f, const double* u, double* r, int* nb_out) {
         Mat A = mat_of(h);
-        auto fn = k_residual<Sh>;
+        auto fn = k_residual<Sh, RES_FULL>;
         dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn, true);
         fn<<<g, kBlock, 0, h->stream>>>(A, f, u, r, h->d_active, h->d_part_rr, h->d_part_ff);
         *nb_out = g.x / kCluster;
@@ -375,26 +375,37 @@ struct Run {
         return P2G_OK;
     }
 
+    // c = Phi^T t with t = FORM(f, s) (RES_VECTOR: t = f).  The residual is
+    // written to the Kp buffer (free between the update and the next SpMV).
     static int restrict_(p2g_handle* h, int form, const double* f, const double* s, int* nb_out) {
         Mat A = mat_of(h);
-        const int k = h->k;
-        KSWITCH(k, {
+        const double* t = f;
+        if (form != RES_VECTOR) {
+            double* tb = h->d_Kp;
             if (form == RES_UPPER) {
-                auto fn = k_restrict<ASh, KM, RES_UPPER>;
-                dim3 g = node_grid<ASh>(h, nnodes(h), (const void*)fn, true);
-                fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_phi, k, h->d_active, h->d_part_c);
-                *nb_out = g.x / kCluster;
-            } else if (form == RES_FULL) {
-                auto fn = k_restrict<ASh, KM, RES_FULL>;
-                dim3 g = node_grid<ASh>(h, nnodes(h), (const void*)fn, true);
-                fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_phi, k, h->d_active, h->d_part_c);
-                *nb_out = g.x / kCluster;
+                auto fn = k_residual<Sh, RES_UPPER>;
+                dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn, true);
+                fn<<<g, kBlock, 0, h->stream>>>(A, f, s, tb, h->d_active, nullptr, nullptr);
             } else {
-                auto fn = k_restrict<ASh, KM, RES_VECTOR>;
-                dim3 g = node_grid<ASh>(h, nnodes(h), (const void*)fn, true);
-                fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_phi, k, h->d_active, h->d_part_c);
-                *nb_out = g.x / kCluster;
+                auto fn = k_residual<Sh, RES_FULL>;
+                dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn, true);
+                fn<<<g, kBlock, 0, h->stream>>>(A, f, s, tb, h->d_active, nullptr, nullptr);
             }
+            count_launch(h, KC_RESTRICT);
+            t = tb;
+        }
+        const int k = h->k;
+        const int n = static_cast<int>(h->pat.n);
+        KSWITCH(k, {
+            using LSh = typename LocalShape<Sh, KM>::type;
+            auto fn = k_restrict_vec<LSh, KM>;
+            const int64_t need = (n + kWarps * LSh::R - 1) / (kWarps * LSh::R);
+            int64_t gx = std::min<int64_t>(need, resident_ctas(h, (const void*)fn, true));
+            gx = std::min<int64_t>(std::max<int64_t>(gx, 1), h->nb_cap);
+            gx = (gx + kCluster - 1) / kCluster * kCluster;
+            dim3 g((unsigned)gx, (unsigned)(h->Bp / LSh::T));
+            fn<<<g, kBlock, 0, h->stream>>>(n, h->Bp, t, h->d_phi, k, h->d_active, h->d_part_c);
+            *nb_out = g.x / kCluster;
         });
         count_launch(h, KC_RESTRICT);
         CU(cudaGetLastError());
@@ -410,18 +421,15 @@ struct Run {
     }
 
     static int prolong(p2g_handle* h, double* s, bool assign) {
-        Mat A = mat_of(h);
         const int k = h->k;
+        const int n = static_cast<int>(h->pat.n);
         KSWITCH(k, {
-            if (assign) {
-                auto fn = k_prolong<ASh, KM, true>;
-                dim3 g = node_grid<ASh>(h, nnodes(h), (const void*)fn);
-                fn<<<g, kBlock, 0, h->stream>>>(A, s, h->d_phi, k, h->d_e, h->d_active);
-            } else {
-                auto fn = k_prolong<ASh, KM, false>;
-                dim3 g = node_grid<ASh>(h, nnodes(h), (const void*)fn);
-                fn<<<g, kBlock, 0, h->stream>>>(A, s, h->d_phi, k, h->d_e, h->d_active);
-            }
+            using LSh = typename LocalShape<Sh, KM>::type;
+            auto fn = assign ? k_prolong<LSh, KM, true> : k_prolong<LSh, KM, false>;
+            const int64_t need = (n + kWarps * LSh::R - 1) / (kWarps * LSh::R);
+            int64_t gx = std::min<int64_t>(need, resident_ctas(h, (const void*)fn, false));
+            dim3 g((unsigned)std::max<int64_t>(gx, 1), (unsigned)(h->Bp / LSh::T));
+            fn<<<g, kBlock, 0, h->stream>>>(n, h->Bp, s, h->d_phi, k, h->d_e, h->d_active);
         });
         count_launch(h, KC_PROLONG);
         CU(cudaGetLastError());
