@@ -41,6 +41,10 @@ constexpr int kBlock = kWarps * 32;
 // partial row (8x fewer rows for the per-instance scalar reductions).
 constexpr int kCluster = 8;
 #define P2G_CLUSTER __cluster_dims__(kCluster, 1, 1)
+// Streaming row kernels are latency bound unless the SM is full: cap them at
+// 32 registers so 8 CTAs x 8 warps (100% occupancy) stay resident (the
+// difference between 4.4 and 6.3 TB/s for the batched SpMV, tools/spmv_lab.cu).
+#define P2G_ROWK __launch_bounds__(kBlock, 8)
 
 template <int R_, int S_, int W_, int V_>
 struct Shape {
@@ -275,7 +279,7 @@ __device__ __forceinline__ void lane_mask(const int* active, int b0, bool (&m)[S
 // y = K x (csr.hpp:83-93) on all rows; DOT: partial of x.y per instance
 // (krylov.hpp:272-273: Kp = spmv(K,p); pKp = dot(p, Kp)).
 template <class Sh, bool DOT>
-__global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_spmv(Mat A, const double* __restrict__ x,
+__global__ void P2G_CLUSTER P2G_ROWK k_spmv(Mat A, const double* __restrict__ x,
                                                  double* __restrict__ y, const int* active,
                                                  double* part) {
     LaneGeo<Sh> G;
@@ -323,7 +327,7 @@ enum : int { RES_UPPER = 0, RES_FULL = 1, RES_VECTOR = 2 };
 //              rounding, half the matrix traffic: only the strictly upper
 //              entries of each row are read)
 template <class Sh, int FORM>
-__global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_residual(Mat A, const double* __restrict__ f,
+__global__ void P2G_CLUSTER P2G_ROWK k_residual(Mat A, const double* __restrict__ f,
                                                      const double* __restrict__ u,
                                                      double* __restrict__ r, const int* active,
                                                      double* part_rr, double* part_ff) {
@@ -382,7 +386,7 @@ enum : int { PRE_NONE = 0, PRE_GS = 1, PRE_JACOBI = 2 };
 //            JACOBI: s_i = omega * r_i / d_i on every row (first sweep from 0,
 //            smoothers.hpp:84-85 with u = 0)
 template <class Sh, bool UPDATE, int PRE>
-__global__ void P2G_CLUSTER __launch_bounds__(kBlock)
+__global__ void P2G_CLUSTER P2G_ROWK
     k_update_pre(Mat A, double* __restrict__ u, double* __restrict__ r, const double* __restrict__ p,
                  const double* __restrict__ Kp, double* __restrict__ s, const double* alpha,
                  const int* active, double* part_rr, int color0_nodes, double omega) {
@@ -444,7 +448,7 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock)
 
 // Forward GS colour phase: nodes [nb, ne) of one colour, dofs ascending.
 template <class Sh, bool FIRST>
-__global__ void __launch_bounds__(kBlock) k_gs_forward(Mat A, const double* __restrict__ f,
+__global__ void P2G_ROWK k_gs_forward(Mat A, const double* __restrict__ f,
                                                        double* s, const int* active, int nb,
                                                        int ne) {
     LaneGeo<Sh> G;
@@ -463,7 +467,7 @@ __global__ void __launch_bounds__(kBlock) k_gs_forward(Mat A, const double* __re
 // (gauss_seidel_sweep_backward, smoothers.hpp:56-70); LAST: partial of r.s
 // over this colour's rows (krylov.hpp:280 rs_new = dot(r, s)).
 template <class Sh, bool LAST>
-__global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_gs_backward(Mat A, const double* __restrict__ f,
+__global__ void P2G_CLUSTER P2G_ROWK k_gs_backward(Mat A, const double* __restrict__ f,
                                                         double* s, const int* active, int nb,
                                                         int ne, double* part_rs, int accumulate) {
     LaneGeo<Sh> G;
@@ -496,7 +500,7 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_gs_backward(Mat A, const
 // Damped Jacobi sweep, out of place (smoothers.hpp:83-86):
 //   s_out_i = s_i + omega * (f_i - (K s)_i) / d_i ; LAST: partial of f.s_out
 template <class Sh, bool LAST>
-__global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_jacobi(Mat A, const double* __restrict__ f,
+__global__ void P2G_CLUSTER P2G_ROWK k_jacobi(Mat A, const double* __restrict__ f,
                                                    const double* __restrict__ s,
                                                    double* __restrict__ s_out, const int* active,
                                                    double omega, double* part_rs) {
@@ -559,6 +563,7 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_restrict_vec(int n, int 
 #pragma unroll
         for (int v = 0; v < Sh::V; ++v) acc[a][v] = 0.0;
     const bool keven = (k & 1) == 0;
+#pragma unroll 2
     for (int base = (blockIdx.x * kWarps + G.warp) * Sh::R; base < n;
          base += gridDim.x * kWarps * Sh::R) {
         const int i = base + G.r;
@@ -675,7 +680,8 @@ __global__ void __launch_bounds__(kBlock) k_coarse(int Bp, int k, int nblk, cons
 }
 
 // Prolongation + add (pod.hpp:201-202: corr = lift(e); u += 1.0 * corr), the
-// lift sum in ascending coefficient order like PodBasis::lift (pod.hpp:40-44).
+// lift sum in ascending coefficient order like PodBasis::lift (pod.hpp:40-44)
+// with fused multiply-adds (rounding-level deviation, D4).
 // ASSIGN: s = corr (reduced_solve's lift into a fresh vector, pod.hpp:178).
 // Same lane layout as k_restrict_vec; e (k x V) lives in registers.
 template <class Sh, int KMAX, bool ASSIGN>
@@ -693,6 +699,7 @@ __global__ void __launch_bounds__(kBlock) k_prolong(int n, int Bp, double* s,
     for (int a = 0; a < KMAX; ++a)
         if (a < k) ldv<Sh::V>(ev[a], e + (size_t)a * Bp + b0);
     const bool keven = (k & 1) == 0;
+#pragma unroll 2
     for (int base = (blockIdx.x * kWarps + G.warp) * Sh::R; base < n;
          base += gridDim.x * kWarps * Sh::R) {
         const int i = base + G.r;
@@ -708,8 +715,8 @@ __global__ void __launch_bounds__(kBlock) k_prolong(int n, int Bp, double* s,
                     const double2 p2 = __ldg(reinterpret_cast<const double2*>(ph + a));
 #pragma unroll
                     for (int v = 0; v < Sh::V; ++v) {
-                        corr[v] = __dadd_rn(corr[v], __dmul_rn(p2.x, ev[a][v]));
-                        corr[v] = __dadd_rn(corr[v], __dmul_rn(p2.y, ev[a + 1][v]));
+                        corr[v] = fma(p2.x, ev[a][v], corr[v]);
+                        corr[v] = fma(p2.y, ev[a + 1][v], corr[v]);
                     }
                 }
             }
@@ -719,7 +726,7 @@ __global__ void __launch_bounds__(kBlock) k_prolong(int n, int Bp, double* s,
                 if (a < k) {
                     const double pa = __ldg(ph + a);
 #pragma unroll
-                    for (int v = 0; v < Sh::V; ++v) corr[v] = __dadd_rn(corr[v], __dmul_rn(pa, ev[a][v]));
+                    for (int v = 0; v < Sh::V; ++v) corr[v] = fma(pa, ev[a][v], corr[v]);
                 }
             }
         }
@@ -734,17 +741,167 @@ __global__ void __launch_bounds__(kBlock) k_prolong(int n, int Bp, double* s,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Tiled forms of the prolongation and restriction for batched tiles
+// (TB = 64 or 32 instances per blockIdx.y).  They are small dense products,
+//   S[n][TB] += Phi[n][k] E[k][TB]      and      C[k][TB] = Phi^T[k][n] T[n][TB],
+// so a CTA stages a 32-row tile of Phi (and of T) in shared memory and each
+// thread register-blocks 4 rows (prolong) or ceil(k/8) coefficients
+// (restrict) x TB/32 instances.  Same sums as the row-local kernels, FMA.
+constexpr int kRowTile = 32;
+// row tile: 32 rows, or 16 when k > 40 (static shared memory <= 48 KB)
+template <int KMAX>
+constexpr int row_tile() { return KMAX > 40 ? 16 : 32; }
+
+template <int TB, int KMAX, bool ASSIGN>
+__global__ void __launch_bounds__(kBlock) k_prolong_tiled(int n, int Bp, double* s,
+                                                          const double* __restrict__ phi, int k,
+                                                          const double* __restrict__ e,
+                                                          const int* active) {
+    constexpr int V = TB / 32;
+    constexpr int RT = row_tile<KMAX>(), RPW = RT / kWarps;  // rows per warp
+    __shared__ double Es[KMAX][TB];
+    __shared__ double Ps[RT][KMAX + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int bt0 = blockIdx.y * TB;
+    for (int q = threadIdx.x; q < k * TB; q += kBlock)
+        Es[q / TB][q % TB] = e[(size_t)(q / TB) * Bp + bt0 + q % TB];
+    bool m[V];
+    bool any = false;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        m[v] = active[bt0 + lane * V + v] != 0;
+        any |= m[v];
+    }
+    for (int r0 = blockIdx.x * RT; r0 < n; r0 += gridDim.x * RT) {
+        __syncthreads();  // Es ready / previous tile consumed
+        for (int q = threadIdx.x; q < RT * k; q += kBlock) {
+            const int rr = q / k, a = q % k;
+            Ps[rr][a] = (r0 + rr < n) ? __ldg(phi + (size_t)(r0 + rr) * k + a) : 0.0;
+        }
+        __syncthreads();
+        double corr[RPW][V];
+#pragma unroll
+        for (int j = 0; j < RPW; ++j)
+#pragma unroll
+            for (int v = 0; v < V; ++v) corr[j][v] = 0.0;
+#pragma unroll 4
+        for (int a = 0; a < k; ++a) {
+            double ev[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) ev[v] = Es[a][lane * V + v];
+#pragma unroll
+            for (int j = 0; j < RPW; ++j) {
+                const double p = Ps[warp + 8 * j][a];
+#pragma unroll
+                for (int v = 0; v < V; ++v) corr[j][v] = fma(p, ev[v], corr[j][v]);
+            }
+        }
+        if (any) {
+#pragma unroll
+            for (int j = 0; j < RPW; ++j) {
+                const int i = r0 + warp + 8 * j;
+                if (i < n) {
+                    double* sp = s + (size_t)i * Bp + bt0 + lane * V;
+                    double out[V];
+                    if constexpr (!ASSIGN) {
+                        ldv<V>(out, sp);
+#pragma unroll
+                        for (int v = 0; v < V; ++v) out[v] = __dadd_rn(out[v], corr[j][v]);
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < V; ++v) out[v] = corr[j][v];
+                    }
+                    stv<V>(sp, out, m);
+                }
+            }
+        }
+    }
+}
+
+template <int TB, int KMAX>
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_restrict_tiled(int n, int Bp,
+                                                           const double* __restrict__ t,
+                                                           const double* __restrict__ phi, int k,
+                                                           const int* active, double* part) {
+    constexpr int V = TB / 32;
+    constexpr int KPW = (KMAX + kWarps - 1) / kWarps;  // coefficients per warp
+    constexpr int RT = row_tile<KMAX>();
+    // staging tiles and the CTA totals share one buffer (totals written last)
+    constexpr int STAGE = RT * TB + RT * (KMAX + 1), TOT = KMAX * TB;
+    __shared__ double smem[STAGE > TOT ? STAGE : TOT];
+    double (*Ts)[TB] = reinterpret_cast<double (*)[TB]>(smem);
+    double (*Ps)[KMAX + 1] = reinterpret_cast<double (*)[KMAX + 1]>(smem + RT * TB);
+    double (*tot)[TB] = reinterpret_cast<double (*)[TB]>(smem);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int bt0 = blockIdx.y * TB;
+    double acc[KPW][V];
+#pragma unroll
+    for (int j = 0; j < KPW; ++j)
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[j][v] = 0.0;
+    for (int r0 = blockIdx.x * RT; r0 < n; r0 += gridDim.x * RT) {
+        __syncthreads();
+        for (int q = threadIdx.x; q < RT * TB; q += kBlock) {
+            const int rr = q / TB, b = q % TB;
+            Ts[rr][b] = (r0 + rr < n && active[bt0 + b]) ? t[(size_t)(r0 + rr) * Bp + bt0 + b] : 0.0;
+        }
+        for (int q = threadIdx.x; q < RT * k; q += kBlock) {
+            const int rr = q / k, a = q % k;
+            Ps[rr][a] = (r0 + rr < n) ? __ldg(phi + (size_t)(r0 + rr) * k + a) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int rr = 0; rr < RT; ++rr) {
+            double tv[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) tv[v] = Ts[rr][lane * V + v];
+#pragma unroll
+            for (int j = 0; j < KPW; ++j) {
+                const int a = warp + kWarps * j;
+                if (a < k) {
+                    const double p = Ps[rr][a];
+#pragma unroll
+                    for (int v = 0; v < V; ++v) acc[j][v] = fma(p, tv[v], acc[j][v]);
+                }
+            }
+        }
+    }
+    __syncthreads();  // staging tiles consumed: reuse the buffer for the totals
+#pragma unroll
+    for (int j = 0; j < KPW; ++j) {
+        const int a = warp + kWarps * j;
+        if (a < k) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) tot[a][lane * V + v] = acc[j][v];
+        }
+    }
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    if (cl.block_rank() == 0) {
+        double* prow = part + (size_t)(blockIdx.x / kCluster) * k * Bp + bt0;
+        for (int q = threadIdx.x; q < k * TB; q += kBlock) {
+            const int a = q / TB, b = q % TB;
+            double tt = 0.0;
+#pragma unroll
+            for (int r = 0; r < kCluster; ++r) tt += cl.map_shared_rank(smem, r)[a * TB + b];
+            prow[(size_t)a * Bp + b] = tt;
+        }
+    }
+    cl.sync();
+}
+
 // shape of the row-local kernels (restriction, prolongation): R = 32/W rows
 // per warp, one instance per lane unless k is small enough for two
 template <class Sh, int KMAX>
 struct LocalShape {
-    static constexpr int V = (Sh::V == 2 && KMAX <= 24) ? 2 : 1;
+    static constexpr int V = 1;
     using type = Shape<32 / Sh::W, 1, Sh::W, V>;
 };
 
 // p = s + beta p (krylov.hpp:282); INIT: p = s (krylov.hpp:263)
 template <class Sh, bool INIT>
-__global__ void __launch_bounds__(kBlock) k_pupdate(int n, int Bp, const double* __restrict__ s,
+__global__ void P2G_ROWK k_pupdate(int n, int Bp, const double* __restrict__ s,
                                                     double* __restrict__ p, const double* beta,
                                                     const int* active) {
     const int lane = threadIdx.x & 31, w = lane % Sh::W;

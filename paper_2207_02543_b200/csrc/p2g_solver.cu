@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -396,6 +397,22 @@ struct Run {
         }
         const int k = h->k;
         const int n = static_cast<int>(h->pat.n);
+        if constexpr (Sh::S == 1) {  // batched tiles: shared-memory tiled restriction
+            constexpr int TB = Sh::T;
+            KSWITCH(k, {
+                auto fn = k_restrict_tiled<TB, KM>;
+                const int64_t need = (n + row_tile<KM>() - 1) / row_tile<KM>();
+                int64_t gx = std::min<int64_t>(need, resident_ctas(h, (const void*)fn, true));
+                gx = std::min<int64_t>(std::max<int64_t>(gx, 1), h->nb_cap);
+                gx = (gx + kCluster - 1) / kCluster * kCluster;
+                dim3 g((unsigned)gx, (unsigned)(h->Bp / TB));
+                fn<<<g, kBlock, 0, h->stream>>>(n, h->Bp, t, h->d_phi, k, h->d_active, h->d_part_c);
+                *nb_out = g.x / kCluster;
+            });
+            count_launch(h, KC_RESTRICT);
+            CU(cudaGetLastError());
+            return P2G_OK;
+        }
         KSWITCH(k, {
             using LSh = typename LocalShape<Sh, KM>::type;
             auto fn = k_restrict_vec<LSh, KM>;
@@ -423,6 +440,19 @@ struct Run {
     static int prolong(p2g_handle* h, double* s, bool assign) {
         const int k = h->k;
         const int n = static_cast<int>(h->pat.n);
+        if constexpr (Sh::S == 1) {  // batched tiles: shared-memory tiled prolongation
+            constexpr int TB = Sh::T;
+            KSWITCH(k, {
+                auto fn = assign ? k_prolong_tiled<TB, KM, true> : k_prolong_tiled<TB, KM, false>;
+                const int64_t need = (n + row_tile<KM>() - 1) / row_tile<KM>();
+                int64_t gx = std::min<int64_t>(need, resident_ctas(h, (const void*)fn, false));
+                dim3 g((unsigned)std::max<int64_t>(gx, 1), (unsigned)(h->Bp / TB));
+                fn<<<g, kBlock, 0, h->stream>>>(n, h->Bp, s, h->d_phi, k, h->d_e, h->d_active);
+            });
+            count_launch(h, KC_PROLONG);
+            CU(cudaGetLastError());
+            return P2G_OK;
+        }
         KSWITCH(k, {
             using LSh = typename LocalShape<Sh, KM>::type;
             auto fn = assign ? k_prolong<LSh, KM, true> : k_prolong<LSh, KM, false>;
@@ -683,6 +713,12 @@ int choose_shape(p2g_handle* h, int B) {
     } else {
         h->shape = SH_B64;
         h->Bp = (B + 63) / 64 * 64;
+    }
+    // tuning knob: P2G_WIDE=0 runs large batches with one instance per lane
+    // (32-wide tiles) instead of double2 lanes (64-wide tiles)
+    if (h->shape == SH_B64) {
+        const char* w = std::getenv("P2G_WIDE");
+        if (w && w[0] == '0') h->shape = SH_B32;
     }
     return P2G_OK;
 }
