@@ -149,16 +149,21 @@ __device__ __forceinline__ double inst_sum(double x) {
 }
 
 // acc[v] += sum_{k in [k0,k1), k = k0+s (mod S)} vals[k][b] * X[ci[k]][b]
-// (separately rounded multiply and add: the reference's `s += v * x`)
+// (separately rounded multiply and add: the reference's `s += v * x`).
+// 32-bit element offsets (nnz * Bp and n * Bp < 2^32, checked at upload)
+// keep the address arithmetic out of 64-bit registers.
 template <class Sh>
 __device__ __forceinline__ void row_dot(const Mat& A, const double* X, int b0, int k0, int k1,
                                         int s, double (&acc)[Sh::V]) {
+    const unsigned Bp = (unsigned)A.Bp;
+    const double* Xb = X + b0;
+    const double* vb = A.vals + b0;
 #pragma unroll 4
     for (int k = k0 + s; k < k1; k += Sh::S) {
-        const int c = __ldg(A.ci + k);
+        const unsigned c = (unsigned)__ldg(A.ci + k);
         double a[Sh::V], x[Sh::V];
-        ldv_stream<Sh::V>(a, A.vals + (size_t)k * A.Bp + b0);
-        ldv<Sh::V>(x, X + (size_t)c * A.Bp + b0);
+        ldv_stream<Sh::V>(a, vb + (unsigned)k * Bp);
+        ldv<Sh::V>(x, Xb + c * Bp);
 #pragma unroll
         for (int v = 0; v < Sh::V; ++v) acc[v] = __dadd_rn(acc[v], __dmul_rn(a[v], x[v]));
     }
@@ -168,12 +173,15 @@ __device__ __forceinline__ void row_dot(const Mat& A, const double* X, int b0, i
 template <class Sh>
 __device__ __forceinline__ void row_sub(const Mat& A, const double* X, int b0, int k0, int k1,
                                         double (&acc)[Sh::V]) {
+    const unsigned Bp = (unsigned)A.Bp;
+    const double* Xb = X + b0;
+    const double* vb = A.vals + b0;
 #pragma unroll 4
     for (int k = k0; k < k1; ++k) {
-        const int c = __ldg(A.ci + k);
+        const unsigned c = (unsigned)__ldg(A.ci + k);
         double a[Sh::V], x[Sh::V];
-        ldv_stream<Sh::V>(a, A.vals + (size_t)k * A.Bp + b0);
-        ldv<Sh::V>(x, X + (size_t)c * A.Bp + b0);
+        ldv_stream<Sh::V>(a, vb + (unsigned)k * Bp);
+        ldv<Sh::V>(x, Xb + c * Bp);
 #pragma unroll
         for (int v = 0; v < Sh::V; ++v) acc[v] = __dsub_rn(acc[v], __dmul_rn(a[v], x[v]));
     }
