@@ -83,17 +83,30 @@ typedef enum {
     P2G_RESIDUAL_UPPER = 1
 } p2g_residual_form;
 
+typedef enum {
+    /* Kp = spmv(K, p) every iteration (krylov.hpp:272), the reference form. */
+    P2G_KP_SPMV = 0,
+    /* With the GS smoother the backward sweep leaves (D+U) s = r - L s' row by
+     * row (s' = the prolongated vector), so K s = r + L (s - s') and
+     *   Kp_new = r + L (s - s') + beta Kp:
+     * the SpMV and the p update become one half-matrix pass.  Same values up
+     * to rounding.  Ignored (SPMV) for the Jacobi smoother. */
+    P2G_KP_RECURRENCE = 1
+} p2g_kp_update;
+
 typedef struct {
     int32_t smoother;       /* p2g_smoother; reference default GS (smoothers.hpp:10-14)  */
     int32_t pre_sweeps;     /* r1 >= 1 (pod.hpp:186, bench.hpp:122)                      */
     int32_t post_sweeps;    /* r2 >= 1                                                   */
     int32_t residual_form;  /* p2g_residual_form                                         */
     double omega;           /* damped Jacobi weight in (0,1] (smoothers.hpp:79)           */
+    int32_t kp_update;      /* p2g_kp_update                                             */
+    int32_t reserved;
 } p2g_config;
 
 /* Initialise cfg with the defaults: GS_MULTICOLOR, r1 = r2 = 1, RESIDUAL_UPPER,
- * omega = 0.5 (2/3, the reference default, is unsafe for these operators:
- * see DESIGN.md). */
+ * KP_RECURRENCE, omega = 0.5 (2/3, the reference default, is unsafe for these
+ * operators: see DESIGN.md). */
 void p2g_config_default(p2g_config* cfg);
 
 /* ---- lifetime ---------------------------------------------------------- */

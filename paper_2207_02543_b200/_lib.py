@@ -92,12 +92,14 @@ def lib():
 class Config(C.Structure):
     """p2g_config (include/pod2g_b200.h)."""
     _fields_ = [("smoother", C.c_int32), ("pre_sweeps", C.c_int32), ("post_sweeps", C.c_int32),
-                ("residual_form", C.c_int32), ("omega", C.c_double)]
+                ("residual_form", C.c_int32), ("omega", C.c_double), ("kp_update", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 # status codes
 OK, EINVAL, EBREAKDOWN, ENONFINITE, ESINGULAR, EZERODIAG, ECUDA, ENCCL, ESTATE = range(9)
 SMOOTHER_GS_MULTICOLOR, SMOOTHER_JACOBI = 0, 1
 RESIDUAL_FULL, RESIDUAL_UPPER = 0, 1
+KP_SPMV, KP_RECURRENCE = 0, 1
 X0_ZERO, X0_GIVEN, X0_REDUCED = 0, 1, 2
 NUM_KCLASS = 9

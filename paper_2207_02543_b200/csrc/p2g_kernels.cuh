@@ -44,7 +44,10 @@ constexpr int kCluster = 8;
 // Streaming row kernels are latency bound unless the SM is full: cap them at
 // 32 registers so 8 CTAs x 8 warps (100% occupancy) stay resident (the
 // difference between 4.4 and 6.3 TB/s for the batched SpMV, tools/spmv_lab.cu).
-#define P2G_ROWK __launch_bounds__(kBlock, 8)
+#define P2G_ROWK __launch_bounds__(kBlock, P2G_MINB)
+#ifndef P2G_MINB
+#define P2G_MINB 4
+#endif
 
 template <int R_, int S_, int W_, int V_>
 struct Shape {
@@ -191,17 +194,22 @@ __device__ __forceinline__ void row_sub(const Mat& A, const double* X, int b0, i
 //   s_i = (f_i - sum_{j != i} K_ij s_j) / K_ii
 // upper == false: only the L part is read (first forward sweep from s = 0:
 // the U-part entries of s are still zero, and subtracting zeros is exact).
+// The L-part values come from xlo, the U-part values from xhi, the result
+// goes to s: in place (xlo == xhi == s) for the reference sweeps, or out of
+// place for the backward sweep of the Kp recurrence (xlo = s' the
+// prolongated vector, xhi = s = the new sweep, D9).
 template <class Sh>
-__device__ __forceinline__ void gs_row(const Mat& A, const double* f, double* s, int i, int b0,
-                                       int lane_s, bool upper, const bool (&m)[Sh::V], bool any) {
+__device__ __forceinline__ void gs_row(const Mat& A, const double* f, const double* xlo,
+                                       const double* xhi, double* s, int i, int b0, int lane_s,
+                                       bool upper, const bool (&m)[Sh::V], bool any) {
     double out[Sh::V];
     if constexpr (Sh::S == 1) {
         if (any) {
             const int kb = __ldg(A.rp + i), kd = __ldg(A.dpos + i), ke = __ldg(A.rp + i + 1);
             double acc[Sh::V], d[Sh::V];
             ldv<Sh::V>(acc, f + (size_t)i * A.Bp + b0);
-            row_sub<Sh>(A, s, b0, kb, kd, acc);
-            if (upper) row_sub<Sh>(A, s, b0, kd + 1, ke, acc);
+            row_sub<Sh>(A, xlo, b0, kb, kd, acc);
+            if (upper) row_sub<Sh>(A, xhi, b0, kd + 1, ke, acc);
             ldv<Sh::V>(d, A.vals + (size_t)kd * A.Bp + b0);
 #pragma unroll
             for (int v = 0; v < Sh::V; ++v) out[v] = __ddiv_rn(acc[v], d[v]);
@@ -215,8 +223,8 @@ __device__ __forceinline__ void gs_row(const Mat& A, const double* f, double* s,
         if (any) {
             const int kb = __ldg(A.rp + i), ke = __ldg(A.rp + i + 1);
             kd = __ldg(A.dpos + i);
-            row_dot<Sh>(A, s, b0, kb, kd, lane_s, acc);
-            if (upper) row_dot<Sh>(A, s, b0, kd + 1, ke, lane_s, acc);
+            row_dot<Sh>(A, xlo, b0, kb, kd, lane_s, acc);
+            if (upper) row_dot<Sh>(A, xhi, b0, kd + 1, ke, lane_s, acc);
         }
 #pragma unroll
         for (int v = 0; v < Sh::V; ++v) acc[v] = slot_sum<Sh>(acc[v]);
@@ -436,7 +444,7 @@ __global__ void P2G_CLUSTER P2G_ROWK
             if constexpr (PRE == PRE_GS) {
                 // every lane participates (S > 1 shuffles); only colour-0 rows work
                 const bool work = any && valid && node < color0_nodes;
-                gs_row<Sh>(A, r, s, work ? i : 0, b0, G.s, false, m, work);
+                gs_row<Sh>(A, r, s, s, s, work ? i : 0, b0, G.s, false, m, work);
             } else if constexpr (PRE == PRE_JACOBI) {
                 if (valid && any && G.s == 0) {
                     double ri[Sh::V], d[Sh::V], si[Sh::V];
@@ -467,7 +475,7 @@ __global__ void P2G_ROWK k_gs_forward(Mat A, const double* __restrict__ f,
         const int node = base_ + G.r;
         const bool valid = node < ne;
         for (int c = 0; c < A.bs; ++c)
-            gs_row<Sh>(A, f, s, valid ? node * A.bs + c : 0, b0, G.s, !FIRST, m, any && valid);
+            gs_row<Sh>(A, f, s, s, s, valid ? node * A.bs + c : 0, b0, G.s, !FIRST, m, any && valid);
     }
 }
 
@@ -476,7 +484,8 @@ __global__ void P2G_ROWK k_gs_forward(Mat A, const double* __restrict__ f,
 // over this colour's rows (krylov.hpp:280 rs_new = dot(r, s)).
 template <class Sh, bool LAST>
 __global__ void P2G_CLUSTER P2G_ROWK k_gs_backward(Mat A, const double* __restrict__ f,
-                                                        double* s, const int* active, int nb,
+                                                        const double* xlo, double* s,
+                                                        const int* active, int nb,
                                                         int ne, double* part_rs, int accumulate) {
     LaneGeo<Sh> G;
     const int b0 = blockIdx.y * Sh::T + G.w * Sh::V;
@@ -490,7 +499,7 @@ __global__ void P2G_CLUSTER P2G_ROWK k_gs_backward(Mat A, const double* __restri
         const bool valid = node < ne;
         for (int c = A.bs - 1; c >= 0; --c) {
             const int i = valid ? node * A.bs + c : 0;
-            gs_row<Sh>(A, f, s, i, b0, G.s, true, m, any && valid);
+            gs_row<Sh>(A, f, xlo, s, s, i, b0, G.s, true, m, any && valid);
             if constexpr (LAST) {
                 if (valid && any && G.s == 0) {
                     double fi[Sh::V], si[Sh::V];
@@ -503,6 +512,77 @@ __global__ void P2G_CLUSTER P2G_ROWK k_gs_backward(Mat A, const double* __restri
         }
     }
     if constexpr (LAST) cluster_partial<Sh>(rs, part_rs, A.Bp, accumulate != 0);
+}
+
+// Kp recurrence (D9), replacing the SpMV and the p update of the next
+// iteration.  After the out-of-place backward sweep, (D + U) s = r - L s'
+// row by row (s' = prolongated vector, s = the new sweep), hence
+//   K s = r + L (s - s'),   Kp_new = K s + beta Kp = r + L (s - s') + beta Kp,
+//   p_new = s + beta p      (krylov.hpp:282),      partial of p_new . Kp_new.
+// Only the strictly lower part of each row is read: half a matrix pass.
+template <class Sh>
+__global__ void P2G_CLUSTER P2G_ROWK k_kp_update(Mat A, const double* __restrict__ r,
+                                                 const double* __restrict__ s,
+                                                 const double* __restrict__ sp,
+                                                 double* __restrict__ Kp, double* __restrict__ p,
+                                                 const double* beta, const int* active,
+                                                 double* part) {
+    LaneGeo<Sh> G;
+    const int b0 = blockIdx.y * Sh::T + G.w * Sh::V;
+    bool m[Sh::V], any;
+    lane_mask<Sh>(active, b0, m, any);
+    double bt[Sh::V], dacc[Sh::V];
+#pragma unroll
+    for (int v = 0; v < Sh::V; ++v) {
+        bt[v] = beta[b0 + v];
+        dacc[v] = 0.0;
+    }
+    const int nn = A.n / A.bs;
+    const unsigned Bp = (unsigned)A.Bp;
+    P2G_NODE_LOOP(Sh, 0, nn, G) {
+        const int node = base_ + G.r;
+        const bool valid = node < nn;
+        for (int c = 0; c < A.bs; ++c) {
+            const int i = node * A.bs + c;
+            double acc[Sh::V];
+#pragma unroll
+            for (int v = 0; v < Sh::V; ++v) acc[v] = 0.0;
+            if (valid && any) {
+                const int kb = __ldg(A.rp + i), kd = __ldg(A.dpos + i);
+                const double* vb = A.vals + b0;
+#pragma unroll 4
+                for (int k = kb + G.s; k < kd; k += Sh::S) {
+                    const unsigned col = (unsigned)__ldg(A.ci + k);
+                    double a[Sh::V], x1[Sh::V], x0[Sh::V];
+                    ldv_stream<Sh::V>(a, vb + (unsigned)k * Bp);
+                    ldv<Sh::V>(x1, s + b0 + col * Bp);
+                    ldv<Sh::V>(x0, sp + b0 + col * Bp);
+#pragma unroll
+                    for (int v = 0; v < Sh::V; ++v)
+                        acc[v] = __dadd_rn(acc[v], __dmul_rn(a[v], __dsub_rn(x1[v], x0[v])));
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < Sh::V; ++v) acc[v] = slot_sum<Sh>(acc[v]);
+            if (valid && any && G.s == 0) {
+                const size_t o = (size_t)i * A.Bp + b0;
+                double ri[Sh::V], si[Sh::V], kpi[Sh::V], pi[Sh::V];
+                ldv<Sh::V>(ri, r + o);
+                ldv<Sh::V>(si, s + o);
+                ldv<Sh::V>(kpi, Kp + o);
+                ldv<Sh::V>(pi, p + o);
+#pragma unroll
+                for (int v = 0; v < Sh::V; ++v) {
+                    kpi[v] = __dadd_rn(__dadd_rn(ri[v], acc[v]), __dmul_rn(bt[v], kpi[v]));
+                    pi[v] = __dadd_rn(si[v], __dmul_rn(bt[v], pi[v]));
+                    dacc[v] = __dadd_rn(dacc[v], __dmul_rn(pi[v], kpi[v]));
+                }
+                stv<Sh::V>(Kp + o, kpi, m);
+                stv<Sh::V>(p + o, pi, m);
+            }
+        }
+    }
+    cluster_partial<Sh>(dacc, part, A.Bp, false);
 }
 
 // Damped Jacobi sweep, out of place (smoothers.hpp:83-86):

@@ -70,7 +70,7 @@ struct p2g_handle {
 
     // vectors [n][Bp]
     double *d_u = nullptr, *d_r = nullptr, *d_s = nullptr, *d_s2 = nullptr, *d_p = nullptr,
-           *d_Kp = nullptr, *d_b = nullptr;
+           *d_Kp = nullptr, *d_b = nullptr, *d_t = nullptr;
     // per-instance
     double *d_alpha = nullptr, *d_beta = nullptr, *d_rsold = nullptr, *d_fnorm = nullptr,
            *d_rel = nullptr, *d_e = nullptr, *d_L = nullptr, *d_Ac = nullptr;
@@ -93,6 +93,7 @@ struct p2g_handle {
     p2g_config cfg{};
     bool setup_done = false;
     double* s_final = nullptr;  // buffer holding B r after the post-smoother
+    double* s_prol = nullptr;   // prolongated s' (Kp recurrence)
 
     // graph
     cudaGraphExec_t loop_exec = nullptr;
@@ -189,6 +190,10 @@ int kbucket(int k) {
         default: { constexpr int KM = 64; __VA_ARGS__; } break;    \
     }
 
+bool kp_recurrence(const p2g_handle* h) {
+    return h->cfg.smoother == P2G_SMOOTHER_GS_MULTICOLOR && h->cfg.kp_update == P2G_KP_RECURRENCE;
+}
+
 Mat mat_of(p2g_handle* h) {
     Mat A;
     A.n = static_cast<int>(h->pat.n);
@@ -258,11 +263,19 @@ struct Run {
 
     static int nnodes(p2g_handle* h) { return static_cast<int>(h->pat.n / h->pat.bs); }
 
+    // the two producers of pKp partials (k_spmv<DOT>, k_kp_update) share one
+    // grid so k_alpha always reduces the same number of partial rows
+    static dim3 dot_grid(p2g_handle* h) {
+        const dim3 a = node_grid<Sh>(h, nnodes(h), (const void*)k_spmv<Sh, true>, true);
+        const dim3 b = node_grid<Sh>(h, nnodes(h), (const void*)k_kp_update<Sh>, true);
+        return a.x <= b.x ? a : b;
+    }
+
     static int spmv(p2g_handle* h, const double* x, double* y, bool dot, int* nb_out) {
         Mat A = mat_of(h);
         if (dot) {
             auto fn = k_spmv<Sh, true>;
-            dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn, true);
+            dim3 g = dot_grid(h);
             fn<<<g, kBlock, 0, h->stream>>>(A, x, y, h->d_active, h->d_part_dot);
             if (nb_out) *nb_out = g.x / kCluster;
         } else {
@@ -333,8 +346,8 @@ struct Run {
     // one backward colour phase; every phase of a sweep uses the same grid
     // (the largest colour's) so the LAST sweep's r.s partials accumulate into
     // the same rows phase after phase (first phase writes, later ones add)
-    static int gs_backward(p2g_handle* h, const double* f, double* s, int c, bool last,
-                           int* rs_rows, bool first_phase) {
+    static int gs_backward(p2g_handle* h, const double* f, const double* xlo, double* s, int c,
+                           bool last, int* rs_rows, bool first_phase) {
         Mat A = mat_of(h);
         const int nb = static_cast<int>(h->pat.color_rows[c] / h->pat.bs);
         const int ne = static_cast<int>(h->pat.color_rows[c + 1] / h->pat.bs);
@@ -344,18 +357,33 @@ struct Run {
         if (last) {
             auto fn = k_gs_backward<Sh, true>;
             dim3 g = node_grid<Sh>(h, maxc, (const void*)fn, true);
-            fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_active, nb, ne, h->d_part_rs,
+            fn<<<g, kBlock, 0, h->stream>>>(A, f, xlo, s, h->d_active, nb, ne, h->d_part_rs,
                                             first_phase ? 0 : 1);
             *rs_rows = g.x / kCluster;
         } else {
             auto fn = k_gs_backward<Sh, false>;
             dim3 g = node_grid<Sh>(h, maxc, (const void*)fn, true);
-            fn<<<g, kBlock, 0, h->stream>>>(A, f, s, h->d_active, nb, ne, nullptr, 0);
+            fn<<<g, kBlock, 0, h->stream>>>(A, f, xlo, s, h->d_active, nb, ne, nullptr, 0);
         }
         count_launch(h, KC_BWD);
         CU(cudaGetLastError());
         return P2G_OK;
     }
+
+    // Kp / p / pKp by the recurrence (D9); returns the partial row count
+    static int kp_update(p2g_handle* h, const double* s_new, const double* s_prol, int* nb_out) {
+        Mat A = mat_of(h);
+        auto fn = k_kp_update<Sh>;
+        dim3 g = dot_grid(h);
+        fn<<<g, kBlock, 0, h->stream>>>(A, h->d_r, s_new, s_prol, h->d_Kp, h->d_p, h->d_beta,
+                                        h->d_active, h->d_part_dot);
+        if (nb_out) *nb_out = g.x / kCluster;
+        count_launch(h, KC_SPMV);
+        CU(cudaGetLastError());
+        return P2G_OK;
+    }
+
+    static int kp_rows(p2g_handle* h) { return dot_grid(h).x / kCluster; }
 
     static int jacobi(p2g_handle* h, const double* f, const double* s, double* s_out, bool last,
                       int* rs_rows, int kclass) {
@@ -376,13 +404,13 @@ struct Run {
         return P2G_OK;
     }
 
-    // c = Phi^T t with t = FORM(f, s) (RES_VECTOR: t = f).  The residual is
-    // written to the Kp buffer (free between the update and the next SpMV).
+    // c = Phi^T t with t = FORM(f, s) (RES_VECTOR: t = f).  The residual goes
+    // to its own buffer d_t (Kp must survive the iteration for the recurrence).
     static int restrict_(p2g_handle* h, int form, const double* f, const double* s, int* nb_out) {
         Mat A = mat_of(h);
         const double* t = f;
         if (form != RES_VECTOR) {
-            double* tb = h->d_Kp;
+            double* tb = h->d_t;
             if (form == RES_UPPER) {
                 auto fn = k_residual<Sh, RES_UPPER>;
                 dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn, true);
@@ -516,8 +544,16 @@ struct Run {
         if (cfg.smoother == P2G_SMOOTHER_GS_MULTICOLOR) {
             for (int sw = 0; sw < cfg.post_sweeps; ++sw) {
                 const bool last = sw + 1 == cfg.post_sweeps;
+                // the recurrence needs s' (the prolongated vector) intact: the
+                // LAST backward sweep reads its L part from s' and writes d_s2
+                const bool oop = last && kp_recurrence(h);
+                double* out = oop ? h->d_s2 : cur;
                 for (int c = C - 1; c >= 0; --c)
-                    TRY(gs_backward(h, rr, cur, c, last, &rs_row, c == C - 1));
+                    TRY(gs_backward(h, rr, cur, out, c, last, &rs_row, c == C - 1));
+                if (oop) {
+                    h->s_prol = cur;
+                    cur = out;
+                }
             }
         } else {
             for (int sw = 0; sw < cfg.post_sweeps; ++sw) {
@@ -532,10 +568,17 @@ struct Run {
         return P2G_OK;
     }
 
-    // one PCG iteration (krylov.hpp:272-288)
+    // one PCG iteration (krylov.hpp:272-288).  Reference form: SpMV first,
+    // p update last.  Recurrence form (D9): the body starts at alpha (pKp
+    // partials of the previous kp_update / prologue SpMV) and ends with the
+    // half-pass kp_update that produces Kp, p and pKp for the next iteration.
     static int iteration(p2g_handle* h, bool in_graph) {
         int nb_dot = 0, nb_rr = 0, rs_rows = 0;
-        TRY(spmv(h, h->d_p, h->d_Kp, true, &nb_dot));
+        const bool rec = kp_recurrence(h);
+        if (rec)
+            nb_dot = kp_rows(h);
+        else
+            TRY(spmv(h, h->d_p, h->d_Kp, true, &nb_dot));
         const int wb = 8;  // warps per block for the per-instance reducers
         k_alpha<<<(h->Bp + wb - 1) / wb, wb * 32, 0, h->stream>>>(h->Bp, nb_dot, h->d_part_dot,
                                                                   h->d_rsold, h->d_alpha,
@@ -547,7 +590,10 @@ struct Run {
             h->d_rel, h->d_iters, h->d_active, h->d_status, h->d_hist, h->d_prm, h->d_flag_ticket,
             h->cond, in_graph ? 1 : 0);
         count_launch(h, KC_REDUCE);
-        TRY(pupdate(h, h->s_final, false));
+        if (rec)
+            TRY(kp_update(h, h->s_final, h->s_prol, nullptr));
+        else
+            TRY(pupdate(h, h->s_final, false));
         CU(cudaGetLastError());
         return P2G_OK;
     }
@@ -678,7 +724,7 @@ int alloc_batch(p2g_handle* h) {
     const size_t nv = (size_t)h->pat.n * h->Bp;
     TRY(dalloc(h, h->d_vals, (size_t)h->pat.nnz * h->Bp));
     CU(cudaMemsetAsync(h->d_vals, 0, (size_t)h->pat.nnz * h->Bp * sizeof(double), h->stream));
-    for (double** p : {&h->d_u, &h->d_r, &h->d_s, &h->d_s2, &h->d_p, &h->d_Kp, &h->d_b}) {
+    for (double** p : {&h->d_u, &h->d_r, &h->d_s, &h->d_s2, &h->d_p, &h->d_Kp, &h->d_b, &h->d_t}) {
         TRY(dalloc(h, *p, nv));
         CU(cudaMemsetAsync(*p, 0, nv * sizeof(double), h->stream));
     }
@@ -749,10 +795,11 @@ int set_values_impl(p2g_handle* h, int32_t batch, const double* host, const doub
 std::vector<uint64_t> graph_key_of(p2g_handle* h) {
     auto u = [](const void* p) { return (uint64_t)(uintptr_t)p; };
     return {u(h->d_vals), u(h->d_phi), u(h->d_e), u(h->d_L), u(h->d_part_c), u(h->d_u), u(h->d_r),
-            u(h->d_s), u(h->d_s2), u(h->d_p), u(h->d_Kp), u(h->d_hist), (uint64_t)h->Bp,
+            u(h->d_s), u(h->d_s2), u(h->d_p), u(h->d_Kp), u(h->d_t), u(h->d_hist), (uint64_t)h->Bp,
             (uint64_t)h->B, (uint64_t)h->k, (uint64_t)h->shape, (uint64_t)h->cfg.smoother,
             (uint64_t)h->cfg.pre_sweeps, (uint64_t)h->cfg.post_sweeps,
-            (uint64_t)h->cfg.residual_form, (uint64_t)std::llround(h->cfg.omega * 1e15)};
+            (uint64_t)h->cfg.residual_form, (uint64_t)std::llround(h->cfg.omega * 1e15),
+            (uint64_t)h->cfg.kp_update};
 }
 
 int build_loop_graph(p2g_handle* h) {
@@ -861,6 +908,7 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
                                                            h->d_rsold, h->d_active, h->d_status);
         count_launch(h, KC_REDUCE);
         TRY(Rn::pupdate(h, h->s_final, true));
+        if (kp_recurrence(h)) TRY(Rn::spmv(h, h->d_p, h->d_Kp, true, nullptr));  // Kp_0, pKp_0
         return P2G_OK;
     });
     if (st != P2G_OK) return st;
@@ -921,6 +969,8 @@ void p2g_config_default(p2g_config* cfg) {
     cfg->post_sweeps = 1;
     cfg->residual_form = P2G_RESIDUAL_UPPER;
     cfg->omega = 0.5;
+    cfg->kp_update = P2G_KP_RECURRENCE;
+    cfg->reserved = 0;
 }
 
 int p2g_abi_version(void) { return P2G_ABI_VERSION; }
@@ -979,7 +1029,7 @@ int p2g_destroy(p2g_handle* h) {
     dfree(h->d_perm);
     dfree(h->d_vals);
     dfree(h->d_phi);
-    for (double** p : {&h->d_u, &h->d_r, &h->d_s, &h->d_s2, &h->d_p, &h->d_Kp, &h->d_b, &h->d_alpha,
+    for (double** p : {&h->d_u, &h->d_r, &h->d_s, &h->d_s2, &h->d_p, &h->d_Kp, &h->d_b, &h->d_t, &h->d_alpha,
                        &h->d_beta, &h->d_rsold, &h->d_fnorm, &h->d_rel, &h->d_e, &h->d_L, &h->d_Ac,
                        &h->d_hist, &h->d_part_dot, &h->d_part_rr, &h->d_part_ff, &h->d_part_rs,
                        &h->d_part_c, &h->d_stage})
@@ -1083,6 +1133,8 @@ int p2g_setup(p2g_handle* h, const p2g_config* cfg, int32_t* status) {
         "jacobi_sweep: omega outside (0,1]");
     REQ(c.residual_form == P2G_RESIDUAL_FULL || c.residual_form == P2G_RESIDUAL_UPPER, P2G_EINVAL,
         "p2g_setup: unknown residual form");
+    REQ(c.kp_update == P2G_KP_SPMV || c.kp_update == P2G_KP_RECURRENCE, P2G_EINVAL,
+        "p2g_setup: unknown kp_update");
     
     h->cfg = c;
     CU(cudaMemsetAsync(h->d_setup_status, 0, sizeof(int) * h->Bp, h->stream));
@@ -1201,7 +1253,7 @@ int p2g_smooth(p2g_handle* h, int32_t direction, const double* f, double* u) {
         } else {
             int row = 0;
             for (int c = C - 1; c >= 0; --c)
-                TRY(Rn::gs_backward(h, h->d_r, h->d_s, c, false, &row, c == C - 1));
+                TRY(Rn::gs_backward(h, h->d_r, h->d_s, h->d_s, c, false, &row, c == C - 1));
         }
         return P2G_OK;
     }));
@@ -1255,10 +1307,19 @@ int p2g_profile_iteration(p2g_handle* h, int32_t reps, double* ms, double* bytes
     REQ(h->setup_done, P2G_ESTATE, "p2g_profile_iteration: p2g_setup not called");
     REQ(reps >= 1, P2G_EINVAL, "p2g_profile_iteration: reps >= 1");
     std::vector<double> acc(P2G_NUM_KCLASS, 0.0);
-    // every instance active: time the full batch (state is scratch)
+    // every instance active for the whole replay: no convergence or max_iter
+    // exit inside the profiled iterations (state is scratch)
+    {
+        SolveParams prm{0.0, (long long)1 << 62, 0};
+        CU(cudaMemcpyAsync(h->d_prm, &prm, sizeof(prm), cudaMemcpyHostToDevice, h->stream));
+    }
     for (int rep = 0; rep < reps; ++rep) {
         CU(cudaMemcpyAsync(h->d_active, h->d_all, sizeof(int) * h->Bp, cudaMemcpyDeviceToDevice,
                            h->stream));
+        if (kp_recurrence(h)) {
+            // the body starts at alpha: refresh Kp and the pKp partials first
+            TRY(dispatch(h, [&](auto R) -> int { return decltype(R)::spmv(h, h->d_p, h->d_Kp, true, nullptr); }));
+        }
         h->profiling = true;
         h->kev_n = 0;
         CU(cudaEventRecord(h->kev[0], h->stream));
@@ -1282,7 +1343,8 @@ int p2g_profile_iteration(p2g_handle* h, int32_t reps, double* ms, double* bytes
     // lower/upper halves of the values (strict), diagonal
     const double zl = 0.5 * (z - n);
     const bool gs = h->cfg.smoother == P2G_SMOOTHER_GS_MULTICOLOR;
-    by[KC_SPMV] = Mv + idx + 16.0 * n * Bp;                    // vals, x once, y
+    by[KC_SPMV] = kp_recurrence(h) ? 8.0 * zl * Bp + 4.0 * zl + 4.0 * n + 64.0 * n * Bp
+                                   : Mv + idx + 16.0 * n * Bp;  // L vals | vals, x once, y
     by[KC_UPDATE] = 48.0 * n * Bp + (gs ? 0.0 : 24.0 * n * Bp);  // u,p,r,Kp r/w (+ s,d for Jacobi)
     by[KC_FWD] = gs ? (8.0 * (zl + n) * Bp + 4.0 * (zl + n) + 4.0 * n + 24.0 * n * Bp * (C - 1) / C)
                     : 0.0;
@@ -1294,7 +1356,7 @@ int p2g_profile_iteration(p2g_handle* h, int32_t reps, double* ms, double* bytes
     by[KC_PROLONG] = 16.0 * n * Bp + 8.0 * n * k;
     by[KC_BWD] = Mv + idx + 24.0 * n * Bp;
     by[KC_REDUCE] = 0.0;
-    by[KC_PUPDATE] = 24.0 * n * Bp;
+    by[KC_PUPDATE] = kp_recurrence(h) ? 0.0 : 24.0 * n * Bp;
     if (h->k == 0) by[KC_RESTRICT] = by[KC_PROLONG] = 0.0;
     for (int q = 0; q < P2G_NUM_KCLASS; ++q) {
         if (ms) ms[q] = acc[q] / reps;

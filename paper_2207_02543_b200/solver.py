@@ -156,8 +156,9 @@ class BatchSolver:
         self.k = p.shape[1]
 
     def setup(self, smoother=L.SMOOTHER_GS_MULTICOLOR, pre_sweeps=1, post_sweeps=1,
-              residual_form=L.RESIDUAL_UPPER, omega=0.5, raise_on_error=False):
-        cfg = L.Config(smoother, pre_sweeps, post_sweeps, residual_form, omega)
+              residual_form=L.RESIDUAL_UPPER, omega=0.5, kp_update=L.KP_RECURRENCE,
+              raise_on_error=False):
+        cfg = L.Config(smoother, pre_sweeps, post_sweeps, residual_form, omega, kp_update, 0)
         st_arr = np.zeros(max(self.B, 1), dtype=np.int32)
         st = self._L.p2g_setup(self._h, C.byref(cfg), st_arr.ctypes.data_as(L.I32))
         if st in (L.EINVAL, L.ECUDA, L.ESTATE) or (raise_on_error and st != L.OK):

@@ -153,10 +153,13 @@ def _check_solve(x, it, conv, status, hist, x_ref_fn, res_ref, tol):
 
 
 @pytest.mark.parametrize("B", [1, 8, 40])
-@pytest.mark.parametrize("form", [L.RESIDUAL_UPPER, L.RESIDUAL_FULL])
-def test_pcg_pod2g_parity(gpu, B, form):
+@pytest.mark.parametrize("form,kp", [(L.RESIDUAL_UPPER, L.KP_RECURRENCE),
+                                     (L.RESIDUAL_FULL, L.KP_RECURRENCE),
+                                     (L.RESIDUAL_FULL, L.KP_SPMV),
+                                     (L.RESIDUAL_UPPER, L.KP_SPMV)])
+def test_pcg_pod2g_parity(gpu, B, form, kp):
     m, rp, ci, f, V, phi = small_problem(B=B, k=10)
-    s = make_solver(m, rp, ci, V, phi, residual_form=form)
+    s = make_solver(m, rp, ci, V, phi, residual_form=form, kp_update=kp)
     perm, prp, pci, pV, pf, pphi = perm_system(s, rp, ci, V, f, phi)
     F = np.broadcast_to(f, (B, m.n)).copy()
     tol = 1e-8
