@@ -153,19 +153,20 @@ __device__ __forceinline__ double inst_sum(double x) {
 
 // acc[v] += sum_{k in [k0,k1), k = k0+s (mod S)} vals[k][b] * X[ci[k]][b]
 // (separately rounded multiply and add: the reference's `s += v * x`).
-// 32-bit element offsets (nnz * Bp and n * Bp < 2^32, checked at upload)
+// 64-bit row base, 32-bit offsets inside the row and for the x gathers
+// (n * Bp < 2^32 is checked at upload)
 // keep the address arithmetic out of 64-bit registers.
 template <class Sh>
 __device__ __forceinline__ void row_dot(const Mat& A, const double* X, int b0, int k0, int k1,
                                         int s, double (&acc)[Sh::V]) {
     const unsigned Bp = (unsigned)A.Bp;
     const double* Xb = X + b0;
-    const double* vb = A.vals + b0;
+    const double* vb = A.vals + (size_t)k0 * Bp + b0;  // 64-bit row base, 32-bit in-row offsets
 #pragma unroll 4
     for (int k = k0 + s; k < k1; k += Sh::S) {
         const unsigned c = (unsigned)__ldg(A.ci + k);
         double a[Sh::V], x[Sh::V];
-        ldv_stream<Sh::V>(a, vb + (unsigned)k * Bp);
+        ldv_stream<Sh::V>(a, vb + (unsigned)(k - k0) * Bp);
         ldv<Sh::V>(x, Xb + c * Bp);
 #pragma unroll
         for (int v = 0; v < Sh::V; ++v) acc[v] = __dadd_rn(acc[v], __dmul_rn(a[v], x[v]));
@@ -178,12 +179,12 @@ __device__ __forceinline__ void row_sub(const Mat& A, const double* X, int b0, i
                                         double (&acc)[Sh::V]) {
     const unsigned Bp = (unsigned)A.Bp;
     const double* Xb = X + b0;
-    const double* vb = A.vals + b0;
+    const double* vb = A.vals + (size_t)k0 * Bp + b0;
 #pragma unroll 4
     for (int k = k0; k < k1; ++k) {
         const unsigned c = (unsigned)__ldg(A.ci + k);
         double a[Sh::V], x[Sh::V];
-        ldv_stream<Sh::V>(a, vb + (unsigned)k * Bp);
+        ldv_stream<Sh::V>(a, vb + (unsigned)(k - k0) * Bp);
         ldv<Sh::V>(x, Xb + c * Bp);
 #pragma unroll
         for (int v = 0; v < Sh::V; ++v) acc[v] = __dsub_rn(acc[v], __dmul_rn(a[v], x[v]));
@@ -549,12 +550,12 @@ __global__ void P2G_CLUSTER P2G_ROWK k_kp_update(Mat A, const double* __restrict
             for (int v = 0; v < Sh::V; ++v) acc[v] = 0.0;
             if (valid && any) {
                 const int kb = __ldg(A.rp + i), kd = __ldg(A.dpos + i);
-                const double* vb = A.vals + b0;
+                const double* vb = A.vals + (size_t)kb * Bp + b0;
 #pragma unroll 4
                 for (int k = kb + G.s; k < kd; k += Sh::S) {
                     const unsigned col = (unsigned)__ldg(A.ci + k);
                     double a[Sh::V], x1[Sh::V], x0[Sh::V];
-                    ldv_stream<Sh::V>(a, vb + (unsigned)k * Bp);
+                    ldv_stream<Sh::V>(a, vb + (unsigned)(k - kb) * Bp);
                     ldv<Sh::V>(x1, s + b0 + col * Bp);
                     ldv<Sh::V>(x0, sp + b0 + col * Bp);
 #pragma unroll

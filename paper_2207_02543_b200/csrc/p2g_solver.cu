@@ -777,6 +777,9 @@ int set_values_impl(p2g_handle* h, int32_t batch, const double* host, const doub
     h->setup_done = false;
     const int oldBp = h->Bp;
     const int oldB = h->B;
+    const int64_t bp_est = batch <= 32 ? (batch == 1 ? 1 : (batch <= 8 ? 8 : 32)) : (batch + 63) / 64 * 64;
+    REQ((uint64_t)h->pat.n * (uint64_t)bp_est < ((uint64_t)1 << 32), P2G_EINVAL,
+        "p2g_set_values: n * batch exceeds 2^32 vector elements (split the batch)");
     h->B = batch;
     choose_shape(h, batch);
     if (h->Bp != oldBp || oldB != batch || !h->d_vals) TRY(alloc_batch(h));
