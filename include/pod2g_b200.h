@@ -217,6 +217,58 @@ void* p2g_get_stream(const p2g_handle* h);
  * kernel this handle has executed (setup, prologue and graph iterations). */
 int p2g_launch_counts(const p2g_handle* h, int64_t* per_iteration, int64_t* total_executed);
 
+/* ---- row-partitioned single system -------------
+ * One large system split by contiguous blocks of global rows.  Every rank
+ * owns rows [row_bounds[r], row_bounds[r+1]) (multiples of block_size) and
+ * keeps ghost copies of the rows its rows couple to.  All ranks use ONE
+ * global node colouring (node_colors[g] for every global node g, a proper
+ * colouring of the node graph); the multicolour sweeps then equal the
+ * single-GPU sweeps in the global colour-major order, with the swept vector's
+ * boundary rows exchanged after every colour phase and the scalar partials
+ * (p.Kp, ||r||^2, Phi^T t, r.s) summed across ranks.
+ *   p2g_part_create_local : all `world` partitions in this process on one
+ *                           device (exchange = device copies; for testing and
+ *                           single-GPU runs)
+ *   p2g_part_create_nccl  : this process is rank `rank` of `world`; exchange
+ *                           by NCCL send/recv, sums by NCCL allreduce (uid from
+ *                           p2g_nccl_unique_id on one rank, broadcast by the caller)
+ * The `rank` argument of the per-partition calls names a hosted partition. */
+typedef struct p2g_part p2g_part;
+int p2g_nccl_unique_id(void* uid /* 128 bytes */);
+int p2g_part_create_local(int device, int world, p2g_part** out);
+int p2g_part_create_nccl(int device, int rank, int world, const void* uid, p2g_part** out);
+int p2g_part_destroy(p2g_part* p);
+const char* p2g_part_last_error(const p2g_part* p);
+/* rows [row_bounds[rank], row_bounds[rank+1]) as a CSR with GLOBAL column
+ * indices (row_offsets local, n_own+1 entries) */
+int p2g_part_set_pattern(p2g_part* p, int rank, int64_t n_global, const int64_t* row_bounds,
+                         const uint64_t* row_offsets, const uint64_t* col_indices,
+                         int32_t block_size, const int32_t* node_colors);
+/* n_own, n_ghost and the global row of every ghost slot (ghost_global may be NULL) */
+int p2g_part_ghosts(p2g_part* p, int rank, int64_t* n_own, int64_t* n_ghost,
+                    int64_t* ghost_global);
+int p2g_part_set_values(p2g_part* p, int rank, int32_t batch, const double* values);
+/* phi_own: n_own x k (caller's local row order); phi_ghost: n_ghost x k in
+ * p2g_part_ghosts order */
+int p2g_part_set_basis(p2g_part* p, int rank, int32_t k, const double* phi_own,
+                       const double* phi_ghost);
+/* collective over all hosted partitions (and all ranks) */
+int p2g_part_setup(p2g_part* p, const p2g_config* cfg, int32_t* status);
+/* b, x0, x: one pointer per hosted partition ([B][n_own]); iters / converged
+ * / status / hist as p2g_solve (identical on every rank) */
+int p2g_part_solve(p2g_part* p, const double* const* b, const double* const* x0, int32_t x0_mode,
+                   double tol, int64_t max_iter, double* const* x, int64_t* iters,
+                   int32_t* converged, int32_t* status, double* hist, int64_t hist_cap);
+int p2g_part_last_solve_ms(const p2g_part* p, double* ms);
+/* Host-only (no device): the partition plan of one rank.  sizes = {n_own,
+ * n_ghost, nnz, ncolors}; send_counts / recv_counts ([ncolors][world], zeroed
+ * by the caller) accumulate the rows exchanged with each peer per colour. */
+int p2g_plan_partition(int rank, int world, const int64_t* row_bounds, int64_t n_global,
+                       const uint64_t* row_offsets, const uint64_t* col_indices,
+                       int32_t block_size, const int32_t* node_colors, int64_t* sizes,
+                       int64_t* ghost_global, int64_t* send_counts, int64_t* recv_counts,
+                       char* errbuf, int32_t errcap);
+
 #ifdef __cplusplus
 }
 #endif

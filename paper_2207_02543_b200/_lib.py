@@ -48,6 +48,21 @@ SIGNATURES = [
     ("p2g_profile_iteration", C.c_int, [H, C.c_int32, D, D, C.POINTER(C.c_char_p)]),
     ("p2g_launch_counts", C.c_int, [H, I64, I64]),
     ("p2g_get_stream", C.c_void_p, [H]),
+    ("p2g_nccl_unique_id", C.c_int, [C.c_void_p]),
+    ("p2g_part_create_local", C.c_int, [C.c_int, C.c_int, C.POINTER(H)]),
+    ("p2g_part_create_nccl", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(H)]),
+    ("p2g_part_destroy", C.c_int, [H]),
+    ("p2g_part_last_error", C.c_char_p, [H]),
+    ("p2g_part_set_pattern", C.c_int, [H, C.c_int, C.c_int64, I64, U64, U64, C.c_int32, I32]),
+    ("p2g_part_ghosts", C.c_int, [H, C.c_int, I64, I64, I64]),
+    ("p2g_part_set_values", C.c_int, [H, C.c_int, C.c_int32, D]),
+    ("p2g_part_set_basis", C.c_int, [H, C.c_int, C.c_int32, D, D]),
+    ("p2g_part_setup", C.c_int, [H, C.c_void_p, I32]),
+    ("p2g_part_solve", C.c_int, [H, C.POINTER(D), C.POINTER(D), C.c_int32, C.c_double, C.c_int64,
+                                 C.POINTER(D), I64, I32, I32, D, C.c_int64]),
+    ("p2g_part_last_solve_ms", C.c_int, [H, D]),
+    ("p2g_plan_partition", C.c_int, [C.c_int, C.c_int, I64, C.c_int64, U64, U64, C.c_int32, I32,
+                                     I64, I64, I64, I64, C.c_char_p, C.c_int32]),
     # pod2g_gen.h
     ("p2g_mesh_create", C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_double,
                                   C.c_double, C.c_double, C.c_double, C.POINTER(H)]),

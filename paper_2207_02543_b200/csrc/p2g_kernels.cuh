@@ -1354,4 +1354,47 @@ __global__ void k_cholesky(int B, int k, const double* Ac, double* L, int* statu
     if (lane == 0 && bad && status[b] == ST_OK) status[b] = ST_ESINGULAR;
 }
 
+// ---------------------------------------------------------------- partitions
+// part[0][j] = sum_{q < nrows} part[q][j] (fixed order, in place): the local
+// total of a partial-row buffer before the cross-rank allreduce
+__global__ void k_reduce_rows(double* part, int nrows, int ncols) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ncols; j += gridDim.x * blockDim.x) {
+        double t = 0.0;
+        for (int q = 0; q < nrows; ++q) t += part[(size_t)q * ncols + j];
+        part[j] = t;
+    }
+}
+
+constexpr int kMaxParts = 16;
+struct PartPtrs {
+    double* p[kMaxParts];
+    int* ip[kMaxParts];
+};
+// emulated allreduce over the in-process partitions: fixed rank order
+__global__ void k_sum_parts(PartPtrs pp, int np, int n) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        double t = 0.0;
+        for (int q = 0; q < np; ++q) t += pp.p[q][j];
+        for (int q = 0; q < np; ++q) pp.p[q][j] = t;
+    }
+}
+__global__ void k_max_parts_int(PartPtrs pp, int np, int n) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        int t = 0;
+        for (int q = 0; q < np; ++q) t = max(t, pp.ip[q][j]);
+        for (int q = 0; q < np; ++q) pp.ip[q][j] = t;
+    }
+}
+// buf[m][b] = X[rows[m]][b]: pack the boundary rows a peer needs
+__global__ void k_pack_rows(const double* __restrict__ X, int Bp, const int* __restrict__ rows,
+                            int64_t count, double* __restrict__ buf) {
+    const int64_t total = count * Bp;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = e / Bp;
+        const int b = (int)(e % Bp);
+        buf[e] = X[(size_t)rows[m] * Bp + b];
+    }
+}
+
 }  // namespace p2g

@@ -23,6 +23,10 @@
 #include "../../include/pod2g_b200.h"
 #include "p2g_kernels.cuh"
 #include "p2g_pattern.h"
+#include "p2g_partition.h"
+
+#include <dlfcn.h>
+#include <nccl.h>
 
 using namespace p2g;
 
@@ -56,6 +60,8 @@ struct p2g_handle {
     // pattern
     ColouredPattern pat;
     bool have_pattern = false;
+    int64_t n_ghost = 0;         // partitioned handles: ghost rows after the owned ones
+    bool own_stream = true;
     int *d_rp = nullptr, *d_ci = nullptr, *d_dpos = nullptr;
     int64_t *d_vperm = nullptr, *d_perm = nullptr;
 
@@ -467,7 +473,7 @@ struct Run {
 
     static int prolong(p2g_handle* h, double* s, bool assign) {
         const int k = h->k;
-        const int n = static_cast<int>(h->pat.n);
+        const int n = static_cast<int>(h->pat.n + h->n_ghost);  // ghosts too (partitioned)
         if constexpr (Sh::S == 1) {  // batched tiles: shared-memory tiled prolongation
             constexpr int TB = Sh::T;
             KSWITCH(k, {
@@ -599,7 +605,7 @@ struct Run {
     }
 
     // ---- setup: A_c = Phi^T K Phi per instance, then Cholesky
-    static int coarse_setup(p2g_handle* h) {
+    static int coarse_setup(p2g_handle* h, bool factor = true) {
         const int k = h->k;
         const int n = static_cast<int>(h->pat.n);
         Mat A = mat_of(h);
@@ -640,6 +646,7 @@ struct Run {
             h->err = "coarse_setup: kernel launch failed";
             return st;
         }
+        if (!factor) return P2G_OK;
         k_cholesky<<<(h->B + 7) / 8, 256, 0, h->stream>>>(h->B, k, h->d_Ac, h->d_L,
                                                           h->d_setup_status); ++h->launches_executed;
         CU(cudaGetLastError());
@@ -721,7 +728,7 @@ void destroy_graph(p2g_handle* h) {
 }
 
 int alloc_batch(p2g_handle* h) {
-    const size_t nv = (size_t)h->pat.n * h->Bp;
+    const size_t nv = (size_t)(h->pat.n + h->n_ghost) * h->Bp;
     TRY(dalloc(h, h->d_vals, (size_t)h->pat.nnz * h->Bp));
     CU(cudaMemsetAsync(h->d_vals, 0, (size_t)h->pat.nnz * h->Bp * sizeof(double), h->stream));
     for (double** p : {&h->d_u, &h->d_r, &h->d_s, &h->d_s2, &h->d_p, &h->d_Kp, &h->d_b, &h->d_t}) {
@@ -1045,7 +1052,7 @@ int p2g_destroy(p2g_handle* h) {
     dfree(h->d_part_ac);
     for (auto& e : h->ev) cudaEventDestroy(e);
     for (auto& e : h->kev) cudaEventDestroy(e);
-    cudaStreamDestroy(h->stream);
+    if (h->own_stream) cudaStreamDestroy(h->stream);
     delete h;
     return P2G_OK;
 }
@@ -1379,3 +1386,786 @@ int p2g_launch_counts(const p2g_handle* h, int64_t* per_iteration, int64_t* last
 }
 
 }  // extern "C"
+
+// ============================================================================
+// Row-partitioned single-system path
+//
+// A p2g_part holds the partitions this process hosts: every rank of the job
+// for the in-process (emulated) transport, or exactly one rank for NCCL.
+// Each partition is an ordinary handle whose pattern is its owned rows (in
+// the global colour-major order) plus ghost rows; the same kernels run on the
+// owned rows and read ghosts through local column indices.  Per iteration the
+// exchange steps are: the swept vector after every forward and backward
+// colour phase (only that colour's boundary rows move), and allreduces of
+// the scalar partials (pKp; ||r||^2; Phi^T t; r.s).  The prolongation is
+// applied to ghost rows locally (ghost rows of Phi are stored; e is
+// replicated), so s' needs no exchange.
+// ============================================================================
+namespace {
+
+struct NcclApi {
+    void* lib = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    bool load(std::string& err) {
+        if (lib) return true;
+        lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) {
+            err = "dlopen(libnccl.so.2) failed";
+            return false;
+        }
+#define P2G_SYM(f, name) f = reinterpret_cast<decltype(f)>(dlsym(lib, name)); if (!f) { err = std::string("missing ") + name; return false; }
+        P2G_SYM(GetUniqueId, "ncclGetUniqueId")
+        P2G_SYM(CommInitRank, "ncclCommInitRank")
+        P2G_SYM(CommDestroy, "ncclCommDestroy")
+        P2G_SYM(AllReduce, "ncclAllReduce")
+        P2G_SYM(Send, "ncclSend")
+        P2G_SYM(Recv, "ncclRecv")
+        P2G_SYM(GroupStart, "ncclGroupStart")
+        P2G_SYM(GroupEnd, "ncclGroupEnd")
+        P2G_SYM(GetErrorString, "ncclGetErrorString")
+#undef P2G_SYM
+        return true;
+    }
+};
+NcclApi g_nccl;
+
+struct PartLocal {
+    int rank = 0;
+    p2g_handle* h = nullptr;
+    PartitionPlan plan;
+    // device send lists: all colours, then one block per colour
+    int* d_rows = nullptr;
+    std::vector<int64_t> all_off;                 // per send_all message
+    std::vector<std::vector<int64_t>> col_off;    // [colour][message]
+    int64_t rows_all = 0;
+    std::vector<int64_t> col_base;                // first entry of colour c in d_rows
+    double* d_sendbuf = nullptr;
+    size_t sendbuf_elems = 0;
+};
+
+}  // namespace
+
+struct p2g_part {
+    int device = 0;
+    int world = 1;
+    bool use_nccl = false;
+    ncclComm_t comm = nullptr;
+    cudaStream_t stream = nullptr;
+    std::vector<PartLocal> parts;
+    std::string err;
+    int B = 0;
+    bool setup_done = false;
+    double last_ms = 0;
+    int64_t iters_host = 0;
+};
+
+namespace {
+
+#define PCU(call)                                                                       \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess) {                                                        \
+            P->err = std::string(#call) + ": " + cudaGetErrorString(e_);                \
+            return static_cast<int>(P2G_ECUDA);                                         \
+        }                                                                               \
+    } while (0)
+#define PNC(call)                                                                       \
+    do {                                                                                \
+        ncclResult_t r_ = (call);                                                       \
+        if (r_ != ncclSuccess) {                                                        \
+            P->err = std::string(#call) + ": " + g_nccl.GetErrorString(r_);             \
+            return static_cast<int>(P2G_ENCCL);                                         \
+        }                                                                               \
+    } while (0)
+#define PTRY(expr)                                                                      \
+    do {                                                                                \
+        int st_ = (expr);                                                               \
+        if (st_ != P2G_OK) {                                                            \
+            if (P->err.empty()) P->err = "partition step failed";                       \
+            return st_;                                                                 \
+        }                                                                               \
+    } while (0)
+
+PartLocal* local_of(p2g_part* P, int rank) {
+    for (auto& L : P->parts)
+        if (L.rank == rank) return &L;
+    return nullptr;
+}
+
+// send the boundary rows of `vec` (member of the handle) of one colour
+// (colour < 0: all ghosts) into the peers' ghost rows
+int part_exchange(p2g_part* P, double* p2g_handle::*vec, int colour) {
+    for (auto& L : P->parts) {
+        p2g_handle* h = L.h;
+        const int64_t base = colour < 0 ? 0 : L.col_base[colour];
+        const int64_t cnt = colour < 0 ? L.rows_all : L.col_base[colour + 1] - L.col_base[colour];
+        if (cnt == 0) continue;
+        const int64_t total = cnt * h->Bp;
+        const int grid = (int)std::min<int64_t>((total + 255) / 256, 4096);
+        k_pack_rows<<<grid, 256, 0, P->stream>>>(h->*vec, h->Bp, L.d_rows + base, cnt, L.d_sendbuf);
+        ++h->launches_executed;
+        PCU(cudaGetLastError());
+    }
+    if (!P->use_nccl) {
+        for (auto& L : P->parts) {  // receive side
+            const auto& recvs = colour < 0 ? L.plan.recv_all : L.plan.recv_c[colour];
+            for (const auto& rm : recvs) {
+                PartLocal* S = local_of(P, rm.peer);
+                if (!S) {
+                    P->err = "partition: peer not hosted in this process";
+                    return P2G_ESTATE;
+                }
+                const auto& sends = colour < 0 ? S->plan.send_all : S->plan.send_c[colour];
+                const auto& offs = colour < 0 ? S->all_off : S->col_off[colour];
+                int64_t off = -1, cnt = 0;
+                for (size_t q = 0; q < sends.size(); ++q)
+                    if (sends[q].peer == L.rank) {
+                        off = offs[q];
+                        cnt = sends[q].count;
+                    }
+                if (off < 0 || cnt != rm.count) {
+                    P->err = "partition: send/receive lists disagree (pattern not symmetric?)";
+                    return P2G_EINVAL;
+                }
+                const int Bp = L.h->Bp;
+                PCU(cudaMemcpyAsync((L.h->*vec) + (size_t)rm.ghost_off * Bp,
+                                    S->d_sendbuf + (size_t)off * Bp, sizeof(double) * cnt * Bp,
+                                    cudaMemcpyDeviceToDevice, P->stream));
+            }
+        }
+        return P2G_OK;
+    }
+    PartLocal& L = P->parts[0];
+    const int Bp = L.h->Bp;
+    const auto& sends = colour < 0 ? L.plan.send_all : L.plan.send_c[colour];
+    const auto& offs = colour < 0 ? L.all_off : L.col_off[colour];
+    const auto& recvs = colour < 0 ? L.plan.recv_all : L.plan.recv_c[colour];
+    PNC(g_nccl.GroupStart());
+    for (size_t q = 0; q < sends.size(); ++q)
+        PNC(g_nccl.Send(L.d_sendbuf + (size_t)offs[q] * Bp, sends[q].count * Bp, ncclFloat64,
+                        sends[q].peer, P->comm, P->stream));
+    for (const auto& rm : recvs)
+        PNC(g_nccl.Recv((L.h->*vec) + (size_t)rm.ghost_off * Bp, rm.count * Bp, ncclFloat64, rm.peer,
+                        P->comm, P->stream));
+    PNC(g_nccl.GroupEnd());
+    return P2G_OK;
+}
+
+// reduce each partition's partial rows to row 0, then sum row 0 across ranks
+int part_allreduce(p2g_part* P, double* p2g_handle::*buf, int nrows, int ncols) {
+    for (auto& L : P->parts) {
+        if (nrows > 1) {
+            k_reduce_rows<<<(ncols + 255) / 256, 256, 0, P->stream>>>(L.h->*buf, nrows, ncols);
+            ++L.h->launches_executed;
+        }
+    }
+    if (P->world == 1) return P2G_OK;
+    if (!P->use_nccl) {
+        PartPtrs pp{};
+        for (size_t q = 0; q < P->parts.size(); ++q) pp.p[q] = P->parts[q].h->*buf;
+        k_sum_parts<<<(ncols + 255) / 256, 256, 0, P->stream>>>(pp, (int)P->parts.size(), ncols);
+        ++P->parts[0].h->launches_executed;
+        PCU(cudaGetLastError());
+        return P2G_OK;
+    }
+    double* b = P->parts[0].h->*buf;
+    PNC(g_nccl.AllReduce(b, b, ncols, ncclFloat64, ncclSum, P->comm, P->stream));
+    return P2G_OK;
+}
+
+int part_allmax_int(p2g_part* P, int* p2g_handle::*buf, int n) {
+    if (P->world == 1) return P2G_OK;
+    if (!P->use_nccl) {
+        PartPtrs pp{};
+        for (size_t q = 0; q < P->parts.size(); ++q) pp.ip[q] = P->parts[q].h->*buf;
+        k_max_parts_int<<<(n + 255) / 256, 256, 0, P->stream>>>(pp, (int)P->parts.size(), n);
+        PCU(cudaGetLastError());
+        return P2G_OK;
+    }
+    int* b = P->parts[0].h->*buf;
+    PNC(g_nccl.AllReduce(b, b, n, ncclInt32, ncclMax, P->comm, P->stream));
+    return P2G_OK;
+}
+
+template <class F>
+int for_parts(p2g_part* P, F&& f) {
+    for (auto& L : P->parts) {
+        const int st = f(L.h);
+        if (st != P2G_OK) {
+            if (P->err.empty()) P->err = L.h->err;
+            return st;
+        }
+    }
+    return P2G_OK;
+}
+
+template <class Sh>
+struct PartRun {
+    using R = Run<Sh>;
+
+    // s = B r on every partition (update: the PCG update of u, r first);
+    // returns the partial-row counts of ||r||^2 (update only) and r.s
+    static int precond(p2g_part* P, bool update, int* nb_rr, int* rs_rows) {
+        const int C = P->parts[0].h->pat.ncolors;
+        const bool rec = kp_recurrence(P->parts[0].h);
+        const bool upper = P->parts[0].h->cfg.residual_form == P2G_RESIDUAL_UPPER;
+        PTRY(for_parts(P, [&](p2g_handle* h) { return R::update_pre(h, update, h->d_r, nb_rr); }));
+        PTRY(part_exchange(P, &p2g_handle::d_s, 0));
+        for (int c = 1; c < C; ++c) {
+            PTRY(for_parts(P, [&](p2g_handle* h) { return R::gs_forward(h, h->d_r, h->d_s, c, true); }));
+            PTRY(part_exchange(P, &p2g_handle::d_s, c));
+        }
+        int nbc = 0;
+        if (P->parts[0].h->k > 0) {
+            PTRY(for_parts(P, [&](p2g_handle* h) {
+                return R::restrict_(h, upper ? RES_UPPER : RES_FULL, h->d_r, h->d_s, &nbc);
+            }));
+            const int kk = P->parts[0].h->k, Bp = P->parts[0].h->Bp;
+            PTRY(part_allreduce(P, &p2g_handle::d_part_c, nbc, kk * Bp));
+            PTRY(for_parts(P, [&](p2g_handle* h) { return R::coarse(h, 1); }));
+            PTRY(for_parts(P, [&](p2g_handle* h) { return R::prolong(h, h->d_s, false); }));
+        }
+        double* p2g_handle::*out = rec ? &p2g_handle::d_s2 : &p2g_handle::d_s;
+        for (int c = C - 1; c >= 0; --c) {
+            PTRY(for_parts(P, [&](p2g_handle* h) {
+                return R::gs_backward(h, h->d_r, h->d_s, h->*out, c, true, rs_rows, c == C - 1);
+            }));
+            PTRY(part_exchange(P, out, c));
+        }
+        for (auto& L : P->parts) {
+            L.h->s_final = L.h->*out;
+            L.h->s_prol = L.h->d_s;
+        }
+        return P2G_OK;
+    }
+
+    static int iteration(p2g_part* P) {
+        p2g_handle* h0 = P->parts[0].h;
+        const bool rec = kp_recurrence(h0);
+        const int Bp = h0->Bp;
+        int nb_dot = R::kp_rows(h0), nb_rr = 0, rs_rows = 0;
+        if (!rec) {
+            PTRY(part_exchange(P, &p2g_handle::d_p, -1));
+            PTRY(for_parts(P, [&](p2g_handle* h) { return R::spmv(h, h->d_p, h->d_Kp, true, &nb_dot); }));
+        }
+        PTRY(part_allreduce(P, &p2g_handle::d_part_dot, nb_dot, Bp));
+        PTRY(for_parts(P, [&](p2g_handle* h) {
+            k_alpha<<<(h->Bp + 7) / 8, 256, 0, h->stream>>>(h->Bp, 1, h->d_part_dot, h->d_rsold,
+                                                           h->d_alpha, h->d_active, h->d_status);
+            count_launch(h, KC_REDUCE);
+            return P2G_OK;
+        }));
+        PTRY(precond(P, true, &nb_rr, &rs_rows));
+        PTRY(part_allreduce(P, &p2g_handle::d_part_rr, nb_rr, Bp));
+        PTRY(part_allreduce(P, &p2g_handle::d_part_rs, rs_rows, Bp));
+        PTRY(for_parts(P, [&](p2g_handle* h) {
+            k_finalize<<<(h->Bp + 7) / 8, 256, 0, h->stream>>>(
+                h->Bp, 1, h->d_part_rs, 1, h->d_part_rr, h->d_fnorm, h->d_rsold, h->d_beta,
+                h->d_rel, h->d_iters, h->d_active, h->d_status, h->d_hist, h->d_prm,
+                h->d_flag_ticket, h->cond, 0);
+            count_launch(h, KC_REDUCE);
+            return P2G_OK;
+        }));
+        if (rec)
+            PTRY(for_parts(P, [&](p2g_handle* h) { return R::kp_update(h, h->s_final, h->s_prol, nullptr); }));
+        else
+            PTRY(for_parts(P, [&](p2g_handle* h) { return R::pupdate(h, h->s_final, false); }));
+        return P2G_OK;
+    }
+
+    static int setup(p2g_part* P) {
+        // A_c per partition (owned rows; ghost rows of Phi for K Phi), summed
+        // over ranks, then factored identically everywhere
+        p2g_handle* h0 = P->parts[0].h;
+        if (h0->k > 0) {
+            PTRY(for_parts(P, [&](p2g_handle* h) { return R::coarse_setup(h, false); }));
+            PTRY(part_allreduce(P, &p2g_handle::d_Ac, 1, h0->k * h0->k * h0->Bp));
+            PTRY(for_parts(P, [&](p2g_handle* h) {
+                k_cholesky<<<(h->B + 7) / 8, 256, 0, h->stream>>>(h->B, h->k, h->d_Ac, h->d_L,
+                                                                  h->d_setup_status);
+                ++h->launches_executed;
+                return P2G_OK;
+            }));
+        }
+        return P2G_OK;
+    }
+
+    static int prologue(p2g_part* P, int x0_mode) {
+        p2g_handle* h0 = P->parts[0].h;
+        const int Bp = h0->Bp;
+        if (x0_mode == P2G_X0_REDUCED) {
+            int nbc = 0;
+            PTRY(for_parts(P, [&](p2g_handle* h) { return R::restrict_(h, RES_VECTOR, h->d_b, nullptr, &nbc); }));
+            PTRY(part_allreduce(P, &p2g_handle::d_part_c, nbc, h0->k * Bp));
+            PTRY(for_parts(P, [&](p2g_handle* h) { return R::coarse(h, 1); }));
+            PTRY(for_parts(P, [&](p2g_handle* h) { return R::prolong(h, h->d_u, true); }));
+        } else if (x0_mode == P2G_X0_GIVEN) {
+            PTRY(part_exchange(P, &p2g_handle::d_u, -1));
+        }
+        int nb = 0;
+        PTRY(for_parts(P, [&](p2g_handle* h) { return R::residual(h, h->d_b, h->d_u, h->d_r, &nb); }));
+        PTRY(part_allreduce(P, &p2g_handle::d_part_rr, nb, Bp));
+        PTRY(part_allreduce(P, &p2g_handle::d_part_ff, nb, Bp));
+        PTRY(for_parts(P, [&](p2g_handle* h) {
+            k_init_rel<<<(h->Bp + 7) / 8, 256, 0, h->stream>>>(
+                h->Bp, h->B, 1, h->d_part_rr, h->d_part_ff, h->d_fnorm, h->d_rel, h->d_iters,
+                h->d_active, h->d_status, h->d_setup_status, h->d_hist, h->d_prm);
+            count_launch(h, KC_REDUCE);
+            return P2G_OK;
+        }));
+        int rs_rows = 0;
+        PTRY(precond(P, false, nullptr, &rs_rows));
+        PTRY(part_allreduce(P, &p2g_handle::d_part_rs, rs_rows, Bp));
+        PTRY(for_parts(P, [&](p2g_handle* h) {
+            k_init_rs<<<(h->Bp + 7) / 8, 256, 0, h->stream>>>(h->Bp, 1, h->d_part_rs, h->d_rsold,
+                                                              h->d_active, h->d_status);
+            count_launch(h, KC_REDUCE);
+            return R::pupdate(h, h->s_final, true);
+        }));
+        if (kp_recurrence(h0)) {
+            PTRY(part_exchange(P, &p2g_handle::d_p, -1));
+            PTRY(for_parts(P, [&](p2g_handle* h) { return R::spmv(h, h->d_p, h->d_Kp, true, nullptr); }));
+        }
+        return P2G_OK;
+    }
+};
+
+template <class F>
+int pdispatch(p2g_part* P, F&& f) {
+    switch (P->parts[0].h->shape) {
+        case SH_B1A: return f(PartRun<ShB1a>{});
+        case SH_B1B: return f(PartRun<ShB1b>{});
+        case SH_B8: return f(PartRun<ShB8>{});
+        case SH_B32: return f(PartRun<ShB32>{});
+        default: return f(PartRun<ShB64>{});
+    }
+}
+
+int part_new(int device, int world, p2g_part** out) {
+    p2g_part* P = new p2g_part();
+    P->device = device;
+    P->world = world;
+    if (cudaSetDevice(device) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete P;
+        return P2G_ECUDA;
+    }
+    *out = P;
+    return P2G_OK;
+}
+
+int part_add_local(p2g_part* P, int rank) {
+    PartLocal L;
+    L.rank = rank;
+    const int st = p2g_create(P->device, &L.h);
+    if (st != P2G_OK) return st;
+    cudaStreamDestroy(L.h->stream);  // every partition of the process shares one stream
+    L.h->stream = P->stream;
+    L.h->own_stream = false;
+    P->parts.push_back(std::move(L));
+    return P2G_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int p2g_nccl_unique_id(void* uid) {
+    std::string err;
+    if (!uid || !g_nccl.load(err)) return P2G_ENCCL;
+    ncclUniqueId id;
+    if (g_nccl.GetUniqueId(&id) != ncclSuccess) return P2G_ENCCL;
+    std::memcpy(uid, &id, sizeof(id));
+    return P2G_OK;
+}
+
+int p2g_part_create_local(int device, int world, p2g_part** out) {
+    if (!out || world < 1 || world > kMaxParts) return P2G_EINVAL;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return P2G_ECUDA;
+    p2g_part* P = nullptr;
+    int st = part_new(device, world, &P);
+    if (st != P2G_OK) return st;
+    for (int r = 0; r < world && st == P2G_OK; ++r) st = part_add_local(P, r);
+    if (st != P2G_OK) {
+        p2g_part_destroy(P);
+        return st;
+    }
+    *out = P;
+    return P2G_OK;
+}
+
+int p2g_part_create_nccl(int device, int rank, int world, const void* uid, p2g_part** out) {
+    if (!out || !uid || world < 1 || rank < 0 || rank >= world) return P2G_EINVAL;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return P2G_ECUDA;
+    std::string err;
+    if (!g_nccl.load(err)) return P2G_ENCCL;
+    p2g_part* P = nullptr;
+    int st = part_new(device, world, &P);
+    if (st != P2G_OK) return st;
+    P->use_nccl = true;
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof(id));
+    if (g_nccl.CommInitRank(&P->comm, world, id, rank) != ncclSuccess) {
+        p2g_part_destroy(P);
+        return P2G_ENCCL;
+    }
+    st = part_add_local(P, rank);
+    if (st != P2G_OK) {
+        p2g_part_destroy(P);
+        return st;
+    }
+    *out = P;
+    return P2G_OK;
+}
+
+int p2g_part_destroy(p2g_part* P) {
+    if (!P) return P2G_EINVAL;
+    cudaSetDevice(P->device);
+    cudaStreamSynchronize(P->stream);
+    for (auto& L : P->parts) {
+        if (L.d_rows) cudaFree(L.d_rows);
+        if (L.d_sendbuf) cudaFree(L.d_sendbuf);
+        if (L.h) p2g_destroy(L.h);
+    }
+    if (P->comm) g_nccl.CommDestroy(P->comm);
+    cudaStreamDestroy(P->stream);
+    delete P;
+    return P2G_OK;
+}
+
+const char* p2g_part_last_error(const p2g_part* P) { return P ? P->err.c_str() : "null"; }
+
+int p2g_part_set_pattern(p2g_part* P, int rank, int64_t n_global, const int64_t* row_bounds,
+                         const uint64_t* row_offsets, const uint64_t* col_indices,
+                         int32_t block_size, const int32_t* node_colors) {
+    if (!P) return P2G_EINVAL;
+    PCU(cudaSetDevice(P->device));
+    PartLocal* L = local_of(P, rank);
+    if (!L) {
+        P->err = "p2g_part_set_pattern: rank not hosted by this handle";
+        return P2G_EINVAL;
+    }
+    PartitionPlan plan;
+    const std::string msg = build_partition_plan(rank, P->world, row_bounds, n_global, row_offsets,
+                                                 col_indices, block_size, node_colors, plan);
+    if (!msg.empty()) {
+        P->err = msg;
+        return P2G_EINVAL;
+    }
+    p2g_handle* h = L->h;
+    destroy_graph(h);
+    // the partition's local pattern: owned rows colour-major, ghosts appended
+    ColouredPattern& pat = h->pat;
+    pat = ColouredPattern();
+    pat.n = plan.n_own;
+    pat.nnz = plan.nnz;
+    pat.bs = plan.bs;
+    pat.ncolors = plan.ncolors;
+    pat.color_rows = plan.color_rows;
+    pat.perm.resize(plan.n_own);
+    for (int64_t i = 0; i < plan.n_own; ++i) pat.perm[i] = plan.own_global[i] - plan.row_begin;
+    pat.rp = plan.rp;
+    pat.ci = plan.ci;
+    pat.dpos = plan.dpos;
+    pat.vperm = plan.vperm;
+    h->n_ghost = plan.n_ghost;
+    h->have_pattern = true;
+    h->have_values = false;
+    h->setup_done = false;
+    h->B = 0;
+    h->Bp = 0;
+    h->k = -1;
+    dfree(h->d_vals);
+    auto up = [&](auto*& d, const auto& v) -> int {
+        using T = std::remove_reference_t<decltype(*d)>;
+        TRY(dalloc(h, d, v.size()));
+        CU(cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+        return P2G_OK;
+    };
+    if (up(h->d_rp, pat.rp) || up(h->d_ci, pat.ci) || up(h->d_dpos, pat.dpos) ||
+        up(h->d_vperm, pat.vperm) || up(h->d_perm, pat.perm)) {
+        P->err = h->err;
+        return P2G_ECUDA;
+    }
+    // device send lists
+    std::vector<int32_t> rows;
+    L->all_off.clear();
+    for (const auto& m : plan.send_all) {
+        L->all_off.push_back((int64_t)rows.size());
+        rows.insert(rows.end(), m.rows.begin(), m.rows.end());
+    }
+    L->rows_all = (int64_t)rows.size();
+    L->col_base.assign(plan.ncolors + 1, 0);
+    L->col_off.assign(plan.ncolors, {});
+    for (int c = 0; c < plan.ncolors; ++c) {
+        L->col_base[c] = (int64_t)rows.size();
+        int64_t rel = 0;
+        for (const auto& m : plan.send_c[c]) {
+            L->col_off[c].push_back(rel);
+            rows.insert(rows.end(), m.rows.begin(), m.rows.end());
+            rel += m.count;
+        }
+    }
+    L->col_base[plan.ncolors] = (int64_t)rows.size();
+    if (L->d_rows) cudaFree(L->d_rows);
+    L->d_rows = nullptr;
+    PCU(cudaMalloc(&L->d_rows, sizeof(int32_t) * std::max<size_t>(rows.size(), 1)));
+    PCU(cudaMemcpy(L->d_rows, rows.data(), sizeof(int32_t) * rows.size(), cudaMemcpyHostToDevice));
+    L->plan = std::move(plan);
+    P->setup_done = false;
+    return P2G_OK;
+}
+
+int p2g_part_ghosts(p2g_part* P, int rank, int64_t* n_own, int64_t* n_ghost, int64_t* ghost_global) {
+    if (!P) return P2G_EINVAL;
+    PartLocal* L = local_of(P, rank);
+    if (!L) return P2G_EINVAL;
+    if (n_own) *n_own = L->plan.n_own;
+    if (n_ghost) *n_ghost = L->plan.n_ghost;
+    if (ghost_global)
+        std::memcpy(ghost_global, L->plan.ghost_global.data(), sizeof(int64_t) * L->plan.n_ghost);
+    return P2G_OK;
+}
+
+int p2g_part_set_values(p2g_part* P, int rank, int32_t batch, const double* values) {
+    if (!P) return P2G_EINVAL;
+    PCU(cudaSetDevice(P->device));
+    PartLocal* L = local_of(P, rank);
+    if (!L) return P2G_EINVAL;
+    const int st = set_values_impl(L->h, batch, values, nullptr);
+    if (st != P2G_OK) {
+        P->err = L->h->err;
+        return st;
+    }
+    const size_t need = (size_t)std::max<int64_t>(L->rows_all, 1) * L->h->Bp;
+    if (L->sendbuf_elems < need) {
+        if (L->d_sendbuf) cudaFree(L->d_sendbuf);
+        PCU(cudaMalloc(&L->d_sendbuf, sizeof(double) * need));
+        L->sendbuf_elems = need;
+    }
+    P->B = batch;
+    P->setup_done = false;
+    return P2G_OK;
+}
+
+int p2g_part_set_basis(p2g_part* P, int rank, int32_t k, const double* phi_own,
+                       const double* phi_ghost) {
+    if (!P) return P2G_EINVAL;
+    PCU(cudaSetDevice(P->device));
+    PartLocal* L = local_of(P, rank);
+    if (!L) return P2G_EINVAL;
+    p2g_handle* h = L->h;
+    if (k < 1 || k > 64 || !phi_own || (L->plan.n_ghost > 0 && !phi_ghost)) {
+        P->err = "p2g_part_set_basis: rank in [1,64] and both row blocks required";
+        return P2G_EINVAL;
+    }
+    const int64_t n = h->pat.n, ng = h->n_ghost;
+    std::vector<double> phi((size_t)(n + ng) * k);
+    for (int64_t i = 0; i < n; ++i)
+        for (int a = 0; a < k; ++a) phi[i * k + a] = phi_own[h->pat.perm[i] * k + a];
+    for (int64_t j = 0; j < ng; ++j)
+        for (int a = 0; a < k; ++a) phi[(n + j) * k + a] = phi_ghost[j * k + a];
+    h->k = k;
+    if (ensure(h, h->d_phi, phi.size()) != P2G_OK) return P2G_ECUDA;
+    PCU(cudaMemcpy(h->d_phi, phi.data(), sizeof(double) * phi.size(), cudaMemcpyHostToDevice));
+    if (h->Bp > 0) {
+        if (ensure(h, h->d_e, (size_t)k * h->Bp) || ensure(h, h->d_L, (size_t)k * k * h->Bp) ||
+            ensure(h, h->d_Ac, (size_t)k * k * h->Bp) ||
+            ensure(h, h->d_part_c, (size_t)h->nb_cap * k * h->Bp))
+            return P2G_ECUDA;
+    }
+    P->setup_done = false;
+    return P2G_OK;
+}
+
+int p2g_part_setup(p2g_part* P, const p2g_config* cfg, int32_t* status) {
+    if (!P) return P2G_EINVAL;
+    PCU(cudaSetDevice(P->device));
+    p2g_config c;
+    if (cfg) c = *cfg; else p2g_config_default(&c);
+    if (c.smoother != P2G_SMOOTHER_GS_MULTICOLOR || c.pre_sweeps != 1 || c.post_sweeps != 1) {
+        P->err = "p2g_part_setup: the partitioned path runs the multicolour GS smoother with r1 = r2 = 1";
+        return P2G_EINVAL;
+    }
+    for (auto& L : P->parts) {
+        if (!L.h->have_values || L.h->k < 1 || L.h->B != P->B) {
+            P->err = "p2g_part_setup: every hosted partition needs pattern, values and basis";
+            return P2G_ESTATE;
+        }
+        L.h->cfg = c;
+        PCU(cudaMemsetAsync(L.h->d_setup_status, 0, sizeof(int) * L.h->Bp, P->stream));
+        Mat A = mat_of(L.h);
+        dim3 g(std::max(1, std::min(1024, (int)((L.h->pat.n + 255) / 256))), L.h->B);
+        k_check_diag<<<g, 256, 0, P->stream>>>(A, L.h->B, L.h->d_setup_status);
+    }
+    PTRY(pdispatch(P, [&](auto R) -> int { return decltype(R)::setup(P); }));
+    PTRY(part_allmax_int(P, &p2g_handle::d_setup_status, P->parts[0].h->Bp));
+    PCU(cudaStreamSynchronize(P->stream));
+    std::vector<int> st(P->parts[0].h->Bp);
+    PCU(cudaMemcpy(st.data(), P->parts[0].h->d_setup_status, sizeof(int) * st.size(),
+                   cudaMemcpyDeviceToHost));
+    int worst = P2G_OK;
+    for (int b = 0; b < P->B; ++b) {
+        if (status) status[b] = st[b];
+        if (st[b] != P2G_OK) worst = st[b];
+    }
+    for (auto& L : P->parts) L.h->setup_done = true;
+    P->setup_done = true;
+    return worst;
+}
+
+// b / x: one pointer per hosted partition (in hosted order = rank order for
+// the in-process group), each [B][n_own] in the caller's local row order.
+int p2g_part_solve(p2g_part* P, const double* const* b, const double* const* x0, int32_t x0_mode,
+                   double tol, int64_t max_iter, double* const* x, int64_t* iters,
+                   int32_t* converged, int32_t* status, double* hist, int64_t hist_cap) {
+    if (!P) return P2G_EINVAL;
+    PCU(cudaSetDevice(P->device));
+    if (!P->setup_done) {
+        P->err = "p2g_part_solve: p2g_part_setup not called";
+        return P2G_ESTATE;
+    }
+    if (!b || (x0_mode == P2G_X0_GIVEN && !x0) || max_iter < 0 || hist_cap < 0) {
+        P->err = "p2g_part_solve: bad arguments";
+        return P2G_EINVAL;
+    }
+    const int64_t cap_dev = std::max<int64_t>(hist_cap, 1);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, P->stream);
+    for (size_t q = 0; q < P->parts.size(); ++q) {
+        p2g_handle* h = P->parts[q].h;
+        if (cap_dev > h->hist_cap_alloc || !h->d_hist) {
+            if (dalloc(h, h->d_hist, (size_t)cap_dev * h->Bp) != P2G_OK) return P2G_ECUDA;
+            h->hist_cap_alloc = cap_dev;
+        }
+        SolveParams prm{tol, (long long)max_iter, (long long)hist_cap};
+        PCU(cudaMemcpyAsync(h->d_prm, &prm, sizeof(prm), cudaMemcpyHostToDevice, P->stream));
+        if (upload_interleaved(h, b[q], nullptr, h->pat.n, h->d_perm, h->d_b) != P2G_OK) {
+            P->err = h->err;
+            return P2G_ECUDA;
+        }
+        if (x0_mode == P2G_X0_GIVEN &&
+            upload_interleaved(h, x0[q], nullptr, h->pat.n, h->d_perm, h->d_u) != P2G_OK) {
+            P->err = h->err;
+            return P2G_ECUDA;
+        }
+        if (x0_mode == P2G_X0_ZERO)
+            PCU(cudaMemsetAsync(h->d_u, 0, (size_t)(h->pat.n + h->n_ghost) * h->Bp * sizeof(double),
+                                P->stream));
+        PCU(cudaMemcpyAsync(h->d_active, h->d_all, sizeof(int) * h->Bp, cudaMemcpyDeviceToDevice,
+                            P->stream));
+    }
+    PTRY(pdispatch(P, [&](auto R) -> int { return decltype(R)::prologue(P, x0_mode); }));
+    // host-driven loop: instances deactivate on the device (exact stopping);
+    // the host polls "any active" every kChunk iterations
+    constexpr int kChunk = 8;
+    int* h_flag = nullptr;
+    PCU(cudaMallocHost(&h_flag, sizeof(int)));
+    int64_t done = 0;
+    const int Bp = P->parts[0].h->Bp;
+    std::vector<int> act(Bp);
+    for (;;) {
+        PCU(cudaMemcpyAsync(act.data(), P->parts[0].h->d_active, sizeof(int) * Bp,
+                            cudaMemcpyDeviceToHost, P->stream));
+        PCU(cudaStreamSynchronize(P->stream));
+        bool any = false;
+        for (int v : act) any |= v != 0;
+        if (!any || done >= max_iter) break;
+        for (int q = 0; q < kChunk; ++q)
+            PTRY(pdispatch(P, [&](auto R) -> int { return decltype(R)::iteration(P); }));
+        done += kChunk;
+    }
+    cudaFreeHost(h_flag);
+    for (auto& L : P->parts) {
+        p2g_handle* h = L.h;
+        const dim3 g((unsigned)std::min<int64_t>((h->pat.n + 255) / 256, 1024), h->B);
+        k_check_finite<<<g, 256, 0, P->stream>>>(static_cast<int>(h->pat.n), h->Bp, h->d_u,
+                                                  h->d_status);
+    }
+    PTRY(part_allmax_int(P, &p2g_handle::d_status, Bp));
+    for (size_t q = 0; q < P->parts.size(); ++q)
+        if (x && x[q] && download_interleaved(P->parts[q].h, P->parts[q].h->d_u, x[q], nullptr) != P2G_OK) {
+            P->err = P->parts[q].h->err;
+            return P2G_ECUDA;
+        }
+    cudaEventRecord(e1, P->stream);
+    PCU(cudaStreamSynchronize(P->stream));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    P->last_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    p2g_handle* h = P->parts[0].h;
+    std::vector<int> it(Bp), stt(Bp);
+    std::vector<double> rel(Bp);
+    PCU(cudaMemcpy(it.data(), h->d_iters, sizeof(int) * Bp, cudaMemcpyDeviceToHost));
+    PCU(cudaMemcpy(stt.data(), h->d_status, sizeof(int) * Bp, cudaMemcpyDeviceToHost));
+    PCU(cudaMemcpy(rel.data(), h->d_rel, sizeof(double) * Bp, cudaMemcpyDeviceToHost));
+    int worst = P2G_OK;
+    for (int bb = 0; bb < P->B; ++bb) {
+        if (iters) iters[bb] = it[bb];
+        if (converged) converged[bb] = rel[bb] <= tol ? 1 : 0;
+        if (status) status[bb] = stt[bb];
+        if (stt[bb] != P2G_OK) worst = stt[bb];
+    }
+    if (hist && hist_cap > 0) {
+        PCU(cudaMemcpy(hist, h->d_hist, sizeof(double) * hist_cap * P->B, cudaMemcpyDeviceToHost));
+        for (int bb = 0; bb < P->B; ++bb)
+            for (int64_t q = std::min<int64_t>(it[bb] + 1, hist_cap); q < hist_cap; ++q)
+                hist[bb * hist_cap + q] = NAN;
+    }
+    return worst;
+}
+
+int p2g_part_last_solve_ms(const p2g_part* P, double* ms) {
+    if (!P || !ms) return P2G_EINVAL;
+    *ms = P->last_ms;
+    return P2G_OK;
+}
+
+}  // extern "C"
+
+extern "C" int p2g_plan_partition(int rank, int world, const int64_t* row_bounds, int64_t n_global,
+                                  const uint64_t* row_offsets, const uint64_t* col_indices,
+                                  int32_t block_size, const int32_t* node_colors, int64_t* sizes,
+                                  int64_t* ghost_global, int64_t* send_counts, int64_t* recv_counts,
+                                  char* errbuf, int32_t errcap) {
+    PartitionPlan plan;
+    const std::string msg = build_partition_plan(rank, world, row_bounds, n_global, row_offsets,
+                                                 col_indices, block_size, node_colors, plan);
+    if (!msg.empty()) {
+        if (errbuf && errcap > 0) {
+            std::strncpy(errbuf, msg.c_str(), errcap - 1);
+            errbuf[errcap - 1] = 0;
+        }
+        return P2G_EINVAL;
+    }
+    if (sizes) {
+        sizes[0] = plan.n_own;
+        sizes[1] = plan.n_ghost;
+        sizes[2] = plan.nnz;
+        sizes[3] = plan.ncolors;
+    }
+    if (ghost_global)
+        std::memcpy(ghost_global, plan.ghost_global.data(), sizeof(int64_t) * plan.n_ghost);
+    for (int c = 0; c < plan.ncolors; ++c) {
+        if (send_counts)
+            for (const auto& m : plan.send_c[c]) send_counts[c * world + m.peer] += m.count;
+        if (recv_counts)
+            for (const auto& m : plan.recv_c[c]) recv_counts[c * world + m.peer] += m.count;
+    }
+    return P2G_OK;
+}

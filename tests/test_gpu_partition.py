@@ -1,0 +1,58 @@
+"""GPU tests of the row-partitioned single-system path:
+`world` partitions hosted in one process on one GPU (exchange = device copies)
+must reproduce the single-handle solve -- same global colour-major sweep
+order, so only the cross-partition reductions differ in association."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_2207_02543_b200 import _lib as L
+from paper_2207_02543_b200 import problems as PR
+from paper_2207_02543_b200.partition import setup_partitioned
+from paper_2207_02543_b200.solver import BatchSolver
+from tests.helpers import random_load_basis, to_scipy
+
+pytestmark = pytest.mark.gpu
+
+
+def _problem(dim, B):
+    if dim == 2:
+        m = PR.Mesh(2, 48, 24, 1, 2.0, 1.0, 1.0)
+    else:
+        m = PR.Mesh(3, 8, 8, 8, 1.0, 1.0, 1.0)
+    rp, ci = m.pattern()
+    f = m.rhs()
+    E, _ = m.kl_field(np.arange(B, dtype=np.uint64) + np.uint64(31), 20 if dim == 2 else 30)
+    V = m.assemble(E)
+    phi = random_load_basis(to_scipy(rp, ci, V[0], m.n), 8, 3)
+    return m, rp, ci, f, V, phi
+
+
+@pytest.mark.parametrize("dim,B,world", [(2, 1, 1), (2, 1, 2), (2, 1, 3), (2, 8, 2), (2, 40, 3),
+                                         (3, 1, 2), (3, 8, 4)])
+@pytest.mark.parametrize("kp", [L.KP_RECURRENCE, L.KP_SPMV])
+def test_partitioned_matches_single_handle(gpu, dim, B, world, kp):
+    m, rp, ci, f, V, phi = _problem(dim, B)
+    F = np.broadcast_to(f, (B, m.n)).copy()
+    s = BatchSolver(0)
+    s.set_pattern(rp, ci, m.block_size)
+    s.set_values(V)
+    s.set_basis(phi)
+    s.setup(kp_update=kp)
+    x1, it1, c1, st1, h1 = s.solve(F, None, 1e-8, 3000, x0_mode=L.X0_REDUCED)
+    s.close()
+    P, bounds, bs, st = setup_partitioned(rp, ci, V, f, phi, world, m.block_size, kp_update=kp)
+    assert np.all(st == 0)
+    xs, it2, c2, st2, h2 = P.solve(bs, 1e-8, 3000, L.X0_REDUCED)
+    P.close()
+    x2 = np.concatenate([xs[r] for r in range(world)], axis=1)
+    assert np.all(st2 == 0) and np.all(c2) and np.all(c1)
+    assert np.all(np.abs(it1 - it2) <= 1), (it1, it2)
+    for b in range(B):
+        k = min(int(it1[b]), int(it2[b])) + 1
+        np.testing.assert_allclose(h2[b, :k], h1[b, :k], rtol=1e-8)
+        if it1[b] == it2[b]:
+            assert np.linalg.norm(x2[b] - x1[b]) <= 1e-9 * np.linalg.norm(x1[b])
+    if world == 1:  # one partition = the single handle exactly (same reductions? no: same kernels)
+        assert np.array_equal(it1, it2)
