@@ -45,6 +45,18 @@ int p2g_mesh_element_stiffness(const p2g_mesh* m, double* Ke);
 int p2g_mesh_assemble(const p2g_mesh* m, int64_t B, const double* E, double* values,
                       int32_t nthreads);
 
+/* On-device generation: the B instances K(E_b) written
+ * straight into a solver handle whose pattern is this mesh's (p2g_set_pattern
+ * with p2g_mesh_pattern), replacing p2g_set_values.  E: [B][nelem] host or
+ * device memory.  Same arithmetic as p2g_mesh_assemble (identical bits). */
+struct p2g_handle;
+struct p2g_part;
+int p2g_mesh_assemble_into(const p2g_mesh* m, struct p2g_handle* h, int32_t batch, const double* E,
+                           int32_t E_on_device);
+/* the same for hosted partition `rank` of a row-partitioned system */
+int p2g_part_assemble(struct p2g_part* p, int rank, const p2g_mesh* m, int32_t batch,
+                      const double* E, int32_t E_on_device);
+
 /* Lognormal modulus E = exp(g) per element (piecewise constant at element
  * centroids), g = sigma * sum_{m<M} sqrt(lambda_m) phi_m(x) xi_m with the
  * separable squared-exponential covariance exp(-|x-y|^2 / (2 ell^2)):

@@ -76,6 +76,8 @@ SIGNATURES = [
                                D, D]),
     ("p2g_kl_eigenvalues", C.c_int, [H, C.c_int32, C.c_double, C.c_int32, D]),
     ("p2g_normal_draws", C.c_int, [C.c_uint64, C.c_int64, D]),
+    ("p2g_mesh_assemble_into", C.c_int, [H, H, C.c_int32, C.c_void_p, C.c_int32]),
+    ("p2g_part_assemble", C.c_int, [H, C.c_int, H, C.c_int32, C.c_void_p, C.c_int32]),
 ]
 
 _lib = None

@@ -1354,6 +1354,86 @@ __global__ void k_cholesky(int B, int k, const double* Ac, double* L, int* statu
     if (lane == 0 && bad && status[b] == ST_OK) status[b] = ST_ESINGULAR;
 }
 
+// ---------------------------------------------------------------- generation
+// On-device instance generation: the values of a structured
+// Q4 / hex8 stiffness matrix K(E) = sum_e E_e K_e^1 written straight into the
+// solver's permuted [nnz][Bp] layout.  Each stored entry (node i, comp c;
+// node j, comp d) is the sum over the elements shared by nodes i and j in
+// ascending element order of E_e * Ke1[a c][b d] -- separately rounded
+// multiply and add, exactly the host generator's arithmetic (p2g_mesh.cpp),
+// so both produce identical bits.
+struct AsmDesc {
+    int dim, ned;
+    long long nx, ny, nz;        // elements per axis
+    long long row_begin;         // first global row of this handle's rows
+    long long q_base;            // generator entry index of row_begin
+    const double* Ke;            // ned x ned
+    const unsigned long long* rpg;  // generator row offsets (global)
+};
+
+__device__ __forceinline__ int hex_local(int ox, int oy, int oz) {
+    return (oy ? (ox ? 2 : 3) : (ox ? 1 : 0)) + 4 * oz;
+}
+
+__global__ void __launch_bounds__(kBlock) k_assemble(Mat A, AsmDesc d, const int64_t* __restrict__ perm,
+                                                     const int64_t* __restrict__ vperm,
+                                                     const double* __restrict__ Et, int B,
+                                                     double* vals) {
+    __shared__ double Ks[24 * 24];
+    for (int q = threadIdx.x; q < d.ned * d.ned; q += blockDim.x) Ks[q] = d.Ke[q];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long NX = d.nx + 1, NY = d.ny + 1, NZ = d.dim == 3 ? d.nz + 1 : 1;
+    for (int i = blockIdx.x * kWarps + warp; i < A.n; i += gridDim.x * kWarps) {
+        const long long g = d.row_begin + perm[i];
+        const int c = (int)(g % d.dim);
+        const long long rn = g / d.dim;
+        const long long ix = rn % d.nx + 1, t = rn / d.nx, iy = t % NY, iz = t / NY;
+        const long long ax = max(1LL, ix - 1), bx = min(NX - 1, ix + 1);
+        const long long ay = max(0LL, iy - 1), by = min(NY - 1, iy + 1);
+        const long long az = max(0LL, iz - 1);
+        const long long sx = bx - ax + 1, sy = by - ay + 1;
+        const long long rowq = (long long)d.rpg[g];
+        (void)az;
+        const int kb = A.rp[i], len = A.rp[i + 1] - kb;
+        for (int p = lane; p < len * B; p += 32) {
+            const int k = kb + p / B, b = p % B;
+            const long long o = vperm[k] + d.q_base - rowq;
+            const long long slot = o / d.dim;
+            const int dd = (int)(o % d.dim);
+            const long long jx = ax + slot % sx, jy = ay + (slot / sx) % sy;
+            const long long jz = d.dim == 3 ? max(0LL, iz - 1) + slot / (sx * sy) : 0;
+            const long long ex0 = max(max(ix, jx) - 1, 0LL), ex1 = min(min(ix, jx), d.nx - 1);
+            const long long ey0 = max(max(iy, jy) - 1, 0LL), ey1 = min(min(iy, jy), d.ny - 1);
+            long long ez0 = 0, ez1 = 0;
+            if (d.dim == 3) {
+                ez0 = max(max(iz, jz) - 1, 0LL);
+                ez1 = min(min(iz, jz), d.nz - 1);
+            }
+            double v = 0.0;
+            for (long long ez = ez0; ez <= ez1; ++ez)
+                for (long long ey = ey0; ey <= ey1; ++ey)
+                    for (long long ex = ex0; ex <= ex1; ++ex) {
+                        const int la = hex_local((int)(ix - ex), (int)(iy - ey), (int)(iz - ez));
+                        const int lb = hex_local((int)(jx - ex), (int)(jy - ey), (int)(jz - ez));
+                        const long long e = (ez * d.ny + ey) * d.nx + ex;
+                        v = __dadd_rn(v, __dmul_rn(Et[e * B + b], Ks[(la * d.dim + c) * d.ned + lb * d.dim + dd]));
+                    }
+            vals[(size_t)k * A.Bp + b] = v;
+        }
+    }
+}
+
+// Et[e][b] = E[b][e]
+__global__ void k_transpose_E(const double* __restrict__ E, int B, long long nelem, double* Et) {
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nelem * B;
+         q += (long long)gridDim.x * blockDim.x) {
+        const long long e = q / B;
+        const int b = (int)(q % B);
+        Et[q] = E[(long long)b * nelem + e];
+    }
+}
+
 // ---------------------------------------------------------------- partitions
 // part[0][j] = sum_{q < nrows} part[q][j] (fixed order, in place): the local
 // total of a partial-row buffer before the cross-rank allreduce

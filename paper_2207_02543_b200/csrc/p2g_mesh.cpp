@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "../../include/pod2g_gen.h"
+#include "p2g_mesh_desc.h"
 
 struct p2g_mesh {
     int dim = 2;
@@ -338,6 +339,23 @@ int build_kl(const p2g_mesh* m, int M, double ell, int quad, KL& kl) {
 }
 
 }  // namespace
+
+namespace p2g {
+bool mesh_desc(const p2g_mesh* m, MeshDesc& d) {
+    if (!m) return false;
+    d.dim = m->dim;
+    d.ned = m->ned;
+    d.nx = m->nx;
+    d.ny = m->ny;
+    d.nz = m->nz;
+    d.n = m->n;
+    d.nnz = m->nnz;
+    d.nelem = m->nelem;
+    d.Ke = m->Ke.data();
+    d.rp = m->rp.data();
+    return true;
+}
+}  // namespace p2g
 
 extern "C" {
 

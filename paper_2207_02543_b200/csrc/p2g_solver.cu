@@ -24,6 +24,8 @@
 #include "p2g_kernels.cuh"
 #include "p2g_pattern.h"
 #include "p2g_partition.h"
+#include "p2g_mesh_desc.h"
+#include "../../include/pod2g_gen.h"
 
 #include <dlfcn.h>
 #include <nccl.h>
@@ -776,10 +778,11 @@ int choose_shape(p2g_handle* h, int B) {
     return P2G_OK;
 }
 
-int set_values_impl(p2g_handle* h, int32_t batch, const double* host, const double* dev) {
+int set_values_impl(p2g_handle* h, int32_t batch, const double* host, const double* dev,
+                    bool upload = true) {
     REQ(h->have_pattern, P2G_ESTATE, "p2g_set_values: pattern not set");
     REQ(batch >= 1, P2G_EINVAL, "p2g_set_values: batch must be >= 1");
-    REQ(host || dev, P2G_EINVAL, "p2g_set_values: null values");
+    REQ(!upload || host || dev, P2G_EINVAL, "p2g_set_values: null values");
     
     h->setup_done = false;
     const int oldBp = h->Bp;
@@ -796,9 +799,60 @@ int set_values_impl(p2g_handle* h, int32_t batch, const double* host, const doub
         TRY(ensure(h, h->d_Ac, (size_t)std::max(h->k * h->k, 1) * h->Bp));
         TRY(ensure(h, h->d_part_c, (size_t)h->nb_cap * std::max(h->k, 1) * h->Bp));
     }
-    TRY(upload_interleaved(h, host, dev, h->pat.nnz, h->d_vperm, h->d_vals));
+    if (host || dev) TRY(upload_interleaved(h, host, dev, h->pat.nnz, h->d_vperm, h->d_vals));
     CU(cudaStreamSynchronize(h->stream));
     h->have_values = true;
+    return P2G_OK;
+}
+
+// values generated on the device from a structured mesh
+int assemble_impl(p2g_handle* h, const p2g_mesh* m, int32_t batch, const double* E,
+                  int64_t row_begin, bool E_on_device) {
+    MeshDesc md;
+    REQ(mesh_desc(m, md), P2G_EINVAL, "assemble: null mesh");
+    REQ(h->have_pattern, P2G_ESTATE, "assemble: pattern not set");
+    REQ(E && batch >= 1, P2G_EINVAL, "assemble: null moduli");
+    TRY(set_values_impl(h, batch, nullptr, nullptr, false));
+    // device copies of Ke, the generator row offsets, the moduli
+    double* dKe = nullptr;
+    unsigned long long* drp = nullptr;
+    double *dE = nullptr, *dEt = nullptr;
+    const size_t ne = (size_t)md.nelem * batch;
+    CU(cudaMalloc(&dKe, sizeof(double) * md.ned * md.ned));
+    CU(cudaMalloc(&drp, sizeof(unsigned long long) * (md.n + 1)));
+    CU(cudaMalloc(&dEt, sizeof(double) * ne));
+    CU(cudaMemcpyAsync(dKe, md.Ke, sizeof(double) * md.ned * md.ned, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpyAsync(drp, md.rp, sizeof(unsigned long long) * (md.n + 1), cudaMemcpyHostToDevice,
+                       h->stream));
+    const double* Esrc = E;
+    if (!E_on_device) {
+        CU(cudaMalloc(&dE, sizeof(double) * ne));
+        CU(cudaMemcpyAsync(dE, E, sizeof(double) * ne, cudaMemcpyHostToDevice, h->stream));
+        Esrc = dE;
+    }
+    k_transpose_E<<<4096, 256, 0, h->stream>>>(Esrc, batch, md.nelem, dEt);
+    AsmDesc d;
+    d.dim = md.dim;
+    d.ned = md.ned;
+    d.nx = md.nx;
+    d.ny = md.ny;
+    d.nz = md.nz;
+    d.row_begin = row_begin;
+    d.q_base = (long long)md.rp[row_begin];
+    d.Ke = dKe;
+    d.rpg = drp;
+    Mat A = mat_of(h);
+    const int64_t need = (h->pat.n + kWarps - 1) / kWarps;
+    k_assemble<<<(unsigned)std::min<int64_t>(need, (int64_t)h->num_sms * 8), kBlock, 0, h->stream>>>(
+        A, d, h->d_perm, h->d_vperm, dEt, batch, h->d_vals);
+    h->launches_executed += 2;
+    const cudaError_t e = cudaGetLastError();
+    cudaStreamSynchronize(h->stream);
+    cudaFree(dKe);
+    cudaFree(drp);
+    cudaFree(dEt);
+    if (dE) cudaFree(dE);
+    CU(e);
     return P2G_OK;
 }
 
@@ -2167,5 +2221,42 @@ extern "C" int p2g_plan_partition(int rank, int world, const int64_t* row_bounds
         if (recv_counts)
             for (const auto& m : plan.recv_c[c]) recv_counts[c * world + m.peer] += m.count;
     }
+    return P2G_OK;
+}
+
+extern "C" int p2g_mesh_assemble_into(const p2g_mesh* m, p2g_handle* h, int32_t batch,
+                                      const double* E, int32_t E_on_device) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    MeshDesc md;
+    REQ(mesh_desc(m, md) && md.n == h->pat.n + 0 && md.nnz == h->pat.nnz, P2G_EINVAL,
+        "p2g_mesh_assemble_into: the handle's pattern is not this mesh's");
+    return assemble_impl(h, m, batch, E, 0, E_on_device != 0);
+}
+
+extern "C" int p2g_part_assemble(p2g_part* P, int rank, const p2g_mesh* m, int32_t batch,
+                                 const double* E, int32_t E_on_device) {
+    if (!P) return P2G_EINVAL;
+    PCU(cudaSetDevice(P->device));
+    PartLocal* L = local_of(P, rank);
+    if (!L) return P2G_EINVAL;
+    MeshDesc md;
+    if (!mesh_desc(m, md) || md.n != L->plan.n_global) {
+        P->err = "p2g_part_assemble: mesh does not match the partitioned system";
+        return P2G_EINVAL;
+    }
+    const int st = assemble_impl(L->h, m, batch, E, L->plan.row_begin, E_on_device != 0);
+    if (st != P2G_OK) {
+        P->err = L->h->err;
+        return st;
+    }
+    const size_t need = (size_t)std::max<int64_t>(L->rows_all, 1) * L->h->Bp;
+    if (L->sendbuf_elems < need) {
+        if (L->d_sendbuf) cudaFree(L->d_sendbuf);
+        PCU(cudaMalloc(&L->d_sendbuf, sizeof(double) * need));
+        L->sendbuf_elems = need;
+    }
+    P->B = batch;
+    P->setup_done = false;
     return P2G_OK;
 }

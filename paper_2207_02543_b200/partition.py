@@ -139,6 +139,13 @@ class PartitionedSolver:
                     "set_values")
         self.B = v.shape[0]
 
+    def assemble(self, rank, mesh, E):
+        """Generate partition `rank`'s rows of K(E_b) on the device."""
+        E = np.ascontiguousarray(np.atleast_2d(E), dtype=np.float64)
+        self._check(self._L.p2g_part_assemble(self._p, rank, mesh._h, E.shape[0],
+                                              E.ctypes.data_as(C.c_void_p), 0), "assemble")
+        self.B = E.shape[0]
+
     def set_basis(self, rank, phi_own, phi_ghost):
         po = np.ascontiguousarray(phi_own, dtype=np.float64)
         pg = np.ascontiguousarray(phi_ghost, dtype=np.float64)

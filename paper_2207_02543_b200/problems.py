@@ -225,11 +225,11 @@ def build_problem(cfg: Config, device: int = 0, n_snapshots=None, k=None, solver
     f = mesh.rhs()
     ns = cfg.n_snapshots if n_snapshots is None else n_snapshots
     kk = cfg.k if k is None else k
-    vals = mesh.assemble(mesh.kl_field(snapshot_seeds(cfg, ns), cfg.kl_terms)[0])
+    E = mesh.kl_field(snapshot_seeds(cfg, ns), cfg.kl_terms)[0]
     s = (solver_cls or BatchSolver)(device)
     try:
         s.set_pattern(rp, ci, mesh.block_size)
-        s.set_values(vals)
+        s.assemble(mesh, E)  # on-device generation
         s.set_basis(None)
         s.setup()
         F = np.broadcast_to(f, (ns, mesh.n)).copy()

@@ -144,6 +144,14 @@ class BatchSolver:
                     "set_values_device")
         self.B = batch
 
+    def assemble(self, mesh, E):
+        """Generate the instances K(E_b) on the device (p2g_mesh_assemble_into);
+        E: [B][nelem] host array.  The pattern must be mesh.pattern()."""
+        E = np.ascontiguousarray(np.atleast_2d(E), dtype=np.float64)
+        self._check(self._L.p2g_mesh_assemble_into(mesh._h, self._h, E.shape[0],
+                                                   E.ctypes.data_as(C.c_void_p), 0), "assemble")
+        self.B = E.shape[0]
+
     def set_basis(self, phi):
         if phi is None or (hasattr(phi, "shape") and phi.shape[1] == 0):
             self._check(self._L.p2g_set_basis(self._h, 0, None), "set_basis")

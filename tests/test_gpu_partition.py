@@ -56,3 +56,25 @@ def test_partitioned_matches_single_handle(gpu, dim, B, world, kp):
             assert np.linalg.norm(x2[b] - x1[b]) <= 1e-9 * np.linalg.norm(x1[b])
     if world == 1:  # one partition = the single handle exactly (same reductions? no: same kernels)
         assert np.array_equal(it1, it2)
+
+
+def test_nccl_transport_single_rank(gpu):
+    """The NCCL transport (send/recv + allreduce through libnccl) with one
+    rank must reproduce the in-process partition exactly."""
+    from paper_2207_02543_b200.partition import (PartitionedSolver, local_rows, node_colors,
+                                                 row_bounds)
+    m, rp, ci, f, V, phi = _problem(2, 4)
+    colors = node_colors(rp, ci, m.block_size)
+    bounds = row_bounds(m.n, 1, m.block_size)
+    out = []
+    for uid in (None, PartitionedSolver.unique_id()):
+        P = PartitionedSolver(1, 0, rank=0, nccl_uid=uid)
+        rpl, cil, _ = local_rows(rp, ci, 0, m.n)
+        P.set_pattern(0, m.n, bounds, rpl, cil, m.block_size, colors)
+        P.set_values(0, V)
+        P.set_basis(0, phi, np.zeros((0, phi.shape[1])))
+        assert np.all(P.setup() == 0)
+        xs, it, conv, st, h = P.solve({0: np.broadcast_to(f, (4, m.n))}, 1e-8, 3000)
+        out.append((xs[0], it))
+        P.close()
+    assert np.array_equal(out[0][1], out[1][1]) and np.array_equal(out[0][0], out[1][0])
