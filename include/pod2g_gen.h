@@ -36,6 +36,12 @@ void p2g_mesh_destroy(p2g_mesh* m);
 int p2g_mesh_info(const p2g_mesh* m, int64_t* n, int64_t* nnz, int64_t* nelem,
                   int32_t* block_size);
 int p2g_mesh_pattern(const p2g_mesh* m, uint64_t* row_offsets, uint64_t* col_indices);
+/* rows [r0, r1) only (node aligned): rp local (r1-r0+1 entries), global columns */
+int p2g_mesh_pattern_range(const p2g_mesh* m, int64_t r0, int64_t r1, uint64_t* row_offsets,
+                           uint64_t* col_indices);
+/* parity colouring of the free nodes: (ix%2) + 2(iy%2) [+ 4(iz%2)], a proper
+ * colouring of the Q4 / hex8 node graph (for the row-partitioned path) */
+int p2g_mesh_node_colors(const p2g_mesh* m, int32_t* colors);
 /* consistent nodal traction load on the free dofs */
 int p2g_mesh_rhs(const p2g_mesh* m, double* f);
 /* element stiffness for E = 1 (n_e x n_e, n_e = dim * 2^dim, row-major) */

@@ -70,6 +70,8 @@ SIGNATURES = [
     ("p2g_mesh_info", C.c_int, [H, I64, I64, I64, I32]),
     ("p2g_mesh_pattern", C.c_int, [H, U64, U64]),
     ("p2g_mesh_rhs", C.c_int, [H, D]),
+    ("p2g_mesh_pattern_range", C.c_int, [H, C.c_int64, C.c_int64, U64, U64]),
+    ("p2g_mesh_node_colors", C.c_int, [H, I32]),
     ("p2g_mesh_element_stiffness", C.c_int, [H, D]),
     ("p2g_mesh_assemble", C.c_int, [H, C.c_int64, D, D, C.c_int32]),
     ("p2g_kl_field", C.c_int, [H, C.c_int32, C.c_double, C.c_double, C.c_int32, C.c_int64, U64,

@@ -451,6 +451,49 @@ int p2g_mesh_pattern(const p2g_mesh* m, uint64_t* rp, uint64_t* ci) {
     return P2G_GEN_OK;
 }
 
+int p2g_mesh_pattern_range(const p2g_mesh* m, int64_t r0, int64_t r1, uint64_t* rp,
+                           uint64_t* ci) {
+    if (!m || !rp || r0 < 0 || r1 > m->n || r0 > r1 || r0 % m->dim || r1 % m->dim)
+        return P2G_GEN_EINVAL;
+    const uint64_t base = m->rp[r0];
+    for (int64_t i = r0; i <= r1; ++i) rp[i - r0] = m->rp[i] - base;
+    if (!ci) return P2G_GEN_OK;
+    const Grid G = grid_of(m);
+    const int dim = m->dim;
+    parallel_rows((r1 - r0) / dim, 0, [&](int64_t a0, int64_t a1) {
+        for (int64_t rn = r0 / dim + a0; rn < r0 / dim + a1; ++rn) {
+            int64_t ix, iy, iz;
+            G.coords(rn, ix, iy, iz);
+            int64_t ax, bx, ay, by, az, bz;
+            nb_range(ix, G.NX, 1, ax, bx);
+            nb_range(iy, G.NY, 0, ay, by);
+            nb_range(iz, G.NZ, 0, az, bz);
+            for (int c = 0; c < dim; ++c) {
+                uint64_t w = m->rp[rn * dim + c] - base;
+                for (int64_t jz = az; jz <= bz; ++jz)
+                    for (int64_t jy = ay; jy <= by; ++jy)
+                        for (int64_t jx = ax; jx <= bx; ++jx) {
+                            const int64_t cn = G.rnode(jx, jy, jz);
+                            for (int d = 0; d < dim; ++d) ci[w++] = static_cast<uint64_t>(cn * dim + d);
+                        }
+            }
+        }
+    });
+    return P2G_GEN_OK;
+}
+
+int p2g_mesh_node_colors(const p2g_mesh* m, int32_t* colors) {
+    if (!m || !colors) return P2G_GEN_EINVAL;
+    const Grid G = grid_of(m);
+    const int64_t nn = m->n / m->dim;
+    for (int64_t rn = 0; rn < nn; ++rn) {
+        int64_t ix, iy, iz;
+        G.coords(rn, ix, iy, iz);
+        colors[rn] = static_cast<int32_t>((ix & 1) + 2 * (iy & 1) + (m->dim == 3 ? 4 * (iz & 1) : 0));
+    }
+    return P2G_GEN_OK;
+}
+
 int p2g_mesh_rhs(const p2g_mesh* m, double* f) {
     if (!m || !f) return P2G_GEN_EINVAL;
     std::fill(f, f + m->n, 0.0);

@@ -97,6 +97,8 @@ class Mesh:
         bs = C.c_int32()
         self._L.p2g_mesh_info(h, C.byref(n), C.byref(nnz), C.byref(ne), C.byref(bs))
         self.dim, self.n, self.nnz, self.nelem, self.block_size = dim, n.value, nnz.value, ne.value, bs.value
+        self.nx, self.ny, self.nz = nx, ny, nz if dim == 3 else 1
+        self.h = Lx / nx
 
     @classmethod
     def for_config(cls, cfg: Config):
@@ -118,6 +120,37 @@ class Mesh:
         ci = np.empty(self.nnz, dtype=np.uint64)
         self._L.p2g_mesh_pattern(self._h, rp.ctypes.data_as(L.U64), ci.ctypes.data_as(L.U64))
         return rp, ci
+
+    def pattern_range(self, r0, r1):
+        """Rows [r0, r1) with global columns (node aligned)."""
+        rp = np.empty(r1 - r0 + 1, dtype=np.uint64)
+        if self._L.p2g_mesh_pattern_range(self._h, r0, r1, rp.ctypes.data_as(L.U64), None) != 0:
+            raise ValueError("pattern_range: bad row range")
+        ci = np.empty(int(rp[-1]), dtype=np.uint64)
+        self._L.p2g_mesh_pattern_range(self._h, r0, r1, rp.ctypes.data_as(L.U64),
+                                       ci.ctypes.data_as(L.U64))
+        return rp, ci
+
+    def node_colors(self):
+        col = np.empty(self.n // self.block_size, dtype=np.int32)
+        self._L.p2g_mesh_node_colors(self._h, col.ctypes.data_as(L.I32))
+        return col
+
+    def dof_coords(self, r0=0, r1=None):
+        """(x, y, z, component) of free dofs [r0, r1) (node-major numbering)."""
+        r1 = self.n if r1 is None else r1
+        return self.dof_coords_rows(np.arange(r0, r1, dtype=np.int64))
+
+    def dof_coords_rows(self, g):
+        """(x, y, z, component) of the free dofs with global indices g."""
+        g = np.asarray(g, dtype=np.int64)
+        d = self.block_size
+        rn, comp = g // d, g % d
+        ix = rn % self.nx + 1
+        t = rn // self.nx
+        iy = t % (self.ny + 1)
+        iz = t // (self.ny + 1)
+        return ix * self.h, iy * self.h, iz * self.h, comp
 
     def rhs(self):
         f = np.empty(self.n)
