@@ -44,7 +44,7 @@ constexpr int kCluster = 8;
 // Streaming row kernels are latency bound unless the SM is full: cap them at
 // 32 registers so 8 CTAs x 8 warps (100% occupancy) stay resident (the
 // difference between 4.4 and 6.3 TB/s for the batched SpMV, tools/spmv_lab.cu).
-#define P2G_ROWK __launch_bounds__(kBlock, P2G_MINB)
+#define P2G_ROWK __launch_bounds__(kBlock, Sh::V == 2 ? P2G_MINB : 8)
 #ifndef P2G_MINB
 #define P2G_MINB 4
 #endif
@@ -461,6 +461,51 @@ __global__ void P2G_CLUSTER P2G_ROWK
         }
     }
     if constexpr (UPDATE) cluster_partial<Sh>(rr, part_rr, A.Bp, false);
+}
+
+// Row-parallel PCG update (krylov.hpp:277-278) for the slot-split shapes
+// (S > 1, small batches): every lane owns rows, instead of one lane per row
+// group as in the fused k_update_pre.  u += alpha p ; r += (-alpha) Kp ;
+// cluster partials of r.r.
+template <class Sh>
+__global__ void P2G_CLUSTER P2G_ROWK k_update_rows(int n, int Bp, double* __restrict__ u,
+                                                   double* __restrict__ r,
+                                                   const double* __restrict__ p,
+                                                   const double* __restrict__ Kp,
+                                                   const double* alpha, const int* active,
+                                                   double* part_rr) {
+    constexpr int W = Sh::W, RL = 32 / Sh::W;
+    const int lane = threadIdx.x & 31, w = lane % W, sl = lane / W;
+    const int b0 = blockIdx.y * Sh::T + w * Sh::V;
+    bool m[Sh::V], any;
+    lane_mask<Sh>(active, b0, m, any);
+    double al[Sh::V], rr[Sh::V];
+#pragma unroll
+    for (int v = 0; v < Sh::V; ++v) {
+        al[v] = alpha[b0 + v];
+        rr[v] = 0.0;
+    }
+    if (any) {
+        for (int i = (blockIdx.x * kWarps + (threadIdx.x >> 5)) * RL + sl; i < n;
+             i += gridDim.x * kWarps * RL) {
+            const size_t o = (size_t)i * Bp + b0;
+            double ui[Sh::V], pi[Sh::V], ri[Sh::V], kpi[Sh::V];
+            ldv<Sh::V>(ui, u + o);
+            ldv<Sh::V>(pi, p + o);
+            ldv<Sh::V>(ri, r + o);
+            ldv<Sh::V>(kpi, Kp + o);
+#pragma unroll
+            for (int v = 0; v < Sh::V; ++v) {
+                ui[v] = __dadd_rn(ui[v], __dmul_rn(al[v], pi[v]));
+                ri[v] = __dadd_rn(ri[v], __dmul_rn(-al[v], kpi[v]));
+                rr[v] = __dadd_rn(rr[v], __dmul_rn(ri[v], ri[v]));
+            }
+            stv<Sh::V>(u + o, ui, m);
+            stv<Sh::V>(r + o, ri, m);
+        }
+    }
+    // every lane of an instance holds a partial: reduce over the row lanes
+    cluster_partial<Sh>(rr, part_rr, Bp, false);
 }
 
 // Forward GS colour phase: nodes [nb, ne) of one colour, dofs ascending.

@@ -309,6 +309,28 @@ struct Run {
 
     // pre-smoothing (+ optional PCG update) ; returns the row count of the rr partials
     static int update_pre(p2g_handle* h, bool update, const double* f_r, int* nb_rr) {
+        if constexpr (Sh::S > 1) {
+            // slot-split rows: a row-parallel update kernel, then colour 0 as a
+            // regular forward phase (GS) -- the fused kernel would leave all
+            // but one lane of each row group idle on the vector update
+            if (update) {
+                auto fn = k_update_rows<Sh>;
+                const int n = static_cast<int>(h->pat.n);
+                constexpr int RL = 32 / Sh::W;
+                const int64_t need = (n + kWarps * RL - 1) / (kWarps * RL);
+                int64_t gx = std::min<int64_t>(need, resident_ctas(h, (const void*)fn, true));
+                gx = std::min<int64_t>(std::max<int64_t>(gx, 1), h->nb_cap);
+                gx = (gx + kCluster - 1) / kCluster * kCluster;
+                dim3 g((unsigned)gx, (unsigned)(h->Bp / Sh::T));
+                fn<<<g, kBlock, 0, h->stream>>>(n, h->Bp, h->d_u, h->d_r, h->d_p, h->d_Kp,
+                                                h->d_alpha, h->d_active, h->d_part_rr);
+                if (nb_rr) *nb_rr = g.x / kCluster;
+                count_launch(h, KC_UPDATE);
+                CU(cudaGetLastError());
+            }
+            const double* rr = update ? h->d_r : f_r;
+            if (h->cfg.smoother == P2G_SMOOTHER_GS_MULTICOLOR) return gs_forward(h, rr, h->d_s, 0, true);
+        }
         Mat A = mat_of(h);
         const int pre = h->cfg.smoother == P2G_SMOOTHER_JACOBI ? PRE_JACOBI : PRE_GS;
         const int c0 = static_cast<int>(h->pat.color_rows[1] / h->pat.bs);
@@ -319,9 +341,9 @@ struct Run {
         dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn, true);                         \
         fn<<<g, kBlock, 0, h->stream>>>(A, h->d_u, r, h->d_p, h->d_Kp, h->d_s, h->d_alpha,   \
                                         h->d_active, h->d_part_rr, c0, h->cfg.omega);        \
-        if (nb_rr) *nb_rr = g.x / kCluster;                                                  \
+        if (U && nb_rr) *nb_rr = g.x / kCluster;                                             \
     }
-        if (update) {
+        if (update && Sh::S == 1) {
             if (pre == PRE_GS) P2G_UP(true, PRE_GS) else P2G_UP(true, PRE_JACOBI)
         } else {
             if (pre == PRE_GS) P2G_UP(false, PRE_GS) else P2G_UP(false, PRE_JACOBI)
@@ -757,7 +779,7 @@ int alloc_batch(p2g_handle* h) {
 int choose_shape(p2g_handle* h, int B) {
     const double avg = (double)h->pat.nnz / (double)h->pat.n;
     if (B == 1) {
-        h->shape = avg > 32.0 ? SH_B1B : SH_B1A;
+        h->shape = SH_B1A;  // 4 rows x 8 slots per warp (more rows in flight than a warp per row)
         h->Bp = 1;
     } else if (B <= 8) {
         h->shape = SH_B8;
