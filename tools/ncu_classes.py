@@ -1,0 +1,114 @@
+"""Per-kernel-class summaries of ncu captures, in the classes of
+p2g_profile_iteration (bench.py's roofline).
+
+  full <report.ncu-rep> [--json out]   one --set full capture of
+        `NO_SOLVE=1 python tools/ncu_iter.py c2 2`: the launches from the last
+        k_alpha to the end are one Kp-recurrence PCG iteration; prints the
+        per-kernel table and writes per_iteration_dram_bytes per class.
+  launches <launches.csv> [--json out]  a --metrics gpu__time_duration.sum
+        launch list of bench.py: per-class launch count, time and share.
+"""
+import csv
+import json
+import re
+import sys
+
+sys.path.insert(0, "tools")
+from ncu_summary import load  # noqa: E402
+
+CLASSES = [
+    ("spmv_dot", r"^(void )?k_(spmv|kp_update)\b"),
+    ("update_presmooth", r"^(void )?k_(update_pre|update_rows|jacobi)\b"),
+    ("gs_forward", r"^(void )?k_gs_forward\b"),
+    ("residual_restrict", r"^(void )?k_(residual|restrict_vec|restrict_tiled)\b"),
+    ("coarse_solve", r"^(void )?k_coarse\b"),
+    ("prolong", r"^(void )?k_prolong(_tiled)?\b"),
+    ("gs_backward", r"^(void )?k_gs_backward\b"),
+    ("scalar_reduce", r"^(void )?k_(alpha|finalize|set_cond|reduce_rows|sum_parts)\b"),
+    ("p_update", r"^(void )?k_pupdate\b"),
+]
+
+
+def kclass(name):
+    for c, rx in CLASSES:
+        if re.search(rx, name):
+            return c
+    return "other"
+
+
+def full(path, out):
+    rep = load(path)
+    last = max(i for i, d in enumerate(rep) if re.search(r"^(void )?k_alpha\b", d["kernel"]))
+    it = rep[last:]
+    agg = {}
+    print("%-60s %9s %9s %9s %7s %6s %5s" % ("kernel (one iteration)", "us", "dram_MB", "GB/s",
+                                              "dram%", "warps%", "regs"))
+    for d in it:
+        c = kclass(d["kernel"])
+        by = ((d.get("dram_rd_MB") or 0) + (d.get("dram_wr_MB") or 0)) * 1e6
+        us = d.get("us") or 0.0
+        a = agg.setdefault(c, {"launches": 0, "us": 0.0, "dram_bytes": 0.0})
+        a["launches"] += 1
+        a["us"] += us
+        a["dram_bytes"] += by
+        print("%-60s %9.1f %9.1f %9.0f %7.1f %6.1f %5.0f" % (
+            d["kernel"][:60], us, by / 1e6, by / (us * 1e-6) / 1e9 if us else 0,
+            d.get("dram_pct") or 0, d.get("warps_act") or 0, d.get("regs") or 0))
+    tot = sum(a["us"] for a in agg.values())
+    print("\nclass               launches        us    share   dram_MB    GB/s")
+    for c, a in agg.items():
+        print("%-18s %9d %9.1f %7.1f%% %9.1f %7.0f" % (
+            c, a["launches"], a["us"], 100 * a["us"] / tot, a["dram_bytes"] / 1e6,
+            a["dram_bytes"] / (a["us"] * 1e-6) / 1e9 if a["us"] else 0))
+    res = {"source": path, "capture": "ncu --set full --clock-control none, one PCG iteration "
+                                      "(last k_alpha .. end) of tools/ncu_iter.py",
+           "per_iteration_dram_bytes": {c: a["dram_bytes"] for c, a in agg.items()},
+           "per_iteration_us": {c: a["us"] for c, a in agg.items()},
+           "launches_per_iteration": {c: a["launches"] for c, a in agg.items()},
+           "kernels": it}
+    if out:
+        with open(out, "w") as fh:
+            json.dump(res, fh, indent=1)
+
+
+def launches(path, out):
+    rows = []
+    with open(path) as fh:
+        lines = [ln for ln in fh if not ln.startswith("==")]
+    rd = list(csv.reader(lines))
+    hdr = rd[0]
+    ki, mi, vi, ui = (hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"),
+                      hdr.index("Metric Unit"))
+    for r in rd[1:]:
+        if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
+            continue
+        v = float(r[vi].replace(",", ""))
+        u = r[ui]
+        us = v / 1e3 if u == "nsecond" else (v * 1e3 if u == "msecond" else v)
+        rows.append((r[ki], us))
+    agg = {}
+    for k, us in rows:
+        c = kclass(k)
+        a = agg.setdefault(c, [0, 0.0])
+        a[0] += 1
+        a[1] += us
+    solve = {c: a for c, a in agg.items() if c != "other"}
+    tot = sum(a[1] for a in solve.values())
+    print(f"{len(rows)} launches; solve-loop classes:")
+    print("class               launches        us    share")
+    for c, a in sorted(solve.items(), key=lambda x: -x[1][1]):
+        print("%-18s %9d %9.0f %7.1f%%" % (c, a[0], a[1], 100 * a[1] / tot))
+    if "other" in agg:
+        print("%-18s %9d %9.0f   (setup / generation / bench helpers)" % ("other", *agg["other"]))
+    if out:
+        with open(out, "w") as fh:
+            json.dump({"source": path, "launches": len(rows),
+                       "classes": {c: {"launches": a[0], "us": a[1],
+                                       "share_of_solve": a[1] / tot if c != "other" else None}
+                                   for c, a in agg.items()}}, fh, indent=1)
+
+
+if __name__ == "__main__":
+    mode, path = sys.argv[1], sys.argv[2]
+    out = sys.argv[sys.argv.index("--json") + 1] if "--json" in sys.argv else None
+    {"full": full, "launches": launches}[mode](path, out)
