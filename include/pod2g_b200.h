@@ -202,7 +202,8 @@ int p2g_analyze_pattern(int64_t n, const uint64_t* row_offsets, const uint64_t* 
 
 /* Per-kernel-class timing of the iteration loop: runs `reps` eager
  * iterations (no graph) with CUDA events between kernel classes on the
- * handle's stream, on the current state of the last solve.  ms receives the
+ * handle's stream, on the current state of the last solve (P2G_ESTATE when
+ * no solve ran since p2g_setup: a zero state has p'Kp = 0).  ms receives the
  * mean time per iteration of each class, bytes the algorithmic HBM bytes per
  * iteration of each class, names the class names (static). */
 #define P2G_NUM_KCLASS 9

@@ -44,7 +44,7 @@ constexpr int kCluster = 8;
 // Streaming row kernels are latency bound unless the SM is full: cap them at
 // 32 registers so 8 CTAs x 8 warps (100% occupancy) stay resident (the
 // difference between 4.4 and 6.3 TB/s for the batched SpMV, tools/spmv_lab.cu).
-#define P2G_ROWK __launch_bounds__(kBlock, Sh::V == 2 ? P2G_MINB : 8)
+#define P2G_ROWK __launch_bounds__(kBlock, Sh::W == 1 ? 6 : P2G_MINB)
 #ifndef P2G_MINB
 #define P2G_MINB 4
 #endif
@@ -876,138 +876,319 @@ __global__ void __launch_bounds__(kBlock) k_prolong(int n, int Bp, double* s,
 }
 
 // ---------------------------------------------------------------------------
-// Tiled forms of the prolongation and restriction for batched tiles
-// (TB = 64 or 32 instances per blockIdx.y).  They are small dense products,
-//   S[n][TB] += Phi[n][k] E[k][TB]      and      C[k][TB] = Phi^T[k][n] T[n][TB],
-// so a CTA stages a 32-row tile of Phi (and of T) in shared memory and each
-// thread register-blocks 4 rows (prolong) or ceil(k/8) coefficients
-// (restrict) x TB/32 instances.  Same sums as the row-local kernels, FMA.
-constexpr int kRowTile = 32;
-// row tile: 32 rows, or 16 when k > 40 (static shared memory <= 48 KB)
-template <int KMAX>
-constexpr int row_tile() { return KMAX > 40 ? 16 : 32; }
+// Bulk-copy (TMA) helpers for the staged tensor-core restriction /
+// prolongation (k_restrict_mma / k_prolong_mma): warp 0 streams each 32-row
+// tile of T (or S) and of Phi into one of NS shared-memory stages with
+// cp.async.bulk, completion signalled on the stage's mbarrier (expect_tx).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "P2G_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra P2G_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared bulk copy (16-byte aligned addresses, size multiple of 16)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
 
-template <int TB, int KMAX, bool ASSIGN>
-__global__ void __launch_bounds__(kBlock) k_prolong_tiled(int n, int Bp, double* s,
-                                                          const double* __restrict__ phi, int k,
-                                                          const double* __restrict__ e,
-                                                          const int* active) {
-    constexpr int V = TB / 32;
-    constexpr int RT = row_tile<KMAX>(), RPW = RT / kWarps;  // rows per warp
-    __shared__ double Es[KMAX][TB];
-    __shared__ double Ps[RT][KMAX + 1];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int bt0 = blockIdx.y * TB;
-    for (int q = threadIdx.x; q < k * TB; q += kBlock)
-        Es[q / TB][q % TB] = e[(size_t)(q / TB) * Bp + bt0 + q % TB];
-    bool m[V];
-    bool any = false;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-        m[v] = active[bt0 + lane * V + v] != 0;
-        any |= m[v];
-    }
-    for (int r0 = blockIdx.x * RT; r0 < n; r0 += gridDim.x * RT) {
-        __syncthreads();  // Es ready / previous tile consumed
-        for (int q = threadIdx.x; q < RT * k; q += kBlock) {
-            const int rr = q / k, a = q % k;
-            Ps[rr][a] = (r0 + rr < n) ? __ldg(phi + (size_t)(r0 + rr) * k + a) : 0.0;
-        }
-        __syncthreads();
-        double corr[RPW][V];
-#pragma unroll
-        for (int j = 0; j < RPW; ++j)
-#pragma unroll
-            for (int v = 0; v < V; ++v) corr[j][v] = 0.0;
-#pragma unroll 4
-        for (int a = 0; a < k; ++a) {
-            double ev[V];
-#pragma unroll
-            for (int v = 0; v < V; ++v) ev[v] = Es[a][lane * V + v];
-#pragma unroll
-            for (int j = 0; j < RPW; ++j) {
-                const double p = Ps[warp + 8 * j][a];
-#pragma unroll
-                for (int v = 0; v < V; ++v) corr[j][v] = fma(p, ev[v], corr[j][v]);
-            }
-        }
-        if (any) {
-#pragma unroll
-            for (int j = 0; j < RPW; ++j) {
-                const int i = r0 + warp + 8 * j;
-                if (i < n) {
-                    double* sp = s + (size_t)i * Bp + bt0 + lane * V;
-                    double out[V];
-                    if constexpr (!ASSIGN) {
-                        ldv<V>(out, sp);
-#pragma unroll
-                        for (int v = 0; v < V; ++v) out[v] = __dadd_rn(out[v], corr[j][v]);
-                    } else {
-#pragma unroll
-                        for (int v = 0; v < V; ++v) out[v] = corr[j][v];
-                    }
-                    stv<V>(sp, out, m);
-                }
-            }
-        }
-    }
+// Row stride (doubles) of the padded Phi copy the tensor-core tiles read:
+// k rounded up to 4 (whole k-steps, zero filled), then to 4 mod 8 so both the
+// A-fragment pattern of the restriction (row = lane%4, col = lane/4) and of
+// the prolongation (row = lane/4, col = lane%4) hit each bank exactly twice
+// (two wavefronts, the minimum for 32 x 8 bytes).
+__host__ __device__ constexpr int phi_stride(int k) {
+    return ((k + 3) / 4 * 4) % 8 == 0 ? (k + 3) / 4 * 4 + 4 : (k + 3) / 4 * 4;
+}
+
+// FP64 tensor-core MMA, D(8x8) += A(8x4) B(4x8); fragments (PTX m8n8k4 .f64):
+// a = A[lane/4][lane%4], b = B[lane%4][lane/4], d = D[lane/4][2(lane%4) + {0,1}]
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
 }
 
 template <int TB, int KMAX>
-__global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_restrict_tiled(int n, int Bp,
-                                                           const double* __restrict__ t,
-                                                           const double* __restrict__ phi, int k,
-                                                           const int* active, double* part) {
-    constexpr int V = TB / 32;
-    constexpr int KPW = (KMAX + kWarps - 1) / kWarps;  // coefficients per warp
-    constexpr int RT = row_tile<KMAX>();
-    // staging tiles and the CTA totals share one buffer (totals written last)
-    constexpr int STAGE = RT * TB + RT * (KMAX + 1), TOT = KMAX * TB;
-    __shared__ double smem[STAGE > TOT ? STAGE : TOT];
-    double (*Ts)[TB] = reinterpret_cast<double (*)[TB]>(smem);
-    double (*Ps)[KMAX + 1] = reinterpret_cast<double (*)[KMAX + 1]>(smem + RT * TB);
-    double (*tot)[TB] = reinterpret_cast<double (*)[TB]>(smem);
+struct MmaTile {
+    static constexpr int RT = 32, NS = 4;
+    static constexpr int TS = TB + 8;  // data-row stride: 8 mod 16 doubles (B fragments)
+    static constexpr int KS = phi_stride(KMAX);
+    static constexpr int T_DBL = RT * TS;
+    static constexpr int STAGE = T_DBL + RT * KS;  // a multiple of 4 doubles (32 bytes)
+    static constexpr size_t SMEM = sizeof(double) * (size_t)NS * STAGE + 64;
+};
+
+// warp 0 streams tile `tile` into a stage: the RT Phi rows (one contiguous
+// copy, stride ks) and, WITH_T, the RT data rows (one copy per row into the
+// padded stride TS)
+template <int TB, int KMAX, bool WITH_T>
+__device__ __forceinline__ void mma_issue(double* stage, uint64_t* bar, int tile, int n, int Bp,
+                                          int bt0, const double* data, const double* phit, int ks,
+                                          int lane) {
+    using MT = MmaTile<TB, KMAX>;
+    const int r0 = tile * MT::RT, nr = min(MT::RT, n - r0);
+    const uint32_t pbytes = static_cast<uint32_t>(nr * ks) * 8u;
+    const uint32_t tbytes = WITH_T ? static_cast<uint32_t>(nr) * TB * 8u : 0u;
+    if (lane == 0) mbar_arrive_tx(bar, pbytes + tbytes);
+    __syncwarp();
+    if (lane == 0) bulk_g2s(stage + MT::T_DBL, phit + (size_t)r0 * ks, pbytes, bar);
+    if constexpr (WITH_T)
+        if (lane < nr)
+            bulk_g2s(stage + lane * MT::TS, data + (size_t)(r0 + lane) * Bp + bt0, TB * 8u, bar);
+}
+
+// Restriction C[k][TB] = Phi^T T on the FP64 tensor cores (pod.hpp:33-37,
+// the batched form): per 4-row k-step a warp owns one 8-instance n-block and
+// every 8-coefficient m-block.  With TB = 32 two warps share an n-block and
+// split the k-steps (summed in fixed order).  Persistent CTAs, NS-stage bulk
+// pipeline; per-cluster partial rows as before (deterministic).  Rows past n
+// contribute zeros; coefficients past k read padding and are not stored.
+template <int TB, int KMAX>
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_restrict_mma(int n, int Bp,
+                                                                     const double* __restrict__ t,
+                                                                     const double* __restrict__ phit,
+                                                                     int k, int ks, double* part) {
+    using MT = MmaTile<TB, KMAX>;
+    constexpr int NB = TB / 8, KSPLIT = kWarps / NB, MBX = (KMAX + 7) / 8;
+    extern __shared__ __align__(128) double dsm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm + (size_t)MT::NS * MT::STAGE);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, tg = lane & 3;
+    const int nb = warp % NB, kpart = warp / NB;
     const int bt0 = blockIdx.y * TB;
-    double acc[KPW][V];
-#pragma unroll
-    for (int j = 0; j < KPW; ++j)
-#pragma unroll
-        for (int v = 0; v < V; ++v) acc[j][v] = 0.0;
-    for (int r0 = blockIdx.x * RT; r0 < n; r0 += gridDim.x * RT) {
-        __syncthreads();
-        for (int q = threadIdx.x; q < RT * TB; q += kBlock) {
-            const int rr = q / TB, b = q % TB;
-            Ts[rr][b] = (r0 + rr < n && active[bt0 + b]) ? t[(size_t)(r0 + rr) * Bp + bt0 + b] : 0.0;
+    const int ntiles = (n + MT::RT - 1) / MT::RT;
+    const int mb = (k + 7) / 8;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < MT::NS; ++q) mbar_init(&full[q], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (warp == 0)
+        for (int q = 0; q < MT::NS; ++q) {
+            const int tile = blockIdx.x + q * gridDim.x;
+            if (tile < ntiles)
+                mma_issue<TB, KMAX, true>(dsm + (size_t)q * MT::STAGE, &full[q], tile, n, Bp, bt0, t,
+                                          phit, ks, lane);
         }
-        for (int q = threadIdx.x; q < RT * k; q += kBlock) {
-            const int rr = q / k, a = q % k;
-            Ps[rr][a] = (r0 + rr < n) ? __ldg(phi + (size_t)(r0 + rr) * k + a) : 0.0;
+    double c[MBX][2];
+#pragma unroll
+    for (int m = 0; m < MBX; ++m) c[m][0] = c[m][1] = 0.0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int st = it % MT::NS;
+        const double* Ts = dsm + (size_t)st * MT::STAGE;
+        const double* Ps = Ts + MT::T_DBL;
+        mbar_wait(&full[st], (it / MT::NS) & 1);
+        const int nr = min(MT::RT, n - tile * MT::RT);
+#pragma unroll
+        for (int q = kpart; q < MT::RT / 4; q += KSPLIT) {
+            const int row = 4 * q + tg;
+            const bool ok = row < nr;
+            const double b = ok ? Ts[row * MT::TS + 8 * nb + g] : 0.0;
+#pragma unroll
+            for (int m = 0; m < MBX; ++m)
+                if (m < mb) {
+                    const double a = ok ? Ps[row * ks + 8 * m + g] : 0.0;
+                    dmma(c[m][0], c[m][1], a, b);
+                }
         }
+        __syncthreads();  // stage consumed by every warp
+        const int nxt = tile + MT::NS * gridDim.x;
+        if (warp == 0 && nxt < ntiles)
+            mma_issue<TB, KMAX, true>(dsm + (size_t)st * MT::STAGE, &full[st], nxt, n, Bp, bt0, t, phit,
+                                      ks, lane);
+    }
+    // CTA totals [k][TB] (k-split halves summed in fixed order), then the
+    // fixed-order cluster sum into this cluster's partial row
+    double* tot = dsm;
+    double* tot2 = dsm + KMAX * TB;
+    if (KSPLIT == 1 || kpart == 0) {
+#pragma unroll
+        for (int m = 0; m < MBX; ++m)
+            if (8 * m + g < k) {
+                tot[(8 * m + g) * TB + 8 * nb + 2 * tg] = c[m][0];
+                tot[(8 * m + g) * TB + 8 * nb + 2 * tg + 1] = c[m][1];
+            }
+    } else {
+#pragma unroll
+        for (int m = 0; m < MBX; ++m)
+            if (8 * m + g < k) {
+                tot2[(8 * m + g) * TB + 8 * nb + 2 * tg] = c[m][0];
+                tot2[(8 * m + g) * TB + 8 * nb + 2 * tg + 1] = c[m][1];
+            }
+    }
+    if constexpr (KSPLIT > 1) {
         __syncthreads();
-#pragma unroll 4
-        for (int rr = 0; rr < RT; ++rr) {
-            double tv[V];
+        for (int q = threadIdx.x; q < k * TB; q += kBlock) tot[q] = tot[q] + tot2[q];
+    }
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    if (cl.block_rank() == 0) {
+        double* prow = part + (size_t)(blockIdx.x / kCluster) * k * Bp + bt0;
+        for (int q = threadIdx.x; q < k * TB; q += kBlock) {
+            double tt = 0.0;
 #pragma unroll
-            for (int v = 0; v < V; ++v) tv[v] = Ts[rr][lane * V + v];
+            for (int r = 0; r < kCluster; ++r) tt += cl.map_shared_rank(tot, r)[q];
+            prow[(size_t)(q / TB) * Bp + q % TB] = tt;
+        }
+    }
+    cl.sync();
+}
+
+// Prolongation S[rows][TB] (+)= Phi E on the tensor cores (pod.hpp:40-44 +
+// 201-202, batched): a warp owns one 8-instance n-block and MPW 8-row
+// m-blocks of each 32-row tile; E's B fragments stay in registers; the
+// correction is formed first, then added to S (as the reference's
+// u += 1.0 * lift(e)).  Masked stores keep inactive instances untouched.
+template <int TB, int KMAX, bool ASSIGN>
+__global__ void __launch_bounds__(kBlock) k_prolong_mma(int n, int Bp, double* s,
+                                                        const double* __restrict__ phit, int k,
+                                                        int ks, const double* __restrict__ e,
+                                                        const int* active) {
+    using MT = MmaTile<TB, KMAX>;
+    constexpr int NB = TB / 8, MPW = (MT::RT / 8) * NB / kWarps, KQ = (KMAX + 3) / 4;
+    extern __shared__ __align__(128) double dsm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm + (size_t)MT::NS * MT::STAGE);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, tg = lane & 3;
+    const int nb = warp % NB, m0 = warp / NB;  // m-blocks m0, m0 + kWarps/NB, ...
+    const int bt0 = blockIdx.y * TB;
+    const int ntiles = (n + MT::RT - 1) / MT::RT;
+    const int kq = (k + 3) / 4;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < MT::NS; ++q) mbar_init(&full[q], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (warp == 0)
+        for (int q = 0; q < MT::NS; ++q) {
+            const int tile = blockIdx.x + q * gridDim.x;
+            if (tile < ntiles)
+                mma_issue<TB, KMAX, !ASSIGN>(dsm + (size_t)q * MT::STAGE, &full[q], tile, n, Bp, bt0, s,
+                                             phit, ks, lane);
+        }
+    double be[KQ];
 #pragma unroll
-            for (int j = 0; j < KPW; ++j) {
-                const int a = warp + kWarps * j;
-                if (a < k) {
-                    const double p = Ps[rr][a];
+    for (int q = 0; q < KQ; ++q) {
+        const int a = 4 * q + tg;
+        be[q] = a < k ? e[(size_t)a * Bp + bt0 + 8 * nb + g] : 0.0;
+    }
+    const int col = bt0 + 8 * nb + 2 * tg;
+    const bool m0a = active[col] != 0, m1a = active[col + 1] != 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int st = it % MT::NS;
+        const double* Ss = dsm + (size_t)st * MT::STAGE;
+        const double* Ps = Ss + MT::T_DBL;
+        mbar_wait(&full[st], (it / MT::NS) & 1);
+        const int r0 = tile * MT::RT, nr = min(MT::RT, n - r0);
 #pragma unroll
-                    for (int v = 0; v < V; ++v) acc[j][v] = fma(p, tv[v], acc[j][v]);
+        for (int j = 0; j < MPW; ++j) {
+            const int mrow = 8 * (m0 + j * (kWarps / NB));
+            double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < KQ; ++q)
+                if (q < kq) dmma(c0, c1, Ps[(mrow + g) * ks + 4 * q + tg], be[q]);
+            const int row = mrow + g;
+            if (row < nr) {
+                double* dst = s + (size_t)(r0 + row) * Bp + col;
+                double o0 = c0, o1 = c1;
+                if constexpr (!ASSIGN) {
+                    o0 = __dadd_rn(Ss[row * MT::TS + 8 * nb + 2 * tg], c0);
+                    o1 = __dadd_rn(Ss[row * MT::TS + 8 * nb + 2 * tg + 1], c1);
+                }
+                if (m0a && m1a)
+                    *reinterpret_cast<double2*>(dst) = make_double2(o0, o1);
+                else {
+                    if (m0a) dst[0] = o0;
+                    if (m1a) dst[1] = o1;
                 }
             }
         }
+        __syncthreads();
+        const int nxt = tile + MT::NS * gridDim.x;
+        if (warp == 0 && nxt < ntiles)
+            mma_issue<TB, KMAX, !ASSIGN>(dsm + (size_t)st * MT::STAGE, &full[st], nxt, n, Bp, bt0, s,
+                                         phit, ks, lane);
     }
-    __syncthreads();  // staging tiles consumed: reuse the buffer for the totals
+}
+
+// Register-fed tensor-core forms (no shared-memory staging): every fragment
+// is loaded straight from global memory -- a B fragment of the restriction
+// is 4 rows x 8 consecutive instances (4 x 64 B), a Phi fragment 4 or 8 rows
+// of the padded copy (L1 hits across the CTA's warps) -- with U k-steps (or
+// m-blocks) of loads issued ahead of their MMAs.
+template <int TB, int KMAX>
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock, KMAX > 40 ? 2 : 4) k_restrict_reg(int n, int Bp,
+                                                                        const double* __restrict__ t,
+                                                                        const double* __restrict__ phit,
+                                                                        int k, int ks, double* part) {
+    constexpr int NB = TB / 8, KSPLIT = kWarps / NB, MBX = (KMAX + 7) / 8;
+    constexpr int U = KMAX <= 24 ? 4 : (KMAX <= 40 ? 2 : 1);  // k-steps of loads ahead
+    __shared__ double tot[KSPLIT][KMAX * TB];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, tg = lane & 3;
+    const int nb = warp % NB, kpart = warp / NB;
+    const int bt0 = blockIdx.y * TB;
+    const int mb = (k + 7) / 8;
+    const int nq = (n + 3) / 4;  // 4-row k-steps
+    const int wk = blockIdx.x * KSPLIT + kpart, nwk = gridDim.x * KSPLIT;  // workers
+    const double* tcol = t + bt0 + 8 * nb + g;
+    double c[MBX][2];
 #pragma unroll
-    for (int j = 0; j < KPW; ++j) {
-        const int a = warp + kWarps * j;
-        if (a < k) {
+    for (int m = 0; m < MBX; ++m) c[m][0] = c[m][1] = 0.0;
+    for (int q0 = wk; q0 < nq; q0 += U * nwk) {
+        double b[U], a[U][MBX];
 #pragma unroll
-            for (int v = 0; v < V; ++v) tot[a][lane * V + v] = acc[j][v];
+        for (int u = 0; u < U; ++u) {
+            const int row = 4 * (q0 + u * nwk) + tg;
+            const bool ok = row < n;
+            b[u] = ok ? __ldg(tcol + (size_t)row * Bp) : 0.0;
+#pragma unroll
+            for (int m = 0; m < MBX; ++m)
+                a[u][m] = (ok && m < mb) ? __ldg(phit + (size_t)row * ks + 8 * m + g) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int m = 0; m < MBX; ++m)
+                if (m < mb) dmma(c[m][0], c[m][1], a[u][m], b[u]);
+    }
+#pragma unroll
+    for (int m = 0; m < MBX; ++m)
+        if (8 * m + g < k) {
+            tot[kpart][(8 * m + g) * TB + 8 * nb + 2 * tg] = c[m][0];
+            tot[kpart][(8 * m + g) * TB + 8 * nb + 2 * tg + 1] = c[m][1];
+        }
+    if constexpr (KSPLIT > 1) {
+        __syncthreads();
+        for (int q = threadIdx.x; q < k * TB; q += kBlock) {
+            double x = tot[0][q];
+#pragma unroll
+            for (int r = 1; r < KSPLIT; ++r) x = x + tot[r][q];
+            tot[0][q] = x;
         }
     }
     cg::cluster_group cl = cg::this_cluster();
@@ -1015,14 +1196,77 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_restrict_tiled(int n, in
     if (cl.block_rank() == 0) {
         double* prow = part + (size_t)(blockIdx.x / kCluster) * k * Bp + bt0;
         for (int q = threadIdx.x; q < k * TB; q += kBlock) {
-            const int a = q / TB, b = q % TB;
             double tt = 0.0;
 #pragma unroll
-            for (int r = 0; r < kCluster; ++r) tt += cl.map_shared_rank(smem, r)[a * TB + b];
-            prow[(size_t)a * Bp + b] = tt;
+            for (int r = 0; r < kCluster; ++r) tt += cl.map_shared_rank(&tot[0][0], r)[q];
+            prow[(size_t)(q / TB) * Bp + q % TB] = tt;
         }
     }
     cl.sync();
+}
+
+// the CTA's warps share 8-row m-blocks (NB n-blocks each; with TB = 32 two
+// m-blocks per step); U steps of S / Phi loads issued before their MMAs
+template <int TB, int KMAX, bool ASSIGN>
+__global__ void __launch_bounds__(kBlock, KMAX > 40 ? 2 : 4) k_prolong_reg(int n, int Bp, double* s,
+                                                           const double* __restrict__ phit, int k,
+                                                           int ks, const double* __restrict__ e,
+                                                           const int* active) {
+    constexpr int NB = TB / 8, MSPLIT = kWarps / NB, KQ = (KMAX + 3) / 4;
+    constexpr int U = KMAX <= 24 ? 2 : 1;  // m-blocks of loads ahead
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, tg = lane & 3;
+    const int nb = warp % NB, mpart = warp / NB;
+    const int bt0 = blockIdx.y * TB;
+    const int kq = (k + 3) / 4;
+    double be[KQ];
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) {
+        const int a = 4 * q + tg;
+        be[q] = a < k ? e[(size_t)a * Bp + bt0 + 8 * nb + g] : 0.0;
+    }
+    const int col = bt0 + 8 * nb + 2 * tg;
+    const bool m0a = active[col] != 0, m1a = active[col + 1] != 0;
+    // the whole warp leaves together (mma.sync needs every lane)
+    if (!__any_sync(0xffffffffu, m0a || m1a)) return;
+    const int nmb = (n + 7) / 8;
+    const int wk = blockIdx.x * MSPLIT + mpart, nwk = gridDim.x * MSPLIT;
+    for (int mb0 = wk; mb0 < nmb; mb0 += U * nwk) {
+        double a[U][KQ], sv[U][2];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int row = 8 * (mb0 + u * nwk) + g;
+            const bool ok = row < n;
+#pragma unroll
+            for (int q = 0; q < KQ; ++q)
+                a[u][q] = (ok && q < kq) ? __ldg(phit + (size_t)row * ks + 4 * q + tg) : 0.0;
+            sv[u][0] = sv[u][1] = 0.0;
+            if (!ASSIGN && ok) {
+                const double2 x = *reinterpret_cast<const double2*>(s + (size_t)row * Bp + col);
+                sv[u][0] = x.x;
+                sv[u][1] = x.y;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < KQ; ++q)
+                if (q < kq) dmma(c0, c1, a[u][q], be[q]);
+            const int row = 8 * (mb0 + u * nwk) + g;
+            if (row < n) {
+                double* dst = s + (size_t)row * Bp + col;
+                const double o0 = ASSIGN ? c0 : __dadd_rn(sv[u][0], c0);
+                const double o1 = ASSIGN ? c1 : __dadd_rn(sv[u][1], c1);
+                if (m0a && m1a)
+                    *reinterpret_cast<double2*>(dst) = make_double2(o0, o1);
+                else {
+                    if (m0a) dst[0] = o0;
+                    if (m1a) dst[1] = o1;
+                }
+            }
+        }
+    }
 }
 
 // shape of the row-local kernels (restriction, prolongation): R = 32/W rows

@@ -74,7 +74,9 @@ struct p2g_handle {
 
     // basis
     int k = -1;
-    double* d_phi = nullptr;
+    double* d_phi = nullptr;   // [rows][k]
+    double* d_phit = nullptr;  // [rows][phi_ks], zero padded (tensor-core tiles, phi_stride)
+    int phi_ks = 0;
 
     // vectors [n][Bp]
     double *d_u = nullptr, *d_r = nullptr, *d_s = nullptr, *d_s2 = nullptr, *d_p = nullptr,
@@ -100,6 +102,7 @@ struct p2g_handle {
     // setup
     p2g_config cfg{};
     bool setup_done = false;
+    bool has_state = false;  // a solve ran since the last setup (Krylov state valid)
     double* s_final = nullptr;  // buffer holding B r after the post-smoother
     double* s_prol = nullptr;   // prolongated s' (Kp recurrence)
 
@@ -198,6 +201,20 @@ int kbucket(int k) {
         default: { constexpr int KM = 64; __VA_ARGS__; } break;    \
     }
 
+// upload Phi ([rows][k], already in local row order) and its padded copy
+int upload_phi(p2g_handle* h, const std::vector<double>& phi, int64_t rows, int k) {
+    TRY(ensure(h, h->d_phi, phi.size() + 2));  // +2: 16-byte rounded bulk tile copies
+    CU(cudaMemcpy(h->d_phi, phi.data(), sizeof(double) * phi.size(), cudaMemcpyHostToDevice));
+    const int ks = phi_stride(std::max(k, 1));
+    std::vector<double> pt((size_t)rows * ks, 0.0);
+    for (int64_t i = 0; i < rows; ++i)
+        for (int a = 0; a < k; ++a) pt[i * ks + a] = phi[i * k + a];
+    TRY(ensure(h, h->d_phit, pt.size()));
+    CU(cudaMemcpy(h->d_phit, pt.data(), sizeof(double) * pt.size(), cudaMemcpyHostToDevice));
+    h->phi_ks = ks;
+    return P2G_OK;
+}
+
 bool kp_recurrence(const p2g_handle* h) {
     return h->cfg.smoother == P2G_SMOOTHER_GS_MULTICOLOR && h->cfg.kp_update == P2G_KP_RECURRENCE;
 }
@@ -230,14 +247,17 @@ void count_launch(p2g_handle* h, int kclass) {
 // Resident CTAs per kernel (one full wave), cached per function.  For the
 // cluster kernels this is the number of co-resident CLUSTERS x kCluster, so
 // the grid never spills into a partial second wave.
-int resident_ctas(p2g_handle* h, const void* fn, bool cluster) {
+int resident_ctas(p2g_handle* h, const void* fn, bool cluster, size_t smem = 0) {
     for (auto& e : h->occ_cache)
         if (e.first == fn) return e.second;
     int ctas = 0;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cluster) {
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3(kCluster * 1024, 1, 1);
         lc.blockDim = dim3(kBlock, 1, 1);
+        lc.dynamicSmemBytes = smem;
         int ncl = 0;
         if (cudaOccupancyMaxActiveClusters(&ncl, fn, &lc) != cudaSuccess || ncl <= 0) {
             cudaGetLastError();
@@ -246,7 +266,7 @@ int resident_ctas(p2g_handle* h, const void* fn, bool cluster) {
         ctas = ncl * kCluster;
     } else {
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, smem);
         ctas = std::max(occ, 1) * h->num_sms;
     }
     h->occ_cache.emplace_back(fn, ctas);
@@ -455,16 +475,17 @@ struct Run {
         }
         const int k = h->k;
         const int n = static_cast<int>(h->pat.n);
-        if constexpr (Sh::S == 1) {  // batched tiles: shared-memory tiled restriction
+        if constexpr (Sh::S == 1) {  // batched tiles: bulk-copy pipelined restriction
             constexpr int TB = Sh::T;
             KSWITCH(k, {
-                auto fn = k_restrict_tiled<TB, KM>;
-                const int64_t need = (n + row_tile<KM>() - 1) / row_tile<KM>();
-                int64_t gx = std::min<int64_t>(need, resident_ctas(h, (const void*)fn, true));
+                auto fn = (std::getenv("P2G_TMA") ? k_restrict_mma<TB, KM> : k_restrict_reg<TB, KM>);
+                const size_t smem = std::getenv("P2G_TMA") ? MmaTile<TB, KM>::SMEM : 0;
+                const int64_t need = (n + 127) / 128;
+                int64_t gx = std::min<int64_t>(need, resident_ctas(h, (const void*)fn, true, smem));
                 gx = std::min<int64_t>(std::max<int64_t>(gx, 1), h->nb_cap);
                 gx = (gx + kCluster - 1) / kCluster * kCluster;
                 dim3 g((unsigned)gx, (unsigned)(h->Bp / TB));
-                fn<<<g, kBlock, 0, h->stream>>>(n, h->Bp, t, h->d_phi, k, h->d_active, h->d_part_c);
+                fn<<<g, kBlock, smem, h->stream>>>(n, h->Bp, t, h->d_phit, k, h->phi_ks, h->d_part_c);
                 *nb_out = g.x / kCluster;
             });
             count_launch(h, KC_RESTRICT);
@@ -498,14 +519,18 @@ struct Run {
     static int prolong(p2g_handle* h, double* s, bool assign) {
         const int k = h->k;
         const int n = static_cast<int>(h->pat.n + h->n_ghost);  // ghosts too (partitioned)
-        if constexpr (Sh::S == 1) {  // batched tiles: shared-memory tiled prolongation
+        if constexpr (Sh::S == 1) {  // batched tiles: bulk-copy pipelined prolongation
             constexpr int TB = Sh::T;
             KSWITCH(k, {
-                auto fn = assign ? k_prolong_tiled<TB, KM, true> : k_prolong_tiled<TB, KM, false>;
-                const int64_t need = (n + row_tile<KM>() - 1) / row_tile<KM>();
-                int64_t gx = std::min<int64_t>(need, resident_ctas(h, (const void*)fn, false));
+                const bool tma = std::getenv("P2G_TMA") != nullptr;
+                auto fn = tma ? (assign ? k_prolong_mma<TB, KM, true> : k_prolong_mma<TB, KM, false>)
+                              : (assign ? k_prolong_reg<TB, KM, true> : k_prolong_reg<TB, KM, false>);
+                const size_t smem = tma ? MmaTile<TB, KM>::SMEM : 0;
+                const int64_t need = (n + 31) / 32;
+                int64_t gx = std::min<int64_t>(need, resident_ctas(h, (const void*)fn, false, smem));
                 dim3 g((unsigned)std::max<int64_t>(gx, 1), (unsigned)(h->Bp / TB));
-                fn<<<g, kBlock, 0, h->stream>>>(n, h->Bp, s, h->d_phi, k, h->d_e, h->d_active);
+                fn<<<g, kBlock, smem, h->stream>>>(n, h->Bp, s, h->d_phit, k, h->phi_ks, h->d_e,
+                                                   h->d_active);
             });
             count_launch(h, KC_PROLONG);
             CU(cudaGetLastError());
@@ -777,7 +802,6 @@ int alloc_batch(p2g_handle* h) {
 }
 
 int choose_shape(p2g_handle* h, int B) {
-    const double avg = (double)h->pat.nnz / (double)h->pat.n;
     if (B == 1) {
         h->shape = SH_B1A;  // 4 rows x 8 slots per warp (more rows in flight than a warp per row)
         h->Bp = 1;
@@ -880,7 +904,7 @@ int assemble_impl(p2g_handle* h, const p2g_mesh* m, int32_t batch, const double*
 
 std::vector<uint64_t> graph_key_of(p2g_handle* h) {
     auto u = [](const void* p) { return (uint64_t)(uintptr_t)p; };
-    return {u(h->d_vals), u(h->d_phi), u(h->d_e), u(h->d_L), u(h->d_part_c), u(h->d_u), u(h->d_r),
+    return {u(h->d_vals), u(h->d_phi), u(h->d_phit), u(h->d_e), u(h->d_L), u(h->d_part_c), u(h->d_u), u(h->d_r),
             u(h->d_s), u(h->d_s2), u(h->d_p), u(h->d_Kp), u(h->d_t), u(h->d_hist), (uint64_t)h->Bp,
             (uint64_t)h->B, (uint64_t)h->k, (uint64_t)h->shape, (uint64_t)h->cfg.smoother,
             (uint64_t)h->cfg.pre_sweeps, (uint64_t)h->cfg.post_sweeps,
@@ -961,6 +985,7 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
     }
     if (!h->loop_exec || h->graph_key != graph_key_of(h)) TRY(build_loop_graph(h));
     const int64_t lc0 = h->launches_executed;
+    h->has_state = true;
     SolveParams prm{tol, (long long)max_iter, (long long)hist_cap};
     CU(cudaMemcpyAsync(h->d_prm, &prm, sizeof(prm), cudaMemcpyHostToDevice, h->stream));
 
@@ -1115,6 +1140,7 @@ int p2g_destroy(p2g_handle* h) {
     dfree(h->d_perm);
     dfree(h->d_vals);
     dfree(h->d_phi);
+    dfree(h->d_phit);
     for (double** p : {&h->d_u, &h->d_r, &h->d_s, &h->d_s2, &h->d_p, &h->d_Kp, &h->d_b, &h->d_t, &h->d_alpha,
                        &h->d_beta, &h->d_rsold, &h->d_fnorm, &h->d_rel, &h->d_e, &h->d_L, &h->d_Ac,
                        &h->d_hist, &h->d_part_dot, &h->d_part_rr, &h->d_part_ff, &h->d_part_rs,
@@ -1192,9 +1218,7 @@ int p2g_set_basis(p2g_handle* h, int32_t k, const double* phi) {
     std::vector<double> perm_phi((size_t)n * std::max(k, 1), 0.0);
     for (int64_t i = 0; i < n; ++i)
         for (int a = 0; a < k; ++a) perm_phi[i * k + a] = phi[h->pat.perm[i] * k + a];
-    TRY(ensure(h, h->d_phi, perm_phi.size()));
-    CU(cudaMemcpy(h->d_phi, perm_phi.data(), sizeof(double) * perm_phi.size(),
-                  cudaMemcpyHostToDevice));
+    TRY(upload_phi(h, perm_phi, n, k));
     if (h->Bp > 0) {
         TRY(ensure(h, h->d_e, (size_t)std::max(k, 1) * h->Bp));
         TRY(ensure(h, h->d_L, (size_t)std::max(k * k, 1) * h->Bp));
@@ -1240,6 +1264,7 @@ int p2g_setup(p2g_handle* h, const p2g_config* cfg, int32_t* status) {
         if (st[b] != P2G_OK) worst = st[b];
     }
     h->setup_done = true;
+    h->has_state = false;
     if (worst != P2G_OK) h->err = "p2g_setup: at least one instance failed (see status)";
     return worst;
 }
@@ -1392,6 +1417,8 @@ int p2g_profile_iteration(p2g_handle* h, int32_t reps, double* ms, double* bytes
     CU(cudaSetDevice(h->device));
     REQ(h->setup_done, P2G_ESTATE, "p2g_profile_iteration: p2g_setup not called");
     REQ(reps >= 1, P2G_EINVAL, "p2g_profile_iteration: reps >= 1");
+    // a zero Krylov state has p'Kp = 0: every instance would stop as a breakdown
+    REQ(h->has_state, P2G_ESTATE, "p2g_profile_iteration: run p2g_solve first (Krylov state)");
     std::vector<double> acc(P2G_NUM_KCLASS, 0.0);
     // every instance active for the whole replay: no convergence or max_iter
     // exit inside the profiled iterations (state is scratch)
@@ -2053,8 +2080,7 @@ int p2g_part_set_basis(p2g_part* P, int rank, int32_t k, const double* phi_own,
     for (int64_t j = 0; j < ng; ++j)
         for (int a = 0; a < k; ++a) phi[(n + j) * k + a] = phi_ghost[j * k + a];
     h->k = k;
-    if (ensure(h, h->d_phi, phi.size()) != P2G_OK) return P2G_ECUDA;
-    PCU(cudaMemcpy(h->d_phi, phi.data(), sizeof(double) * phi.size(), cudaMemcpyHostToDevice));
+    if (upload_phi(h, phi, n + ng, k) != P2G_OK) return P2G_ECUDA;
     if (h->Bp > 0) {
         if (ensure(h, h->d_e, (size_t)k * h->Bp) || ensure(h, h->d_L, (size_t)k * k * h->Bp) ||
             ensure(h, h->d_Ac, (size_t)k * k * h->Bp) ||
