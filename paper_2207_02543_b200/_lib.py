@@ -95,11 +95,12 @@ def lib():
     """Load libpod2g_b200.so (once).  Raises if it has not been built."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
+        path = os.environ.get("P2G_LIB_PATH", LIB_PATH)  # tuning experiments only
+        if not os.path.exists(path):
             raise RuntimeError(
                 f"{LIB_PATH} is missing: build it with `make -C {HERE}/csrc` "
                 "(there is no CPU fallback)")
-        L = C.CDLL(LIB_PATH)
+        L = C.CDLL(path)
         for name, res, args in SIGNATURES:
             fn = getattr(L, name)
             fn.restype = res

@@ -45,6 +45,11 @@ constexpr int kCluster = 8;
 // 32 registers so 8 CTAs x 8 warps (100% occupancy) stay resident (the
 // difference between 4.4 and 6.3 TB/s for the batched SpMV, tools/spmv_lab.cu).
 #define P2G_ROWK __launch_bounds__(kBlock, Sh::W == 1 ? 6 : P2G_MINB)
+#ifndef P2G_UNROLL
+#define P2G_UNROLL 4  // entries of a row in flight per warp (row loops)
+#endif
+#define P2G_PRAGMA_(x) _Pragma(#x)
+#define P2G_PRAGMA(x) P2G_PRAGMA_(x)
 #ifndef P2G_MINB
 #define P2G_MINB 4
 #endif
@@ -162,7 +167,7 @@ __device__ __forceinline__ void row_dot(const Mat& A, const double* X, int b0, i
     const unsigned Bp = (unsigned)A.Bp;
     const double* Xb = X + b0;
     const double* vb = A.vals + (size_t)k0 * Bp + b0;  // 64-bit row base, 32-bit in-row offsets
-#pragma unroll 4
+P2G_PRAGMA(unroll P2G_UNROLL)
     for (int k = k0 + s; k < k1; k += Sh::S) {
         const unsigned c = (unsigned)__ldg(A.ci + k);
         double a[Sh::V], x[Sh::V];
@@ -180,7 +185,7 @@ __device__ __forceinline__ void row_sub(const Mat& A, const double* X, int b0, i
     const unsigned Bp = (unsigned)A.Bp;
     const double* Xb = X + b0;
     const double* vb = A.vals + (size_t)k0 * Bp + b0;
-#pragma unroll 4
+P2G_PRAGMA(unroll P2G_UNROLL)
     for (int k = k0; k < k1; ++k) {
         const unsigned c = (unsigned)__ldg(A.ci + k);
         double a[Sh::V], x[Sh::V];
@@ -596,7 +601,7 @@ __global__ void P2G_CLUSTER P2G_ROWK k_kp_update(Mat A, const double* __restrict
             if (valid && any) {
                 const int kb = __ldg(A.rp + i), kd = __ldg(A.dpos + i);
                 const double* vb = A.vals + (size_t)kb * Bp + b0;
-#pragma unroll 4
+P2G_PRAGMA(unroll P2G_UNROLL)
                 for (int k = kb + G.s; k < kd; k += Sh::S) {
                     const unsigned col = (unsigned)__ldg(A.ci + k);
                     double a[Sh::V], x1[Sh::V], x0[Sh::V];

@@ -17,6 +17,7 @@
 
 #include "../../include/pod2g_gen.h"
 #include "p2g_mesh_desc.h"
+#include "p2g_pattern.h"
 
 struct p2g_mesh {
     int dim = 2;
@@ -486,10 +487,24 @@ int p2g_mesh_node_colors(const p2g_mesh* m, int32_t* colors) {
     if (!m || !colors) return P2G_GEN_EINVAL;
     const Grid G = grid_of(m);
     const int64_t nn = m->n / m->dim;
+    // parity classes, processed in the order p2g_set_pattern's colouring would
+    // pick (order_colours): class coupling = common neighbours of adjacent
+    // nodes, which depends on the parity difference only (Q4: edge 4,
+    // diagonal 2; hex8: face 16, edge 10, corner 6)
+    const int ncol = m->dim == 3 ? 8 : 4;
+    std::vector<double> W((size_t)ncol * ncol, 0.0);
+    for (int a = 0; a < ncol; ++a)
+        for (int b = 0; b < ncol; ++b) {
+            const int bits = __builtin_popcount(a ^ b);
+            W[(size_t)a * ncol + b] = bits == 0 ? 0.0
+                                      : m->dim == 3 ? (bits == 1 ? 16.0 : bits == 2 ? 10.0 : 6.0)
+                                                    : (bits == 1 ? 4.0 : 2.0);
+        }
+    const std::vector<int32_t> rank = p2g::order_colours(ncol, W);
     for (int64_t rn = 0; rn < nn; ++rn) {
         int64_t ix, iy, iz;
         G.coords(rn, ix, iy, iz);
-        colors[rn] = static_cast<int32_t>((ix & 1) + 2 * (iy & 1) + (m->dim == 3 ? 4 * (iz & 1) : 0));
+        colors[rn] = rank[(ix & 1) + 2 * (iy & 1) + (m->dim == 3 ? 4 * (iz & 1) : 0)];
     }
     return P2G_GEN_OK;
 }
