@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define P2G_ABI_VERSION 1
+#define P2G_ABI_VERSION 2
 
 typedef struct p2g_handle p2g_handle;
 
@@ -147,10 +147,32 @@ int p2g_setup(p2g_handle* h, const p2g_config* cfg, int32_t* status);
 int p2g_initial_guess(p2g_handle* h, const double* b, double* x0);
 
 enum {
-    P2G_X0_ZERO = 0,     /* u0 empty => zero (krylov.hpp:247)                  */
-    P2G_X0_GIVEN = 1,    /* x0 argument                                        */
-    P2G_X0_REDUCED = 2   /* x0 = reduced_solve(K, b, Phi), computed on device  */
+    P2G_X0_ZERO = 0,      /* u0 empty => zero (krylov.hpp:247)                  */
+    P2G_X0_GIVEN = 1,     /* x0 argument                                        */
+    P2G_X0_REDUCED = 2,   /* x0 = reduced_solve(K, b, Phi), computed on device  */
+    P2G_X0_SURROGATE = 3  /* x0 = predict(model, theta_b) (p2g_set_surrogate +
+                             p2g_set_theta), computed on device                 */
 };
+
+/* ---- surrogate warm start ---------------------------------------
+ * predict(model, theta) = Phi * denormalize(mlp(normalize(theta)))
+ * (surrogate.hpp:354-357), the x0 run_monte_carlo uses (bench.hpp:418-420).
+ * The model's linear decoder is the handle's basis (p2g_set_basis); the MLP:
+ *   nlayers >= 1 dense layers, widths[0..nlayers] (input p, hidden..., output
+ *   = the basis rank k), activation on hidden layers only (Mlp::forward,
+ *   surrogate.hpp:62-74): P2G_ACT_TANH / P2G_ACT_RELU;
+ *   weights = the row-major W_l (widths[l+1] x widths[l]) concatenated in
+ *   layer order, biases likewise -- the order of the reference's weights.bin;
+ *   in_mean/in_std [p], lat_mean/lat_std [k]: AffineNormalizer
+ *   (surrogate.hpp:144-157).  Widths up to 4096. */
+enum { P2G_ACT_TANH = 0, P2G_ACT_RELU = 1 };
+int p2g_set_surrogate(p2g_handle* h, int32_t nlayers, const int32_t* widths, int32_t activation,
+                      const double* weights, const double* biases, const double* in_mean,
+                      const double* in_std, const double* lat_mean, const double* lat_std);
+/* parameters theta [B][p] (host) of the instances, for P2G_X0_SURROGATE */
+int p2g_set_theta(p2g_handle* h, const double* theta);
+/* x [B][n] (host) = predict(model, theta_b) per instance (sets theta too) */
+int p2g_surrogate_predict(p2g_handle* h, const double* theta, double* x);
 
 /* pcg_solve per instance (krylov.hpp:243-297) with the POD-2G preconditioner.
  *   b        [B][n]   right-hand sides
@@ -194,6 +216,10 @@ int p2g_coarse_operator(p2g_handle* h, double* Ac);
  * ncolors+1 node-row offsets (cap entries at most). */
 int p2g_get_permutation(p2g_handle* h, int64_t* perm, int32_t* ncolors, int64_t* color_offsets,
                         int32_t cap);
+
+/* Host-only: fnv1a_hash (core/io.hpp:92-99) of a byte payload -- the checksum
+ * of the reference's artefacts (weights.bin, vector batches). */
+uint64_t p2g_fnv1a64(const void* bytes, int64_t count);
 
 /* Host-only (no device needed): the colouring p2g_set_pattern would use. */
 int p2g_analyze_pattern(int64_t n, const uint64_t* row_offsets, const uint64_t* col_indices,

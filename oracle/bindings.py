@@ -59,6 +59,24 @@ class _Csr(C.Structure):
     _fields_ = [("n", C.c_int64), ("rp", _I64), ("ci", _I64), ("v", _D)]
 
 
+def _surrogate_args(model, phi, theta):
+    """Flatten a surrogate model (any object with the reference's fields:
+    widths, activation 'tanh'/'relu', weights [W_l], biases [b_l], input_mean,
+    input_std, latent_mean, latent_std) for or_/ref_surrogate_predict."""
+    widths = np.ascontiguousarray(model.widths, dtype=np.int64)
+    W = np.ascontiguousarray(np.concatenate([np.asarray(w, dtype=np.float64).ravel() for w in model.weights]))
+    b = np.ascontiguousarray(np.concatenate([np.asarray(x, dtype=np.float64).ravel() for x in model.biases]))
+    norms = [np.ascontiguousarray(a, dtype=np.float64) for a in
+             (model.input_mean, model.input_std, model.latent_mean, model.latent_std)]
+    phi = _f64(phi)
+    theta = np.ascontiguousarray(np.atleast_2d(theta), dtype=np.float64)
+    act = 0 if model.activation == "tanh" else 1
+    keep = (widths, W, b, norms, phi, theta)
+    args = [len(widths) - 1, _i64(widths), act, _d(W), _d(b)] + [_d(a) for a in norms] + \
+        [phi.shape[0], _d(phi), theta.shape[0], _d(theta)]
+    return args, keep, (theta.shape[0], phi.shape[0])
+
+
 class Oracle:
     """The C restatement of krylov.hpp/pod.hpp/smoothers.hpp/csr.hpp."""
 
@@ -86,6 +104,8 @@ class Oracle:
         L.or_pcg_pod2g_batch.argtypes = [C.c_int64, _I64, _I64, C.c_int64, _D, C.c_int64, _D,
                                          C.c_int64, _D, _D, C.c_double, C.c_int64, C.c_int,
                                          C.c_double, _D, _I64, _I32, _I32, C.c_int]
+        L.or_surrogate_predict.argtypes = [C.c_int, _I64, C.c_int, _D, _D, _D, _D, _D, _D,
+                                           C.c_int64, _D, C.c_int64, _D, _D]
 
     @staticmethod
     def _csr(rp, ci, v):
@@ -134,6 +154,14 @@ class Oracle:
         u = np.empty(n)
         self.lib.or_lift(n, k, _d(phi), _d(z), _d(u))
         return u
+
+    def surrogate_predict(self, model, phi, theta):
+        """predict (surrogate.hpp:354-357) for each row of theta -> [B][n]."""
+        args, keep, (B, n) = _surrogate_args(model, phi, theta)
+        x = np.empty((B, n))
+        if self.lib.or_surrogate_predict(*args, _d(x)) != 0:
+            raise ValueError("or_surrogate_predict: bad model")
+        return x
 
     def dense_solve(self, A, b):
         A = _f64(A).copy()
@@ -235,11 +263,40 @@ class Reference:
         L.ref_its_case.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
                                    C.c_int64, _I64, _I64, _I64, _I64, _I64, _D, _D, _D,
                                    C.c_int64]
+        L.ref_surrogate_predict.argtypes = [C.c_int, _I64, C.c_int, _D, _D, _D, _D, _D, _D,
+                                            C.c_int64, _D, C.c_int64, _D, _D]
+        L.ref_save_surrogate.argtypes = [C.c_char_p, C.c_int, _I64, C.c_int, _D, _D, _D, _D,
+                                         _D, _D, C.c_int64, _D]
+        L.ref_load_predict.argtypes = [C.c_char_p, C.c_int64, _D, _D]
 
     def _check(self, st):
         if st != 0:
             msg = self.lib.ref_last_error().decode()
             raise (ValueError if st == 1 else RuntimeError)(msg)
+
+    def surrogate_predict(self, model, phi, theta):
+        """pod2g::predict (surrogate.hpp:354-357) for each row of theta."""
+        args, keep, (B, n) = _surrogate_args(model, phi, theta)
+        x = np.empty((B, n))
+        self._check(self.lib.ref_surrogate_predict(*args, _d(x)))
+        return x
+
+    def save_surrogate(self, directory, model, phi):
+        """pod2g::save_surrogate_model of `model` with basis `phi`."""
+        args, keep, _ = _surrogate_args(model, phi, np.zeros((1, len(model.input_mean))))
+        self._check(self.lib.ref_save_surrogate(str(directory).encode(), *args[:9],
+                                                args[9], args[10]))
+
+    def load_predict(self, directory, theta):
+        """pod2g::load_surrogate_model(directory) then predict per theta row."""
+        theta = np.ascontiguousarray(np.atleast_2d(theta), dtype=np.float64)
+        with open(os.path.join(directory, "basis.json")) as fh:
+            import json
+            n = int(json.load(fh)["dim"])
+        x = np.empty((theta.shape[0], n))
+        self._check(self.lib.ref_load_predict(str(directory).encode(), theta.shape[0], _d(theta),
+                                              _d(x)))
+        return x
 
     def spmv(self, rp, ci, v, x):
         rp, ci, v, x = _ix(rp), _ix(ci), _f64(v), _f64(x)

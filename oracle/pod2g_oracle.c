@@ -444,3 +444,44 @@ int or_pcg_pod2g_batch(int64_t n, const int64_t* rp, const int64_t* ci, int64_t 
         if (status[b] != OR_OK) worst = status[b];
     return worst;
 }
+
+/* surrogate.hpp:354-357 (see the header) */
+int or_surrogate_predict(int nlayers, const int64_t* widths, int act, const double* W,
+                         const double* bias, const double* in_mean, const double* in_std,
+                         const double* lat_mean, const double* lat_std, int64_t n,
+                         const double* phi, int64_t B, const double* theta, double* x) {
+    if (nlayers < 1) return OR_EINVAL;
+    int64_t wmax = 0;
+    for (int l = 0; l <= nlayers; ++l) wmax = widths[l] > wmax ? widths[l] : wmax;
+    const int64_t p = widths[0], k = widths[nlayers];
+    double* a = (double*)malloc(sizeof(double) * (size_t)wmax);
+    double* z = (double*)malloc(sizeof(double) * (size_t)wmax);
+    if (!a || !z) {
+        free(a);
+        free(z);
+        return OR_EINVAL;
+    }
+    for (int64_t b = 0; b < B; ++b) {
+        for (int64_t j = 0; j < p; ++j) a[j] = (theta[b * p + j] - in_mean[j]) / in_std[j];
+        const double* Wl = W;
+        const double* bl = bias;
+        for (int l = 0; l < nlayers; ++l) {
+            const int64_t fi = widths[l], fo = widths[l + 1];
+            for (int64_t i = 0; i < fo; ++i) {
+                double s = bl[i];
+                for (int64_t j = 0; j < fi; ++j) s += Wl[i * fi + j] * a[j];
+                z[i] = s;
+            }
+            if (l + 1 < nlayers)
+                for (int64_t i = 0; i < fo; ++i) z[i] = act == 0 ? tanh(z[i]) : fmax(z[i], 0.0);
+            for (int64_t i = 0; i < fo; ++i) a[i] = z[i];
+            Wl += fo * fi;
+            bl += fo;
+        }
+        for (int64_t i = 0; i < k; ++i) a[i] = a[i] * lat_std[i] + lat_mean[i];
+        or_lift(n, k, phi, a, x + b * n);
+    }
+    free(a);
+    free(z);
+    return OR_OK;
+}

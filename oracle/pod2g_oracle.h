@@ -109,6 +109,17 @@ int or_pcg_pod2g_batch(int64_t n, const int64_t* rp, const int64_t* ci, int64_t 
                        int smoother, double omega, double* u, int64_t* iters, int* converged,
                        int* status, int nthreads);
 
+/* surrogate.hpp:354-357 predict: x = Phi * denormalize(mlp(normalize(theta))).
+ * Mlp::forward surrogate.hpp:62-74 (z = b; z_i += W_ij a_j ascending j; hidden
+ * activation tanh (act 0) / relu (act 1), identity output); AffineNormalizer
+ * surrogate.hpp:144-157.  widths[0..nlayers]; W = the layers' row-major
+ * matrices (widths[l+1] x widths[l]) concatenated; bias likewise.  theta [B][p],
+ * x [B][n], phi [n][k] with k == widths[nlayers]. */
+int or_surrogate_predict(int nlayers, const int64_t* widths, int act, const double* W,
+                         const double* bias, const double* in_mean, const double* in_std,
+                         const double* lat_mean, const double* lat_std, int64_t n,
+                         const double* phi, int64_t B, const double* theta, double* x);
+
 #ifdef __cplusplus
 }
 #endif

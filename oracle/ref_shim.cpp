@@ -19,6 +19,7 @@
 #include "pod2g/pod.hpp"
 #include "pod2g/problems.hpp"
 #include "pod2g/smoothers.hpp"
+#include "pod2g/surrogate.hpp"
 
 using namespace pod2g;
 
@@ -337,6 +338,80 @@ int ref_its_case(int64_t res, int64_t n_snapshots, uint64_t offline_seed, uint64
         std::memcpy(f, sys.f.data(), sizeof(double) * sys.f.size());
         const int64_t cnt = static_cast<int64_t>(basis.phi_r.data.size());
         std::memcpy(phi, basis.phi_r.data.data(), sizeof(double) * std::min(cnt, phi_cap));
+    });
+}
+
+namespace {
+SurrogateModel make_model(int nlayers, const int64_t* widths, int act, const double* W,
+                          const double* bias, const double* in_mean, const double* in_std,
+                          const double* lat_mean, const double* lat_std, int64_t n,
+                          const double* phi) {
+    SurrogateModel m;
+    const index_t k = static_cast<index_t>(widths[nlayers]);
+    m.basis.rank = k;
+    m.basis.phi_r = DenseMatrix(static_cast<index_t>(n), k);
+    m.basis.phi_r.data.assign(phi, phi + n * k);
+    m.basis.eigenvalues.assign(k, 1.0);
+    m.mlp.widths.assign(widths, widths + nlayers + 1);
+    m.mlp.activation = act == 0 ? Activation::Tanh : Activation::Relu;
+    const double* w = W;
+    const double* bb = bias;
+    for (int l = 0; l < nlayers; ++l) {
+        const index_t fi = m.mlp.widths[l], fo = m.mlp.widths[l + 1];
+        DenseMatrix M(fo, fi);
+        M.data.assign(w, w + fo * fi);
+        m.mlp.weights.push_back(std::move(M));
+        m.mlp.biases.emplace_back(bb, bb + fo);
+        w += fo * fi;
+        bb += fo;
+    }
+    const index_t p = m.mlp.widths.front();
+    m.input_norm.mean.assign(in_mean, in_mean + p);
+    m.input_norm.std.assign(in_std, in_std + p);
+    m.latent_norm.mean.assign(lat_mean, lat_mean + k);
+    m.latent_norm.std.assign(lat_std, lat_std + k);
+    return m;
+}
+}  // namespace
+
+// save_surrogate_model (surrogate.hpp:361-386) of a model built from arrays
+int ref_save_surrogate(const char* dir, int nlayers, const int64_t* widths, int act,
+                       const double* W, const double* bias, const double* in_mean,
+                       const double* in_std, const double* lat_mean, const double* lat_std,
+                       int64_t n, const double* phi) {
+    return guarded([&] {
+        save_surrogate_model(dir, make_model(nlayers, widths, act, W, bias, in_mean, in_std,
+                                             lat_mean, lat_std, n, phi));
+    });
+}
+
+// load_surrogate_model (surrogate.hpp:388-432) + predict for each theta row
+int ref_load_predict(const char* dir, int64_t B, const double* theta, double* x) {
+    return guarded([&] {
+        const SurrogateModel m = load_surrogate_model(dir);
+        const index_t p = m.mlp.widths.front(), n = m.basis.dim();
+        for (int64_t b = 0; b < B; ++b) {
+            const Vector th(theta + b * p, theta + (b + 1) * p);
+            const Vector u = predict(m, th);
+            std::memcpy(x + b * n, u.data(), sizeof(double) * n);
+        }
+    });
+}
+
+// predict (surrogate.hpp:354-357) over a SurrogateModel built from arrays
+int ref_surrogate_predict(int nlayers, const int64_t* widths, int act, const double* W,
+                          const double* bias, const double* in_mean, const double* in_std,
+                          const double* lat_mean, const double* lat_std, int64_t n,
+                          const double* phi, int64_t B, const double* theta, double* x) {
+    return guarded([&] {
+        const SurrogateModel m = make_model(nlayers, widths, act, W, bias, in_mean, in_std,
+                                            lat_mean, lat_std, n, phi);
+        const index_t p = m.mlp.widths.front();
+        for (int64_t b = 0; b < B; ++b) {
+            const Vector th(theta + b * p, theta + (b + 1) * p);
+            const Vector u = predict(m, th);
+            std::memcpy(x + b * n, u.data(), sizeof(double) * n);
+        }
     });
 }
 

@@ -33,6 +33,10 @@ SIGNATURES = [
     ("p2g_set_basis", C.c_int, [H, C.c_int32, D]),
     ("p2g_setup", C.c_int, [H, C.c_void_p, I32]),
     ("p2g_initial_guess", C.c_int, [H, D, D]),
+    ("p2g_set_surrogate", C.c_int, [H, C.c_int32, I32, C.c_int32, D, D, D, D, D, D]),
+    ("p2g_set_theta", C.c_int, [H, D]),
+    ("p2g_fnv1a64", C.c_uint64, [C.c_char_p, C.c_int64]),
+    ("p2g_surrogate_predict", C.c_int, [H, D, D]),
     ("p2g_solve", C.c_int, [H, D, D, C.c_int32, C.c_double, C.c_int64, D, I64, I32, I32, D,
                             C.c_int64]),
     ("p2g_solve_device", C.c_int, [H, C.c_void_p, C.c_void_p, C.c_int32, C.c_double, C.c_int64,
@@ -121,5 +125,6 @@ OK, EINVAL, EBREAKDOWN, ENONFINITE, ESINGULAR, EZERODIAG, ECUDA, ENCCL, ESTATE =
 SMOOTHER_GS_MULTICOLOR, SMOOTHER_JACOBI = 0, 1
 RESIDUAL_FULL, RESIDUAL_UPPER = 0, 1
 KP_SPMV, KP_RECURRENCE = 0, 1
-X0_ZERO, X0_GIVEN, X0_REDUCED = 0, 1, 2
+X0_ZERO, X0_GIVEN, X0_REDUCED, X0_SURROGATE = 0, 1, 2, 3
+ACT_TANH, ACT_RELU = 0, 1
 NUM_KCLASS = 9

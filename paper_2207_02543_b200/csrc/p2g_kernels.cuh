@@ -1274,6 +1274,46 @@ __global__ void __launch_bounds__(kBlock, KMAX > 40 ? 2 : 4) k_prolong_reg(int n
     }
 }
 
+// Surrogate latent coordinates (surrogate.hpp:354-357 without the lift):
+// e[:, b] = denormalize(mlp(normalize(theta_b))), one CTA per instance.
+// Mlp::forward (surrogate.hpp:62-74): z = bias, z_i += W_ij a_j in ascending
+// j (separately rounded), activation on hidden layers only; AffineNormalizer
+// (surrogate.hpp:150-157).  norm = [in_mean p | in_std p | lat_mean k | lat_std k].
+__global__ void __launch_bounds__(kBlock) k_mlp_latent(int nlayers, const int* widths, int act,
+                                                       const double* __restrict__ W,
+                                                       const double* __restrict__ bias,
+                                                       const double* __restrict__ norm,
+                                                       const double* __restrict__ theta,
+                                                       int wmax, int Bp, double* e) {
+    extern __shared__ double mlp_sm[];
+    double* a = mlp_sm;
+    double* z = mlp_sm + wmax;
+    const int b = blockIdx.x;
+    const int p = widths[0], k = widths[nlayers];
+    for (int j = threadIdx.x; j < p; j += blockDim.x)
+        a[j] = __ddiv_rn(__dsub_rn(theta[(size_t)b * p + j], norm[j]), norm[p + j]);
+    __syncthreads();
+    size_t wo = 0, bo = 0;
+    for (int l = 0; l < nlayers; ++l) {
+        const int fi = widths[l], fo = widths[l + 1];
+        for (int i = threadIdx.x; i < fo; i += blockDim.x) {
+            const double* Wi = W + wo + (size_t)i * fi;
+            double s = bias[bo + i];
+            for (int j = 0; j < fi; ++j) s = __dadd_rn(s, __dmul_rn(Wi[j], a[j]));
+            if (l + 1 < nlayers) s = act == 0 ? tanh(s) : fmax(s, 0.0);
+            z[i] = s;
+        }
+        __syncthreads();
+        double* t = a;
+        a = z;
+        z = t;
+        wo += (size_t)fo * fi;
+        bo += fo;
+    }
+    for (int i = threadIdx.x; i < k; i += blockDim.x)
+        e[(size_t)i * Bp + b] = __dadd_rn(__dmul_rn(a[i], norm[2 * p + k + i]), norm[2 * p + i]);
+}
+
 // shape of the row-local kernels (restriction, prolongation): R = 32/W rows
 // per warp, one instance per lane unless k is small enough for two
 template <class Sh, int KMAX>

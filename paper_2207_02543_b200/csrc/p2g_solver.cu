@@ -78,6 +78,13 @@ struct p2g_handle {
     double* d_phit = nullptr;  // [rows][phi_ks], zero padded (tensor-core tiles, phi_stride)
     int phi_ks = 0;
 
+    // surrogate warm start (p2g_set_surrogate): MLP on the device
+    int sg_layers = 0, sg_act = 0, sg_wmax = 0;
+    std::vector<int> sg_widths;
+    int* d_sg_widths = nullptr;
+    double *d_sg_W = nullptr, *d_sg_b = nullptr, *d_sg_norm = nullptr, *d_theta = nullptr;
+    bool theta_set = false;
+
     // vectors [n][Bp]
     double *d_u = nullptr, *d_r = nullptr, *d_s = nullptr, *d_s2 = nullptr, *d_p = nullptr,
            *d_Kp = nullptr, *d_b = nullptr, *d_t = nullptr;
@@ -967,13 +974,32 @@ int build_loop_graph(p2g_handle* h) {
     return P2G_OK;
 }
 
+// u = predict(model, theta_b) per instance: MLP latent coordinates into the
+// coarse-coefficient buffer, then the prolongation in assign mode (lift)
+int surrogate_x0(p2g_handle* h, double* u) {
+    const size_t smem = sizeof(double) * 2 * (size_t)h->sg_wmax;
+    if (smem > 48 * 1024)
+        CU(cudaFuncSetAttribute(k_mlp_latent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+    k_mlp_latent<<<h->B, kBlock, smem, h->stream>>>(h->sg_layers, h->d_sg_widths, h->sg_act,
+                                                    h->d_sg_W, h->d_sg_b, h->d_sg_norm,
+                                                    h->d_theta, h->sg_wmax, h->Bp, h->d_e);
+    ++h->launches_executed;
+    CU(cudaGetLastError());
+    return dispatch(h, [&](auto R) -> int { return decltype(R)::prolong(h, u, true); });
+}
+
 int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const double* x0_host,
                const double* x0_dev, int32_t x0_mode, double tol, int64_t max_iter,
                double* x_host, double* x_dev, int64_t* iters, int32_t* converged, int32_t* status,
                double* hist, int64_t hist_cap) {
     REQ(h->setup_done, P2G_ESTATE, "p2g_solve: p2g_setup not called");
     REQ(b_host || b_dev, P2G_EINVAL, "p2g_solve: null right-hand side");
-    REQ(x0_mode >= 0 && x0_mode <= 2, P2G_EINVAL, "p2g_solve: bad x0_mode");
+    REQ(x0_mode >= 0 && x0_mode <= 3, P2G_EINVAL, "p2g_solve: bad x0_mode");
+    REQ(x0_mode != P2G_X0_SURROGATE || (h->sg_layers > 0 && h->theta_set),
+        P2G_ESTATE, "p2g_solve: surrogate x0 needs p2g_set_surrogate and p2g_set_theta");
+    REQ(x0_mode != P2G_X0_SURROGATE || h->sg_widths.back() == h->k, P2G_EINVAL,
+        "predict: surrogate output width differs from the basis rank");
     REQ(x0_mode != P2G_X0_GIVEN || x0_host || x0_dev, P2G_EINVAL, "p2g_solve: null x0");
     REQ(x0_mode != P2G_X0_REDUCED || h->k > 0, P2G_EINVAL,
         "p2g_solve: reduced initial guess needs a basis");
@@ -1003,6 +1029,8 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
             TRY(Rn::restrict_(h, RES_VECTOR, h->d_b, nullptr, &nbc));
             TRY(Rn::coarse(h, nbc));
             TRY(Rn::prolong(h, h->d_u, true));
+        } else if (x0_mode == P2G_X0_SURROGATE) {
+            TRY(surrogate_x0(h, h->d_u));
         } else {
             CU(cudaMemsetAsync(h->d_u, 0, (size_t)h->pat.n * h->Bp * sizeof(double), h->stream));
         }
@@ -1141,6 +1169,11 @@ int p2g_destroy(p2g_handle* h) {
     dfree(h->d_vals);
     dfree(h->d_phi);
     dfree(h->d_phit);
+    dfree(h->d_sg_widths);
+    dfree(h->d_sg_W);
+    dfree(h->d_sg_b);
+    dfree(h->d_sg_norm);
+    dfree(h->d_theta);
     for (double** p : {&h->d_u, &h->d_r, &h->d_s, &h->d_s2, &h->d_p, &h->d_Kp, &h->d_b, &h->d_t, &h->d_alpha,
                        &h->d_beta, &h->d_rsold, &h->d_fnorm, &h->d_rel, &h->d_e, &h->d_L, &h->d_Ac,
                        &h->d_hist, &h->d_part_dot, &h->d_part_rr, &h->d_part_ff, &h->d_part_rs,
@@ -1287,6 +1320,86 @@ int p2g_initial_guess(p2g_handle* h, const double* b, double* x0) {
         return P2G_OK;
     }));
     TRY(download_interleaved(h, h->d_u, x0, nullptr));
+    return P2G_OK;
+}
+
+uint64_t p2g_fnv1a64(const void* bytes, int64_t count) {
+    const unsigned char* c = static_cast<const unsigned char*>(bytes);
+    uint64_t hsh = 1469598103934665603ull;
+    for (int64_t i = 0; i < count; ++i) {
+        hsh ^= c[i];
+        hsh *= 1099511628211ull;
+    }
+    return hsh;
+}
+
+int p2g_set_surrogate(p2g_handle* h, int32_t nlayers, const int32_t* widths, int32_t activation,
+                      const double* weights, const double* biases, const double* in_mean,
+                      const double* in_std, const double* lat_mean, const double* lat_std) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    REQ(nlayers >= 1 && widths, P2G_EINVAL, "Mlp: at least input and output layers required");
+    REQ(weights && biases && in_mean && in_std && lat_mean && lat_std, P2G_EINVAL,
+        "p2g_set_surrogate: null argument");
+    REQ(activation == P2G_ACT_TANH || activation == P2G_ACT_RELU, P2G_EINVAL,
+        "p2g_set_surrogate: unknown activation");
+    size_t nw = 0, nb = 0;
+    int wmax = 0;
+    for (int l = 0; l <= nlayers; ++l) {
+        REQ(widths[l] >= 1 && widths[l] <= 4096, P2G_EINVAL, "p2g_set_surrogate: widths in [1, 4096]");
+        wmax = std::max(wmax, (int)widths[l]);
+        if (l < nlayers) {
+            nw += (size_t)widths[l] * widths[l + 1];
+            nb += widths[l + 1];
+        }
+    }
+    const int p = widths[0], k = widths[nlayers];
+    std::vector<double> norm;
+    norm.insert(norm.end(), in_mean, in_mean + p);
+    norm.insert(norm.end(), in_std, in_std + p);
+    norm.insert(norm.end(), lat_mean, lat_mean + k);
+    norm.insert(norm.end(), lat_std, lat_std + k);
+    TRY(ensure(h, h->d_sg_widths, (size_t)nlayers + 1));
+    TRY(ensure(h, h->d_sg_W, nw));
+    TRY(ensure(h, h->d_sg_b, nb));
+    TRY(ensure(h, h->d_sg_norm, norm.size()));
+    CU(cudaMemcpy(h->d_sg_widths, widths, sizeof(int) * (nlayers + 1), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_sg_W, weights, sizeof(double) * nw, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_sg_b, biases, sizeof(double) * nb, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_sg_norm, norm.data(), sizeof(double) * norm.size(), cudaMemcpyHostToDevice));
+    h->sg_layers = nlayers;
+    h->sg_act = activation;
+    h->sg_wmax = wmax;
+    h->sg_widths.assign(widths, widths + nlayers + 1);
+    h->theta_set = false;
+    return P2G_OK;
+}
+
+int p2g_set_theta(p2g_handle* h, const double* theta) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    REQ(h->sg_layers > 0, P2G_ESTATE, "p2g_set_theta: p2g_set_surrogate not called");
+    REQ(h->B > 0, P2G_ESTATE, "p2g_set_theta: values not set (batch size unknown)");
+    REQ(theta, P2G_EINVAL, "p2g_set_theta: null theta");
+    const size_t cnt = (size_t)h->B * h->sg_widths[0];
+    TRY(ensure(h, h->d_theta, cnt));
+    CU(cudaMemcpy(h->d_theta, theta, sizeof(double) * cnt, cudaMemcpyHostToDevice));
+    h->theta_set = true;
+    return P2G_OK;
+}
+
+int p2g_surrogate_predict(p2g_handle* h, const double* theta, double* x) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    REQ(x, P2G_EINVAL, "p2g_surrogate_predict: null output");
+    TRY(p2g_set_theta(h, theta));
+    REQ(h->k > 0 && h->sg_widths.back() == h->k, P2G_EINVAL,
+        "predict: surrogate output width differs from the basis rank");
+    REQ(h->d_e, P2G_ESTATE, "p2g_surrogate_predict: basis / values not set");
+    CU(cudaMemcpyAsync(h->d_active, h->d_all, sizeof(int) * h->Bp, cudaMemcpyDeviceToDevice,
+                       h->stream));
+    TRY(surrogate_x0(h, h->d_u));
+    TRY(download_interleaved(h, h->d_u, x, nullptr));
     return P2G_OK;
 }
 

@@ -180,6 +180,31 @@ class BatchSolver:
         self._check(self._L.p2g_initial_guess(self._h, _d(b), _d(x0)), "initial_guess")
         return x0
 
+    def set_surrogate(self, model):
+        """The surrogate's MLP and normalisers (surrogate.SurrogateModel); its
+        decoder is this handle's basis (set_basis)."""
+        widths = np.ascontiguousarray(model.widths, dtype=np.int32)
+        W, b = model.flat_parameters()
+        norms = [_f64(a) for a in (model.input_mean, model.input_std, model.latent_mean,
+                                   model.latent_std)]
+        act = L.ACT_TANH if model.activation == "tanh" else L.ACT_RELU
+        self._check(self._L.p2g_set_surrogate(self._h, len(widths) - 1,
+                                              widths.ctypes.data_as(L.I32), act, _d(W), _d(b),
+                                              *[_d(a) for a in norms]), "set_surrogate")
+        self._sg_p = int(widths[0])
+
+    def set_theta(self, theta):
+        """Instance parameters [B][p] for x0_mode=X0_SURROGATE."""
+        th = _f64(theta).reshape(self.B, self._sg_p)
+        self._check(self._L.p2g_set_theta(self._h, _d(th)), "set_theta")
+
+    def surrogate_predict(self, theta):
+        """predict(model, theta_b) per instance (surrogate.hpp:354-357) -> [B][n]."""
+        th = _f64(theta).reshape(self.B, self._sg_p)
+        x = np.empty((self.B, self.n))
+        self._check(self._L.p2g_surrogate_predict(self._h, _d(th), _d(x)), "surrogate_predict")
+        return x
+
     def solve(self, b, x0=None, tol=1e-8, max_iter=100000, x0_mode=None, hist_cap=None):
         """Batched pcg_solve.  Returns (x[B][n], iters[B], converged[B], status[B], hist)."""
         b = _f64(b).reshape(self.B, self.n)

@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_status_strings():
     lib = L.lib()
-    assert lib.p2g_abi_version() == 1
+    assert lib.p2g_abi_version() == 2
     assert lib.p2g_status_string(L.EBREAKDOWN).decode().startswith("PCG breakdown")
 
 
