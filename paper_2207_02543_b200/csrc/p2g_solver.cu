@@ -989,6 +989,14 @@ int surrogate_x0(p2g_handle* h, double* u) {
     return dispatch(h, [&](auto R) -> int { return decltype(R)::prolong(h, u, true); });
 }
 
+bool eager_loop() {
+    static const bool e = [] {
+        const char* v = std::getenv("P2G_EAGER_LOOP");
+        return v && v[0] == '1';
+    }();
+    return e;
+}
+
 int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const double* x0_host,
                const double* x0_dev, int32_t x0_mode, double tol, int64_t max_iter,
                double* x_host, double* x_dev, int64_t* iters, int32_t* converged, int32_t* status,
@@ -1052,7 +1060,25 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
     });
     if (st != P2G_OK) return st;
     CU(cudaEventRecord(h->ev[1], h->stream));
-    CU(cudaGraphLaunch(h->loop_exec, h->stream));
+    int64_t eager_iters = -1;
+    if (eager_loop()) {
+        // profiling aid (P2G_EAGER_LOOP=1): the same loop body launched eagerly so
+        // ncu lists every kernel (it does not descend into the conditional-WHILE
+        // graph body); the host polls the active flags every 16 iterations --
+        // surplus iterations are fully masked no-ops
+        std::vector<int> act(h->Bp);
+        for (eager_iters = 0;; ++eager_iters) {
+            if (eager_iters % 16 == 0) {
+                CU(cudaMemcpyAsync(act.data(), h->d_active, sizeof(int) * h->Bp,
+                                   cudaMemcpyDeviceToHost, h->stream));
+                CU(cudaStreamSynchronize(h->stream));
+                if (std::none_of(act.begin(), act.end(), [](int a) { return a != 0; })) break;
+            }
+            TRY(dispatch(h, [&](auto R) -> int { return decltype(R)::iteration(h, false); }));
+        }
+    } else {
+        CU(cudaGraphLaunch(h->loop_exec, h->stream));
+    }
     CU(cudaEventRecord(h->ev[2], h->stream));
     {
         const dim3 g((unsigned)std::min<int64_t>((h->pat.n + 255) / 256, 1024), h->B);
@@ -1090,7 +1116,7 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
     h->last_ms[1] = ms_loop;
     int64_t maxit = 0;
     for (int b = 0; b < h->B; ++b) maxit = std::max<int64_t>(maxit, it[b]);
-    h->launches_executed += 1 /*set_cond*/ + maxit * h->launches_per_iter;
+    if (eager_iters < 0) h->launches_executed += 1 /*set_cond*/ + maxit * h->launches_per_iter;
     h->launches_last_solve = h->launches_executed - lc0;
     if (worst != P2G_OK) h->err = "p2g_solve: at least one instance failed (see status)";
     return worst;

@@ -20,9 +20,9 @@ CLASSES = [
     ("spmv_dot", r"^(void )?k_(spmv|kp_update)\b"),
     ("update_presmooth", r"^(void )?k_(update_pre|update_rows|jacobi)\b"),
     ("gs_forward", r"^(void )?k_gs_forward\b"),
-    ("residual_restrict", r"^(void )?k_(residual|restrict_vec|restrict_tiled)\b"),
+    ("residual_restrict", r"^(void )?k_(residual|restrict_vec|restrict_tiled|restrict_reg|restrict_mma)\b"),
     ("coarse_solve", r"^(void )?k_coarse\b"),
-    ("prolong", r"^(void )?k_prolong(_tiled)?\b"),
+    ("prolong", r"^(void )?k_prolong(_tiled|_reg|_mma)?\b"),
     ("gs_backward", r"^(void )?k_gs_backward\b"),
     ("scalar_reduce", r"^(void )?k_(alpha|finalize|set_cond|reduce_rows|sum_parts)\b"),
     ("p_update", r"^(void )?k_pupdate\b"),
@@ -36,8 +36,27 @@ def kclass(name):
     return "other"
 
 
+def load_any(path):
+    """an .ncu-rep (through ncu -i) or its `--page raw --csv` export (.csv[.gz])"""
+    if path.endswith(".csv.gz") or path.endswith(".csv"):
+        import gzip
+        import io
+        import subprocess
+        import ncu_summary as NS
+        opener = gzip.open if path.endswith(".gz") else open
+        with opener(path, "rt") as fh:
+            text = fh.read()
+        real = subprocess.run
+        NS.subprocess.run = lambda *a, **k: type("R", (), {"stdout": text})()
+        try:
+            return NS.load(path)
+        finally:
+            NS.subprocess.run = real
+    return load(path)
+
+
 def full(path, out):
-    rep = load(path)
+    rep = load_any(path)
     last = max(i for i, d in enumerate(rep) if re.search(r"^(void )?k_alpha\b", d["kernel"]))
     it = rep[last:]
     agg = {}
@@ -73,7 +92,8 @@ def full(path, out):
 
 def launches(path, out):
     rows = []
-    with open(path) as fh:
+    import gzip
+    with (gzip.open(path, "rt") if path.endswith(".gz") else open(path)) as fh:
         lines = [ln for ln in fh if not ln.startswith("==")]
     rd = list(csv.reader(lines))
     hdr = rd[0]
@@ -84,7 +104,7 @@ def launches(path, out):
             continue
         v = float(r[vi].replace(",", ""))
         u = r[ui]
-        us = v / 1e3 if u == "nsecond" else (v * 1e3 if u == "msecond" else v)
+        us = v / 1e3 if u in ("nsecond", "ns") else (v * 1e3 if u in ("msecond", "ms") else v)
         rows.append((r[ki], us))
     agg = {}
     for k, us in rows:
