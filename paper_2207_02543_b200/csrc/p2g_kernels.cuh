@@ -204,22 +204,33 @@ P2G_PRAGMA(unroll P2G_UNROLL)
 // goes to s: in place (xlo == xhi == s) for the reference sweeps, or out of
 // place for the backward sweep of the Kp recurrence (xlo = s' the
 // prolongated vector, xhi = s = the new sweep, D9).
+// fo / so (optional) receive f_i and the new s_i on the lanes that store
+// them, so a caller's epilogue (the r.s partial) needs no reload.
 template <class Sh>
 __device__ __forceinline__ void gs_row(const Mat& A, const double* f, const double* xlo,
                                        const double* xhi, double* s, int i, int b0, int lane_s,
-                                       bool upper, const bool (&m)[Sh::V], bool any) {
+                                       bool upper, const bool (&m)[Sh::V], bool any,
+                                       double* fo = nullptr, double* so = nullptr) {
     double out[Sh::V];
     if constexpr (Sh::S == 1) {
         if (any) {
             const int kb = __ldg(A.rp + i), kd = __ldg(A.dpos + i), ke = __ldg(A.rp + i + 1);
             double acc[Sh::V], d[Sh::V];
             ldv<Sh::V>(acc, f + (size_t)i * A.Bp + b0);
+            if (fo) {
+#pragma unroll
+                for (int v = 0; v < Sh::V; ++v) fo[v] = acc[v];
+            }
             row_sub<Sh>(A, xlo, b0, kb, kd, acc);
             if (upper) row_sub<Sh>(A, xhi, b0, kd + 1, ke, acc);
             ldv<Sh::V>(d, A.vals + (size_t)kd * A.Bp + b0);
 #pragma unroll
             for (int v = 0; v < Sh::V; ++v) out[v] = __ddiv_rn(acc[v], d[v]);
             stv<Sh::V>(s + (size_t)i * A.Bp + b0, out, m);
+            if (so) {
+#pragma unroll
+                for (int v = 0; v < Sh::V; ++v) so[v] = out[v];
+            }
         }
     } else {
         double acc[Sh::V];
@@ -241,6 +252,13 @@ __device__ __forceinline__ void gs_row(const Mat& A, const double* f, const doub
 #pragma unroll
             for (int v = 0; v < Sh::V; ++v) out[v] = __ddiv_rn(__dsub_rn(fi[v], acc[v]), d[v]);
             stv<Sh::V>(s + (size_t)i * A.Bp + b0, out, m);
+            if (fo && so) {
+#pragma unroll
+                for (int v = 0; v < Sh::V; ++v) {
+                    fo[v] = fi[v];
+                    so[v] = out[v];
+                }
+            }
         }
         __syncwarp();  // the next dof of this node reads s_i
     }
@@ -550,15 +568,16 @@ __global__ void P2G_CLUSTER P2G_ROWK k_gs_backward(Mat A, const double* __restri
         const bool valid = node < ne;
         for (int c = A.bs - 1; c >= 0; --c) {
             const int i = valid ? node * A.bs + c : 0;
-            gs_row<Sh>(A, f, xlo, s, s, i, b0, G.s, true, m, any && valid);
             if constexpr (LAST) {
+                // r.s partial from the row's own f_i and new s_i (no reload)
+                double fi[Sh::V], si[Sh::V];
+                gs_row<Sh>(A, f, xlo, s, s, i, b0, G.s, true, m, any && valid, fi, si);
                 if (valid && any && G.s == 0) {
-                    double fi[Sh::V], si[Sh::V];
-                    ldv<Sh::V>(fi, f + (size_t)i * A.Bp + b0);
-                    ldv<Sh::V>(si, s + (size_t)i * A.Bp + b0);
 #pragma unroll
                     for (int v = 0; v < Sh::V; ++v) rs[v] = __dadd_rn(rs[v], __dmul_rn(fi[v], si[v]));
                 }
+            } else {
+                gs_row<Sh>(A, f, xlo, s, s, i, b0, G.s, true, m, any && valid);
             }
         }
     }
