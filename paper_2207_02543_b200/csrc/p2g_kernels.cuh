@@ -12,7 +12,7 @@
 //
 // Warp tiling (Shape<R,S,W,V>): a warp covers R rows (nodes) x S slot lanes
 // per row x W instance lanes, each instance lane owning V instances.
-//   B == 1  : R=4,S=8,W=1  (2D rows, ~18 nnz)   or R=1,S=32,W=1 (3D rows, ~81 nnz)
+//   B == 1  : R=4,S=8,W=1  (4 rows x 8 slot lanes per warp, 2D and 3D rows)
 //   B <= 8  : R=1,S=4,W=8
 //   B <= 32 : R=1,S=1,W=32
 //   B  > 32 : R=1,S=1,W=32,V=2 (double2 per lane, 64 instances per tile)
