@@ -189,6 +189,16 @@ int p2g_solve(p2g_handle* h, const double* b, const double* x0, int32_t x0_mode,
               int64_t max_iter, double* x, int64_t* iters, int32_t* converged, int32_t* status,
               double* hist, int64_t hist_cap);
 
+/* pod2g_solve (pod.hpp:224-256): the standalone POD two-grid iteration
+ * u <- cycle(f, u) -- forward GS pre- AND post-smoothing (adjoint_post =
+ * false, pod.hpp:196-207; cfg.pre_sweeps / post_sweeps = r1 / r2), coarse
+ * correction with A_c from p2g_setup -- until the relative TRUE residual
+ * ||f - K u|| / ||f|| <= tol or max_cycles.  Arguments and outputs as
+ * p2g_solve (cycles = SolveReport::cycles); needs the GS smoother. */
+int p2g_pod2g_solve(p2g_handle* h, const double* b, const double* x0, int32_t x0_mode,
+                    double tol, int64_t max_cycles, double* x, int64_t* cycles,
+                    int32_t* converged, int32_t* status, double* hist, int64_t hist_cap);
+
 /* Same with b / x0 / x in DEVICE memory ([B][n]); iters/converged/status/hist
  * stay host pointers. */
 int p2g_solve_device(p2g_handle* h, const double* d_b, const double* d_x0, int32_t x0_mode,

@@ -106,6 +106,9 @@ class Oracle:
                                          C.c_double, _D, _I64, _I32, _I32, C.c_int]
         L.or_surrogate_predict.argtypes = [C.c_int, _I64, C.c_int, _D, _D, _D, _D, _D, _D,
                                            C.c_int64, _D, C.c_int64, _D, _D]
+        L.or_pod2g_solve.argtypes = [C.POINTER(_Csr), _D, C.c_int64, _D, _D, C.c_double,
+                                     C.c_int64, C.c_int64, C.c_int64, _D, _I64, _I32, _D,
+                                     C.c_int64, _I64]
 
     @staticmethod
     def _csr(rp, ci, v):
@@ -212,6 +215,23 @@ class Oracle:
                                    _d(hist), cap, C.byref(hl))
         return SolveResult(u, it.value, bool(conv.value), hist[: min(hl.value, cap)].copy(), st)
 
+    def pod2g_solve(self, rp, ci, v, f, phi, u0=None, delta=1e-8, max_cycles=100000, r1=1, r2=1,
+                    hist_cap=None):
+        """pod2g_solve (pod.hpp:224-256)."""
+        A, keep = self._csr(rp, ci, v)
+        f, phi_a = _f64(f), _f64(phi)
+        u0a = None if u0 is None else _f64(u0)
+        u = np.empty(A.n)
+        it = C.c_int64()
+        conv = C.c_int()
+        cap = int(hist_cap if hist_cap is not None else min(max_cycles, 200000) + 1)
+        hist = np.empty(cap)
+        hl = C.c_int64()
+        st = self.lib.or_pod2g_solve(C.byref(A), _d(f), phi_a.shape[1], _d(phi_a), _d(u0a), delta,
+                                     max_cycles, r1, r2, _d(u), C.byref(it), C.byref(conv),
+                                     _d(hist), cap, C.byref(hl))
+        return SolveResult(u, it.value, bool(conv.value), hist[: min(hl.value, cap)].copy(), st)
+
     def pcg_pod2g_batch(self, rp, ci, values, f, phi, u0=None, delta=1e-8, max_iter=100000,
                         smoother=SMOOTHER_GS, omega=2.0 / 3.0, nthreads=1):
         rp, ci = _ix(rp), _ix(ci)
@@ -268,6 +288,9 @@ class Reference:
         L.ref_save_surrogate.argtypes = [C.c_char_p, C.c_int, _I64, C.c_int, _D, _D, _D, _D,
                                          _D, _D, C.c_int64, _D]
         L.ref_load_predict.argtypes = [C.c_char_p, C.c_int64, _D, _D]
+        L.ref_pod2g_solve.argtypes = [C.c_int64, _I64, _I64, _D, _D, C.c_int64, _D, _D,
+                                      C.c_double, C.c_int64, _D, _I64, _I32, _D, C.c_int64,
+                                      _I64, _D]
 
     def _check(self, st):
         if st != 0:
@@ -355,6 +378,27 @@ class Reference:
                                              phi.shape[1], _d(phi), smoother, omega, _d(r),
                                              _d(s)))
         return s
+
+    def pod2g_solve(self, rp, ci, v, f, phi, u0=None, delta=1e-8, max_cycles=100000,
+                    hist_cap=None):
+        """pod2g::pod2g_solve (pod.hpp:224-256), r1 = r2 = 1."""
+        rp, ci, v, f, phi = _ix(rp), _ix(ci), _f64(v), _f64(f), _f64(phi)
+        n = len(rp) - 1
+        u0a = None if u0 is None else _f64(u0)
+        u = np.empty(n)
+        it = C.c_int64()
+        conv = C.c_int()
+        cap = int(hist_cap if hist_cap is not None else min(max_cycles, 200000) + 1)
+        hist = np.empty(cap)
+        hl = C.c_int64()
+        wall = C.c_double()
+        st = self.lib.ref_pod2g_solve(n, _i64(rp), _i64(ci), _d(v), _d(f), phi.shape[1], _d(phi),
+                                      _d(u0a), delta, max_cycles, _d(u), C.byref(it),
+                                      C.byref(conv), _d(hist), cap, C.byref(hl), C.byref(wall))
+        if st != 0:
+            return SolveResult(u, 0, False, np.empty(0), st)
+        return SolveResult(u, it.value, bool(conv.value), hist[: min(hl.value, cap)].copy(), 0,
+                           wall.value)
 
     def pcg_pod2g(self, rp, ci, v, f, phi, u0=None, delta=1e-8, max_iter=100000,
                   smoother=SMOOTHER_GS, omega=2.0 / 3.0, hist_cap=None):

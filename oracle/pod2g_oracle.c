@@ -485,3 +485,62 @@ int or_surrogate_predict(int nlayers, const int64_t* widths, int act, const doub
     free(z);
     return OR_OK;
 }
+
+/* pod.hpp:224-256 (see the header) */
+int or_pod2g_solve(const or_csr* K, const double* f, int64_t k, const double* phi,
+                   const double* u0, double delta, int64_t max_cycles, int64_t r1, int64_t r2,
+                   double* u, int64_t* cycles, int* converged, double* hist, int64_t hist_cap,
+                   int64_t* hist_len) {
+    const int64_t n = K->n;
+    double* lu = (double*)malloc(sizeof(double) * (size_t)(k * k > 0 ? k * k : 1));
+    int64_t* perm = (int64_t*)malloc(sizeof(int64_t) * (size_t)(k > 0 ? k : 1));
+    double* r = (double*)malloc(sizeof(double) * (size_t)(n ? n : 1));
+    double* c = (double*)malloc(sizeof(double) * (size_t)(k > 0 ? k : 1));
+    double* e = (double*)malloc(sizeof(double) * (size_t)(k > 0 ? k : 1));
+    double* corr = (double*)malloc(sizeof(double) * (size_t)(n ? n : 1));
+    or_pod2g P;
+    int st = or_pod2g_setup(&P, K, k, phi, r1, r2, OR_SMOOTHER_GS, 0.0, lu, perm);
+    int64_t hl = 0, it = 0;
+    for (int64_t i = 0; i < n; ++i) u[i] = u0 ? u0[i] : 0.0;
+    if (st == OR_OK) {
+        const double fnorm = sqrt(or_dot(n, f, f));
+        or_residual(K, f, u, r);
+        double rel = relative_residual(sqrt(or_dot(n, r, r)), fnorm);
+        if (hist && hl < hist_cap) hist[hl] = rel;
+        ++hl;
+        while (rel > delta && it < max_cycles) {
+            if ((st = or_gs_forward(K, f, u, r1)) != OR_OK) break; /* cycle(f, u) */
+            if (k > 0) {
+                or_residual(K, f, u, r);
+                or_project(n, k, phi, r, c);
+                or_lu_solve(k, lu, perm, c, e);
+                or_lift(n, k, phi, e, corr);
+                for (int64_t i = 0; i < n; ++i) u[i] += 1.0 * corr[i];
+            }
+            if ((st = or_gs_forward(K, f, u, r2)) != OR_OK) break;
+            or_residual(K, f, u, r);
+            rel = relative_residual(sqrt(or_dot(n, r, r)), fnorm);
+            if (hist && hl < hist_cap) hist[hl] = rel;
+            ++hl;
+            ++it;
+        }
+        *converged = rel <= delta;
+        if (st == OR_OK)
+            for (int64_t i = 0; i < n; ++i)
+                if (!isfinite(u[i])) {
+                    st = OR_ENONFINITE;
+                    break;
+                }
+    } else {
+        *converged = 0;
+    }
+    *cycles = it;
+    if (hist_len) *hist_len = hl;
+    free(lu);
+    free(perm);
+    free(r);
+    free(c);
+    free(e);
+    free(corr);
+    return st;
+}

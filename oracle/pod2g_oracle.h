@@ -109,6 +109,15 @@ int or_pcg_pod2g_batch(int64_t n, const int64_t* rp, const int64_t* ci, int64_t 
                        int smoother, double omega, double* u, int64_t* iters, int* converged,
                        int* status, int nthreads);
 
+/* pod.hpp:224-256 pod2g_solve: the standalone two-grid iteration
+ * u <- cycle(f, u) with FORWARD post-smoothing (pod.hpp:196-207,
+ * adjoint_post = false), stopped on the true relative residual; GS smoother,
+ * r1 / r2 sweeps.  hist as or_pcg_pod2g; *cycles = iterations done. */
+int or_pod2g_solve(const or_csr* K, const double* f, int64_t k, const double* phi,
+                   const double* u0, double delta, int64_t max_cycles, int64_t r1, int64_t r2,
+                   double* u, int64_t* cycles, int* converged, double* hist, int64_t hist_cap,
+                   int64_t* hist_len);
+
 /* surrogate.hpp:354-357 predict: x = Phi * denormalize(mlp(normalize(theta))).
  * Mlp::forward surrogate.hpp:62-74 (z = b; z_i += W_ij a_j ascending j; hidden
  * activation tanh (act 0) / relu (act 1), identity output); AffineNormalizer

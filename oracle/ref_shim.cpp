@@ -222,6 +222,23 @@ int ref_pcg_pod2g(int64_t n, const int64_t* rp, const int64_t* ci, const double*
     });
 }
 
+// pod2g_solve (pod.hpp:224-256): the standalone two-grid iteration
+int ref_pod2g_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                    const double* f, int64_t k, const double* phi, const double* u0,
+                    double delta, int64_t max_cycles, double* u, int64_t* cycles,
+                    int* converged, double* hist, int64_t hist_cap, int64_t* hist_len,
+                    double* wall_s) {
+    return guarded([&] {
+        const CsrMatrix K = make_csr(n, rp, ci, v);
+        const PodBasis basis = make_basis(n, k, phi);
+        Vector uu0 = u0 ? Vector(u0, u0 + n) : Vector{};
+        const SolveOut o{u, cycles, converged, hist, hist_cap, hist_len, wall_s};
+        write_out(pod2g_solve(K, Vector(f, f + n), basis, uu0, delta,
+                              static_cast<index_t>(max_cycles)),
+                  o);
+    });
+}
+
 int ref_cg_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
                  const double* f, double delta, int64_t max_iter, double* u, int64_t* iters,
                  int* converged, double* hist, int64_t hist_cap, int64_t* hist_len) {

@@ -1450,6 +1450,47 @@ __global__ void __launch_bounds__(256) k_finalize(int Bp, int nrs, const double*
     }
 }
 
+// End of one pod2g_solve cycle (pod.hpp:243-250): rel from the TRUE residual
+// partials, history, cycle count, convergence; graph condition as k_finalize.
+__global__ void __launch_bounds__(256) k_cycle_finalize(int Bp, int nrr, const double* part_rr,
+                                                        const double* fnorm, double* rel,
+                                                        int* iters, int* active, double* hist,
+                                                        const SolveParams* prm,
+                                                        unsigned* flag_ticket,
+                                                        cudaGraphConditionalHandle cond,
+                                                        int set_cond) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.x * (blockDim.x >> 5) + warp;
+    int any = 0;
+    if (b < Bp && active[b]) {
+        const double rr = warp_col_sum(part_rr, nrr, Bp, b);
+        if (lane == 0) {
+            const int it = iters[b] + 1;
+            iters[b] = it;
+            const double fn = fnorm[b];
+            const double rn = sqrt(rr);
+            const double rl = fn > 0.0 ? rn / fn : rn;  // krylov.hpp:235-237
+            rel[b] = rl;
+            if (it < prm->hist_cap) hist[(size_t)b * prm->hist_cap + it] = rl;
+            if (!(rl > prm->tol) || it >= prm->max_iter)
+                active[b] = 0;
+            else
+                any = 1;
+        }
+    }
+    any = __syncthreads_or(any);
+    if (set_cond && threadIdx.x == 0) {
+        if (any) atomicOr(&flag_ticket[0], 1u);
+        __threadfence();
+        const unsigned t = atomicAdd(&flag_ticket[1], 1u);
+        if (t == gridDim.x - 1) {
+            const unsigned f = atomicExch(&flag_ticket[0], 0u);
+            atomicExch(&flag_ticket[1], 0u);
+            cudaGraphSetConditional(cond, f ? 1u : 0u);
+        }
+    }
+}
+
 // Initial residual bookkeeping (krylov.hpp:252-260): fnorm, rel0, hist[0],
 // the loop-entry test.  Instances with a setup error are not entered.
 __global__ void k_init_rel(int Bp, int B, int nrows, const double* part_rr, const double* part_ff,

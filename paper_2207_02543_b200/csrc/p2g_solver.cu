@@ -117,6 +117,11 @@ struct p2g_handle {
     cudaGraphExec_t loop_exec = nullptr;
     std::vector<uint64_t> graph_key;  // what the captured graph baked in
     cudaGraphConditionalHandle cond = 0;
+    // the pod2g_solve cycle loop (p2g_pod2g_solve): its own graph and condition
+    cudaGraphExec_t cyc_exec = nullptr;
+    std::vector<uint64_t> cyc_key;
+    cudaGraphConditionalHandle cyc_cond = 0;
+    int64_t launches_per_cycle = 0;
 
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     std::vector<std::pair<const void*, int>> occ_cache;
@@ -660,6 +665,32 @@ struct Run {
         return P2G_OK;
     }
 
+    // One pod2g_solve cycle (pod.hpp:243-250: op.cycle(f, u); r = f - K u):
+    // r1 forward sweeps on u (full rows), t = f - K u, coarse correction,
+    // r2 FORWARD sweeps (adjoint_post = false, pod.hpp:196-207), the true
+    // residual with its norm partials, bookkeeping.
+    static int cycle(p2g_handle* h, bool in_graph) {
+        const int C = h->pat.ncolors;
+        for (int sw = 0; sw < h->cfg.pre_sweeps; ++sw)
+            for (int c = 0; c < C; ++c) TRY(gs_forward(h, h->d_b, h->d_u, c, false));
+        if (h->k > 0) {
+            int nbc = 0;
+            TRY(restrict_(h, RES_FULL, h->d_b, h->d_u, &nbc));
+            TRY(coarse(h, nbc));
+            TRY(prolong(h, h->d_u, false));
+        }
+        for (int sw = 0; sw < h->cfg.post_sweeps; ++sw)
+            for (int c = 0; c < C; ++c) TRY(gs_forward(h, h->d_b, h->d_u, c, false));
+        int nb = 0;
+        TRY(residual(h, h->d_b, h->d_u, h->d_r, &nb));
+        k_cycle_finalize<<<(h->Bp + 7) / 8, 256, 0, h->stream>>>(
+            h->Bp, nb, h->d_part_rr, h->d_fnorm, h->d_rel, h->d_iters, h->d_active, h->d_hist,
+            h->d_prm, h->d_flag_ticket, h->cyc_cond, in_graph ? 1 : 0);
+        count_launch(h, KC_REDUCE);
+        CU(cudaGetLastError());
+        return P2G_OK;
+    }
+
     // ---- setup: A_c = Phi^T K Phi per instance, then Cholesky
     static int coarse_setup(p2g_handle* h, bool factor = true) {
         const int k = h->k;
@@ -781,6 +812,8 @@ int download_interleaved(p2g_handle* h, const double* src, double* dst_host, dou
 void destroy_graph(p2g_handle* h) {
     if (h->loop_exec) cudaGraphExecDestroy(h->loop_exec);
     h->loop_exec = nullptr;
+    if (h->cyc_exec) cudaGraphExecDestroy(h->cyc_exec);
+    h->cyc_exec = nullptr;
 }
 
 int alloc_batch(p2g_handle* h) {
@@ -919,13 +952,16 @@ std::vector<uint64_t> graph_key_of(p2g_handle* h) {
             (uint64_t)h->cfg.kp_update};
 }
 
-int build_loop_graph(p2g_handle* h) {
-    destroy_graph(h);
+// cycle == false: the PCG iteration loop; true: the pod2g_solve cycle loop
+int build_loop_graph(p2g_handle* h, bool cycle = false) {
+    cudaGraphExec_t& exec = cycle ? h->cyc_exec : h->loop_exec;
+    if (exec) cudaGraphExecDestroy(exec);
+    exec = nullptr;
     cudaGraph_t outer = nullptr;
     CU(cudaGraphCreate(&outer, 0));
     cudaGraphConditionalHandle cond;
     CU(cudaGraphConditionalHandleCreate(&cond, outer, 0, 0));
-    h->cond = cond;
+    (cycle ? h->cyc_cond : h->cond) = cond;
     // upstream kernel: condition := any instance active
     cudaKernelNodeParams kp = {};
     int Bp = h->Bp;
@@ -950,7 +986,9 @@ int build_loop_graph(p2g_handle* h) {
                                      cudaStreamCaptureModeRelaxed));
     const int64_t before = h->launch_counter;
     h->capturing = true;
-    int st = dispatch(h, [&](auto R) -> int { return decltype(R)::iteration(h, true); });
+    int st = dispatch(h, [&](auto R) -> int {
+        return cycle ? decltype(R)::cycle(h, true) : decltype(R)::iteration(h, true);
+    });
     h->capturing = false;
     cudaGraph_t captured = nullptr;
     cudaError_t ce = cudaStreamEndCapture(h->stream, &captured);
@@ -963,9 +1001,9 @@ int build_loop_graph(p2g_handle* h) {
         h->err = std::string("graph capture: ") + cudaGetErrorString(ce);
         return P2G_ECUDA;
     }
-    h->launches_per_iter = h->launch_counter - before;
-    h->graph_key = graph_key_of(h);
-    cudaError_t ie = cudaGraphInstantiate(&h->loop_exec, outer, 0);
+    (cycle ? h->launches_per_cycle : h->launches_per_iter) = h->launch_counter - before;
+    (cycle ? h->cyc_key : h->graph_key) = graph_key_of(h);
+    cudaError_t ie = cudaGraphInstantiate(&exec, outer, 0);
     cudaGraphDestroy(outer);
     if (ie != cudaSuccess) {
         h->err = std::string("graph instantiate: ") + cudaGetErrorString(ie);
@@ -997,11 +1035,15 @@ bool eager_loop() {
     return e;
 }
 
+// cycle == false: pcg_solve (krylov.hpp:243-297) with the POD-2G preconditioner;
+// cycle == true: pod2g_solve (pod.hpp:224-256), iters = cycles
 int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const double* x0_host,
                const double* x0_dev, int32_t x0_mode, double tol, int64_t max_iter,
                double* x_host, double* x_dev, int64_t* iters, int32_t* converged, int32_t* status,
-               double* hist, int64_t hist_cap) {
+               double* hist, int64_t hist_cap, bool cycle = false) {
     REQ(h->setup_done, P2G_ESTATE, "p2g_solve: p2g_setup not called");
+    REQ(!cycle || h->cfg.smoother == P2G_SMOOTHER_GS_MULTICOLOR, P2G_EINVAL,
+        "p2g_pod2g_solve: the standalone iteration uses the Gauss-Seidel smoother (pod.hpp:227)");
     REQ(b_host || b_dev, P2G_EINVAL, "p2g_solve: null right-hand side");
     REQ(x0_mode >= 0 && x0_mode <= 3, P2G_EINVAL, "p2g_solve: bad x0_mode");
     REQ(x0_mode != P2G_X0_SURROGATE || (h->sg_layers > 0 && h->theta_set),
@@ -1017,9 +1059,13 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
         TRY(dalloc(h, h->d_hist, (size_t)cap_dev * h->Bp));
         h->hist_cap_alloc = cap_dev;
     }
-    if (!h->loop_exec || h->graph_key != graph_key_of(h)) TRY(build_loop_graph(h));
+    if (cycle) {
+        if (!h->cyc_exec || h->cyc_key != graph_key_of(h)) TRY(build_loop_graph(h, true));
+    } else if (!h->loop_exec || h->graph_key != graph_key_of(h)) {
+        TRY(build_loop_graph(h));
+    }
     const int64_t lc0 = h->launches_executed;
-    h->has_state = true;
+    h->has_state = !cycle;
     SolveParams prm{tol, (long long)max_iter, (long long)hist_cap};
     CU(cudaMemcpyAsync(h->d_prm, &prm, sizeof(prm), cudaMemcpyHostToDevice, h->stream));
 
@@ -1048,6 +1094,7 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
             h->Bp, h->B, nb, h->d_part_rr, h->d_part_ff, h->d_fnorm, h->d_rel, h->d_iters,
             h->d_active, h->d_status, h->d_setup_status, h->d_hist, h->d_prm);
         count_launch(h, KC_REDUCE);
+        if (cycle) return P2G_OK;  // pod2g_solve: u, r, rel and the history entry 0 only
         // s = T r0 ; rs_old = r.s ; p = s   (krylov.hpp:262-266)
         int rs_rows = 0;
         TRY(Rn::precond(h, false, h->d_r, nullptr, &rs_rows));
@@ -1074,10 +1121,12 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
                 CU(cudaStreamSynchronize(h->stream));
                 if (std::none_of(act.begin(), act.end(), [](int a) { return a != 0; })) break;
             }
-            TRY(dispatch(h, [&](auto R) -> int { return decltype(R)::iteration(h, false); }));
+            TRY(dispatch(h, [&](auto R) -> int {
+                return cycle ? decltype(R)::cycle(h, false) : decltype(R)::iteration(h, false);
+            }));
         }
     } else {
-        CU(cudaGraphLaunch(h->loop_exec, h->stream));
+        CU(cudaGraphLaunch(cycle ? h->cyc_exec : h->loop_exec, h->stream));
     }
     CU(cudaEventRecord(h->ev[2], h->stream));
     {
@@ -1116,7 +1165,9 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
     h->last_ms[1] = ms_loop;
     int64_t maxit = 0;
     for (int b = 0; b < h->B; ++b) maxit = std::max<int64_t>(maxit, it[b]);
-    if (eager_iters < 0) h->launches_executed += 1 /*set_cond*/ + maxit * h->launches_per_iter;
+    if (eager_iters < 0)
+        h->launches_executed +=
+            1 /*set_cond*/ + maxit * (cycle ? h->launches_per_cycle : h->launches_per_iter);
     h->launches_last_solve = h->launches_executed - lc0;
     if (worst != P2G_OK) h->err = "p2g_solve: at least one instance failed (see status)";
     return worst;
@@ -1436,6 +1487,15 @@ int p2g_solve(p2g_handle* h, const double* b, const double* x0, int32_t x0_mode,
     CU(cudaSetDevice(h->device));
     return solve_impl(h, b, nullptr, x0, nullptr, x0_mode, tol, max_iter, x, nullptr, iters,
                       converged, status, hist, hist_cap);
+}
+
+int p2g_pod2g_solve(p2g_handle* h, const double* b, const double* x0, int32_t x0_mode,
+                    double tol, int64_t max_cycles, double* x, int64_t* cycles,
+                    int32_t* converged, int32_t* status, double* hist, int64_t hist_cap) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    return solve_impl(h, b, nullptr, x0, nullptr, x0_mode, tol, max_cycles, x, nullptr, cycles,
+                      converged, status, hist, hist_cap, true);
 }
 
 int p2g_solve_device(p2g_handle* h, const double* d_b, const double* d_x0, int32_t x0_mode,

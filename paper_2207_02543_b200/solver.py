@@ -205,7 +205,8 @@ class BatchSolver:
         self._check(self._L.p2g_surrogate_predict(self._h, _d(th), _d(x)), "surrogate_predict")
         return x
 
-    def solve(self, b, x0=None, tol=1e-8, max_iter=100000, x0_mode=None, hist_cap=None):
+    def solve(self, b, x0=None, tol=1e-8, max_iter=100000, x0_mode=None, hist_cap=None,
+              _entry="p2g_solve"):
         """Batched pcg_solve.  Returns (x[B][n], iters[B], converged[B], status[B], hist)."""
         b = _f64(b).reshape(self.B, self.n)
         if x0_mode is None:
@@ -217,12 +218,18 @@ class BatchSolver:
         conv = np.zeros(self.B, dtype=np.int32)
         status = np.zeros(self.B, dtype=np.int32)
         hist = np.empty((self.B, max(cap, 1)))
-        st = self._L.p2g_solve(self._h, _d(b), _d(x0a), x0_mode, tol, max_iter, _d(x),
-                               it.ctypes.data_as(L.I64), conv.ctypes.data_as(L.I32),
-                               status.ctypes.data_as(L.I32), _d(hist) if cap > 0 else None, cap)
+        st = getattr(self._L, _entry)(self._h, _d(b), _d(x0a), x0_mode, tol, max_iter, _d(x),
+                                      it.ctypes.data_as(L.I64), conv.ctypes.data_as(L.I32),
+                                      status.ctypes.data_as(L.I32), _d(hist) if cap > 0 else None,
+                                      cap)
         if st in (L.EINVAL, L.ECUDA, L.ESTATE):
             self._check(st, "solve")
         return x, it, conv.astype(bool), status, hist[:, :cap]
+
+    def pod2g_solve(self, b, x0=None, tol=1e-8, max_cycles=100000, x0_mode=None, hist_cap=None):
+        """Batched pod2g_solve (pod.hpp:224-256), the standalone two-grid
+        iteration.  Returns (x, cycles, converged, status, hist)."""
+        return self.solve(b, x0, tol, max_cycles, x0_mode, hist_cap, _entry="p2g_pod2g_solve")
 
     def solve_device(self, b_ptr, x_ptr, x0_ptr=None, x0_mode=L.X0_ZERO, tol=1e-8,
                      max_iter=100000, hist_cap=0):

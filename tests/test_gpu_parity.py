@@ -293,3 +293,29 @@ def test_device_assembly_is_bit_identical(gpu, dims, B):
         assert np.array_equal(a.spmv(e), b.spmv(e))
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("B", [1, 40])
+def test_pod2g_solve_matches_oracle(gpu, B):
+    """pod2g_solve (pod.hpp:224-256): the standalone two-grid iteration with
+    forward pre- and post-smoothing, on the GPU vs the oracle on P K P^T."""
+    m, rp, ci, f, V, phi = small_problem(B=B, k=10)
+    s = make_solver(m, rp, ci, V, phi)
+    perm, prp, pci, pV, pf, pphi = perm_system(s, rp, ci, V, f, phi)
+    F = np.broadcast_to(f, (B, m.n)).copy()
+    tol = 1e-8
+    x, cyc, conv, status, hist = s.pod2g_solve(F, None, tol, 6000, x0_mode=L.X0_REDUCED)
+    assert np.all(conv) and np.all(status == 0)
+    for b in (0, B - 1):
+        x0_ref, _, _ = ORC.reduced_solve(prp, pci, pV[b], pf, pphi)
+        ref = ORC.pod2g_solve(prp, pci, pV[b], pf, pphi, x0_ref, tol, 6000)
+        assert ref.converged and abs(int(cyc[b]) - ref.iters) <= 1, (int(cyc[b]), ref.iters)
+        mm = min(int(cyc[b]), ref.iters) + 1
+        # the TRUE residual f - K u near 1e-8 is cancellation-dominated: after
+        # ~2000 cycles the rounding-level differences (D4, D10) show up at
+        # ~1e-13 absolute, so the history bar gets an absolute floor of 1e-4 tol
+        np.testing.assert_allclose(hist[b, :mm], ref.history[:mm], rtol=HIST_RTOL, atol=1e-4 * tol)
+        ref_m = ORC.pod2g_solve(prp, pci, pV[b], pf, pphi, x0_ref, 0.0, int(cyc[b]))
+        err = np.linalg.norm(x[b][perm] - ref_m.u) / np.linalg.norm(ref_m.u)
+        assert err <= X_RTOL, err
+    s.close()

@@ -233,3 +233,18 @@ def test_reference_jacobi_two_thirds_breaks_down_on_its():
     ref = R.pcg_pod2g(rp, ci, v, f, phi, None, 1e-8, 2000, smoother=SMOOTHER_JACOBI,
                       omega=2.0 / 3.0)
     assert res.status == 2 and ref.status != 0
+
+
+@needs_ref
+def test_pod2g_solve_restatement_equals_reference():
+    """pod.hpp:224-256 standalone two-grid iteration: the oracle's restatement is
+    bit-identical to the compiled reference (cycles, history, solution)."""
+    REF = Reference()
+    g = golden("q4c1.npz")
+    rp, ci, v, f, phi, x0 = g["rp"], g["ci"], g["v"], g["f"], g["phi"], g["x0"]
+    for u0, tol in ((x0, 1e-8), (None, 1e-6)):
+        a = ORC.pod2g_solve(rp, ci, v, f, phi, u0, tol, 3000)
+        b = REF.pod2g_solve(rp, ci, v, f, phi, u0, tol, 3000)
+        assert a.status == 0 and b.status == 0 and a.converged and b.converged
+        assert a.iters == b.iters
+        assert np.array_equal(a.history, b.history) and np.array_equal(a.u, b.u)
