@@ -227,6 +227,18 @@ int p2g_coarse_operator(p2g_handle* h, double* Ac);
 int p2g_get_permutation(p2g_handle* h, int64_t* perm, int32_t* ncolors, int64_t* color_offsets,
                         int32_t cap);
 
+/* compute_pod's fp64 contractions on the FP64 tensor cores (pod.hpp:81-87 and
+ * :120-129), handle-free:
+ *   p2g_gram:    G [N][N] (host) = U U^T, the snapshot Gram matrix, U [N][d]
+ *                row-major (host, or device with U_on_device = 1);
+ *   p2g_combine: Phi [d][r] = U^T W, W [N][r] (host, r <= 64) -- Phi = U Psi
+ *                Lambda^{-1/2} with W = Psi Lambda^{-1/2}; Phi is host memory, or
+ *                device memory when U_on_device = 1.
+ * Deterministic (fixed-order partial sums). */
+int p2g_gram(int32_t device, int64_t N, int64_t d, const double* U, int32_t U_on_device, double* G);
+int p2g_combine(int32_t device, int64_t N, int64_t d, const double* U, int32_t U_on_device,
+                int64_t r, const double* W, double* Phi);
+
 /* Host-only: fnv1a_hash (core/io.hpp:92-99) of a byte payload -- the checksum
  * of the reference's artefacts (weights.bin, vector batches). */
 uint64_t p2g_fnv1a64(const void* bytes, int64_t count);

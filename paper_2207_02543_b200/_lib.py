@@ -38,6 +38,9 @@ SIGNATURES = [
     ("p2g_set_surrogate", C.c_int, [H, C.c_int32, I32, C.c_int32, D, D, D, D, D, D]),
     ("p2g_set_theta", C.c_int, [H, D]),
     ("p2g_fnv1a64", C.c_uint64, [C.c_char_p, C.c_int64]),
+    ("p2g_gram", C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_void_p, C.c_int32, D]),
+    ("p2g_combine", C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_void_p, C.c_int32, C.c_int64,
+                              D, C.c_void_p]),
     ("p2g_surrogate_predict", C.c_int, [H, D, D]),
     ("p2g_solve", C.c_int, [H, D, D, C.c_int32, C.c_double, C.c_int64, D, I64, I32, I32, D,
                             C.c_int64]),

@@ -107,7 +107,7 @@ def _orthonormal(parts_own, parts_ghost, comm):
 
 
 def run(cfg_name="c5", world=1, hosted=None, nccl_uid=None, n_snapshots=48, snap_batch=8,
-        k=None, snap_tol=None, log=print):
+        k=None, snap_tol=None, log=print, device=0):
     cfg = PR.CONFIGS[cfg_name]
     k = cfg.k if k is None else k
     snap_tol = PR.SNAP_TOL if snap_tol is None else snap_tol
@@ -119,7 +119,7 @@ def run(cfg_name="c5", world=1, hosted=None, nccl_uid=None, n_snapshots=48, snap
     colors = mesh.node_colors()
     bounds = row_bounds(n, world, bs)
     f = mesh.rhs()
-    P = PartitionedSolver(world, 0, rank=hosted[0] if nccl_uid is not None else None,
+    P = PartitionedSolver(world, device, rank=hosted[0] if nccl_uid is not None else None,
                           nccl_uid=nccl_uid)
     ghosts, own_rows = {}, {}
     for r in hosted:
@@ -156,13 +156,16 @@ def run(cfg_name="c5", world=1, hosted=None, nccl_uid=None, n_snapshots=48, snap
     U = {r: np.concatenate(snaps[r], axis=0) for r in hosted}
     U_gh = comm.rows(U, bounds, ghosts)
     # compute_pod (pod.hpp:73-148) with RankTarget{k}, distributed Gram
-    G = comm.sum({r: U[r] @ U[r].T for r in hosted})
+    # the Gram partials and Phi's rows on the FP64 tensor cores
+    G = comm.sum({r: PR.gram_device(U[r], device) for r in hosted})
     G = 0.5 * (G + G.T)
     w, V = np.linalg.eigh(G)
     order = np.argsort(-w, kind="stable")
     w, V = w[order][:k], V[:, order][:, :k]
-    phi_own = {r: np.ascontiguousarray((U[r].T @ V) / np.sqrt(w)) for r in hosted}
-    phi_gh = {r: np.ascontiguousarray((U_gh[r].T @ V) / np.sqrt(w)) for r in hosted}
+    Wk = np.ascontiguousarray(V / np.sqrt(w))
+    phi_own = {r: PR.combine_device(U[r], Wk, device) for r in hosted}
+    phi_gh = {r: (PR.combine_device(U_gh[r], Wk, device) if U_gh[r].shape[1]
+                  else np.zeros((0, k))) for r in hosted}
     defect = np.max(np.abs(comm.sum({r: phi_own[r].T @ phi_own[r] for r in hosted}) - np.eye(k)))
     if defect > 1e-8:
         phi_own, phi_gh = _orthonormal(phi_own, phi_gh, comm)

@@ -1333,6 +1333,105 @@ __global__ void __launch_bounds__(kBlock) k_mlp_latent(int nlayers, const int* w
         e[(size_t)i * Bp + b] = __dadd_rn(__dmul_rn(a[i], norm[2 * p + k + i]), norm[2 * p + i]);
 }
 
+// ---------------------------------------------------------------------------
+// compute_pod's contractions (pod.hpp:81-87 Gram, :120-129 Phi = U Psi
+// Lambda^{-1/2}) on the FP64 tensor cores.
+// Gram G = U U^T, U [N][d] row-major: CTA (x = column chunk, y = macro tile
+// (I, J) of 64 x 64 entries, I <= J) stages its two 64-row panels of 32
+// columns in shared memory (row stride 36: the fragment pattern row = lane/4,
+// col = lane%4 hits each bank twice); warp w accumulates row block w of I
+// against the 8 column blocks of J.  Partials [chunk][tile][64][64], reduced
+// in fixed order by k_gram_reduce.
+constexpr int kGramMT = 64, kGramCW = 32, kGramS = kGramCW + 4;
+
+__global__ void __launch_bounds__(kBlock) k_gram(int N, int64_t d, const double* __restrict__ U,
+                                                 const int* __restrict__ tiles, double* part) {
+    __shared__ double P[2][kGramMT * kGramS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, tg = lane & 3;
+    const int I = tiles[2 * blockIdx.y], J = tiles[2 * blockIdx.y + 1];
+    double c[8][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[j][0] = c[j][1] = 0.0;
+    for (int64_t c0 = (int64_t)blockIdx.x * kGramCW; c0 < d; c0 += (int64_t)gridDim.x * kGramCW) {
+        for (int q = threadIdx.x; q < 2 * kGramMT * kGramCW; q += kBlock) {
+            const int pnl = q / (kGramMT * kGramCW), rem = q % (kGramMT * kGramCW);
+            const int row = rem / kGramCW, col = rem % kGramCW;
+            const int a = (pnl ? J : I) * kGramMT + row;
+            const int64_t cc = c0 + col;
+            P[pnl][row * kGramS + col] = (a < N && cc < d) ? __ldg(U + (size_t)a * d + cc) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ks = 0; ks < kGramCW / 4; ++ks) {
+            const double af = P[0][(8 * warp + g) * kGramS + 4 * ks + tg];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                dmma(c[j][0], c[j][1], af, P[1][(8 * j + g) * kGramS + 4 * ks + tg]);
+        }
+        __syncthreads();
+    }
+    double* out = part + ((size_t)blockIdx.x * gridDim.y + blockIdx.y) * kGramMT * kGramMT;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        out[(8 * warp + g) * kGramMT + 8 * j + 2 * tg] = c[j][0];
+        out[(8 * warp + g) * kGramMT + 8 * j + 2 * tg + 1] = c[j][1];
+    }
+}
+
+// G[a][b] (a, b < N) = fixed-order sum over the chunk partials; symmetric fill
+__global__ void k_gram_reduce(int N, int nchunks, int ntiles, const int* __restrict__ tiles,
+                              const double* __restrict__ part, double* G) {
+    const int t = blockIdx.y, I = tiles[2 * t], J = tiles[2 * t + 1];
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < kGramMT * kGramMT;
+         q += gridDim.x * blockDim.x) {
+        const int a = I * kGramMT + q / kGramMT, b = J * kGramMT + q % kGramMT;
+        if (a >= N || b >= N || (I == J && a > b)) continue;
+        double s = 0.0;
+        for (int ch = 0; ch < nchunks; ++ch) s += part[((size_t)ch * ntiles + t) * kGramMT * kGramMT + q];
+        G[(size_t)a * N + b] = s;
+        G[(size_t)b * N + a] = s;
+    }
+}
+
+// Phi[d][r] = U^T W (U [N][d], W [N][r], r <= 64): warp = 8 consecutive rows
+// of Phi x all column blocks; A fragment U[a0 + lane%4][i0 + lane/4] (each U
+// element read once), B fragments W from L1; k-steps over the N snapshots.
+__global__ void __launch_bounds__(kBlock) k_combine(int N, int64_t d, const double* __restrict__ U,
+                                                    int r, const double* __restrict__ W,
+                                                    double* __restrict__ Phi) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, tg = lane & 3;
+    const int nb = (r + 7) / 8;
+    for (int64_t i0 = ((int64_t)blockIdx.x * kWarps + warp) * 8; i0 < d;
+         i0 += (int64_t)gridDim.x * kWarps * 8) {
+        double c[8][2];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) c[j][0] = c[j][1] = 0.0;
+        const int64_t i = i0 + g;
+        for (int a0 = 0; a0 < N; a0 += 4) {
+            const int a = a0 + tg;
+            const double af = (a < N && i < d) ? __ldg(U + (size_t)a * d + i) : 0.0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j < nb) {
+                    const int col = 8 * j + g;
+                    const double bf = (a < N && col < r) ? __ldg(W + (size_t)a * r + col) : 0.0;
+                    dmma(c[j][0], c[j][1], af, bf);
+                }
+        }
+        if (i < d) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j < nb) {
+                    const int col = 8 * j + 2 * tg;
+                    if (col < r) Phi[(size_t)i * r + col] = c[j][0];
+                    if (col + 1 < r) Phi[(size_t)i * r + col + 1] = c[j][1];
+                }
+        }
+    }
+}
+
 // shape of the row-local kernels (restriction, prolongation): R = 32/W rows
 // per warp, one instance per lane unless k is small enough for two
 template <class Sh, int KMAX>

@@ -1175,6 +1175,24 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
 
 }  // namespace
 
+namespace {
+struct DevScratch {  // handle-free entry points: own stream and buffers
+    cudaStream_t st = nullptr;
+    std::vector<void*> bufs;
+    ~DevScratch() {
+        for (void* p : bufs) cudaFree(p);
+        if (st) cudaStreamDestroy(st);
+    }
+    template <class T>
+    T* alloc(size_t count) {
+        void* p = nullptr;
+        if (cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)) != cudaSuccess) return nullptr;
+        bufs.push_back(p);
+        return static_cast<T*>(p);
+    }
+};
+}  // namespace
+
 // ============================================================================ C-ABI
 extern "C" {
 
@@ -1398,6 +1416,73 @@ int p2g_initial_guess(p2g_handle* h, const double* b, double* x0) {
     }));
     TRY(download_interleaved(h, h->d_u, x0, nullptr));
     return P2G_OK;
+}
+
+// ---- compute_pod's contractions on the device -------------------
+
+int p2g_gram(int32_t device, int64_t N, int64_t d, const double* U, int32_t U_on_device, double* G) {
+    if (N < 1 || d < 1 || !U || !G) return P2G_EINVAL;
+    if (cudaSetDevice(device) != cudaSuccess) return P2G_ECUDA;
+    DevScratch S;
+    if (cudaStreamCreateWithFlags(&S.st, cudaStreamNonBlocking) != cudaSuccess) return P2G_ECUDA;
+    const double* dU = U;
+    if (!U_on_device) {
+        double* t = S.alloc<double>((size_t)N * d);
+        if (!t || cudaMemcpyAsync(t, U, sizeof(double) * N * d, cudaMemcpyHostToDevice, S.st))
+            return P2G_ECUDA;
+        dU = t;
+    }
+    const int NM = (int)((N + kGramMT - 1) / kGramMT);
+    std::vector<int> tiles;
+    for (int I = 0; I < NM; ++I)
+        for (int J = I; J < NM; ++J) tiles.push_back(I), tiles.push_back(J);
+    const int ntiles = (int)tiles.size() / 2;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int64_t chunks = (d + kGramCW - 1) / kGramCW;
+    const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)4 * sms / ntiles));
+    int* dT = S.alloc<int>(tiles.size());
+    double* part = S.alloc<double>((size_t)gx * ntiles * kGramMT * kGramMT);
+    double* dG = S.alloc<double>((size_t)N * N);
+    if (!dT || !part || !dG) return P2G_ECUDA;
+    if (cudaMemcpyAsync(dT, tiles.data(), sizeof(int) * tiles.size(), cudaMemcpyHostToDevice, S.st))
+        return P2G_ECUDA;
+    k_gram<<<dim3(gx, ntiles), kBlock, 0, S.st>>>((int)N, d, dU, dT, part);
+    k_gram_reduce<<<dim3(16, ntiles), 256, 0, S.st>>>((int)N, gx, ntiles, dT, part, dG);
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(G, dG, sizeof(double) * N * N, cudaMemcpyDeviceToHost, S.st) ||
+        cudaStreamSynchronize(S.st))
+        return P2G_ECUDA;
+    return P2G_OK;
+}
+
+int p2g_combine(int32_t device, int64_t N, int64_t d, const double* U, int32_t U_on_device,
+                int64_t r, const double* W, double* Phi) {
+    if (N < 1 || d < 1 || r < 1 || r > 64 || !U || !W || !Phi) return P2G_EINVAL;
+    if (cudaSetDevice(device) != cudaSuccess) return P2G_ECUDA;
+    DevScratch S;
+    if (cudaStreamCreateWithFlags(&S.st, cudaStreamNonBlocking) != cudaSuccess) return P2G_ECUDA;
+    const double* dU = U;
+    if (!U_on_device) {
+        double* t = S.alloc<double>((size_t)N * d);
+        if (!t || cudaMemcpyAsync(t, U, sizeof(double) * N * d, cudaMemcpyHostToDevice, S.st))
+            return P2G_ECUDA;
+        dU = t;
+    }
+    double* dW = S.alloc<double>((size_t)N * r);
+    double* dP = U_on_device ? Phi : S.alloc<double>((size_t)d * r);
+    if (!dW || !dP || cudaMemcpyAsync(dW, W, sizeof(double) * N * r, cudaMemcpyHostToDevice, S.st))
+        return P2G_ECUDA;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int64_t need = (d + 8 * kWarps - 1) / (8 * kWarps);
+    const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)8 * sms));
+    k_combine<<<gx, kBlock, 0, S.st>>>((int)N, d, dU, (int)r, dW, dP);
+    if (cudaGetLastError() != cudaSuccess) return P2G_ECUDA;
+    if (!U_on_device &&
+        cudaMemcpyAsync(Phi, dP, sizeof(double) * d * r, cudaMemcpyDeviceToHost, S.st))
+        return P2G_ECUDA;
+    return cudaStreamSynchronize(S.st) == cudaSuccess ? P2G_OK : P2G_ECUDA;
 }
 
 uint64_t p2g_fnv1a64(const void* bytes, int64_t count) {

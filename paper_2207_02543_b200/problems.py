@@ -197,18 +197,44 @@ def normal_draws(seed: int, count: int):
     return out
 
 
-def compute_pod(snapshots: np.ndarray, rank: int):
+def gram_device(U, device=0):
+    """G = U U^T on the FP64 tensor cores (p2g_gram, pod.hpp:81-87)."""
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    N, d = U.shape
+    G = np.empty((N, N))
+    st = L.lib().p2g_gram(device, N, d, U.ctypes.data, 0, G.ctypes.data_as(L.D))
+    if st != L.OK:
+        raise RuntimeError(f"p2g_gram failed: status {st}")
+    return G
+
+
+def combine_device(U, W, device=0):
+    """Phi = U^T W on the FP64 tensor cores (p2g_combine, pod.hpp:120-129)."""
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    W = np.ascontiguousarray(W, dtype=np.float64)
+    N, d = U.shape
+    r = W.shape[1]
+    Phi = np.empty((d, r))
+    st = L.lib().p2g_combine(device, N, d, U.ctypes.data, 0, r, W.ctypes.data_as(L.D),
+                             Phi.ctypes.data)
+    if st != L.OK:
+        raise RuntimeError(f"p2g_combine failed: status {st}")
+    return Phi
+
+
+def compute_pod(snapshots: np.ndarray, rank: int, device=None):
     """pod.hpp:73-148 with RankTarget{rank}: Gram U^T U, eigenpairs, cutoff
     1e-12 lambda_max, Phi = U Psi Lambda^{-1/2}, MGS if the orthonormality
     defect exceeds 1e-8.  snapshots: [N][d].  Returns (phi [d][r], eigenvalues,
-    energy_fraction)."""
+    energy_fraction).  device: run the two contractions (Gram, Phi) on that GPU
+    (SURVEY f4); the N x N eigenproblem stays on the host."""
     U = np.ascontiguousarray(snapshots, dtype=np.float64)
     N = U.shape[0]
     if N < 1:
         raise ValueError("compute_pod: no snapshots")
     if rank < 1:
         raise ValueError("compute_pod: rank target must be >= 1")
-    G = U @ U.T
+    G = U @ U.T if device is None else gram_device(U, device)
     G = 0.5 * (G + G.T)
     w, V = np.linalg.eigh(G)
     order = np.argsort(-w, kind="stable")
@@ -217,7 +243,8 @@ def compute_pod(snapshots: np.ndarray, rank: int):
         raise RuntimeError("compute_pod: snapshot matrix is zero")
     numerical_rank = int(np.sum(w > 1e-12 * w[0]))
     r = min(rank, numerical_rank)
-    phi = (U.T @ V[:, :r]) / np.sqrt(w[:r])[None, :]
+    Wr = V[:, :r] / np.sqrt(w[:r])[None, :]
+    phi = U.T @ Wr if device is None or r > 64 else combine_device(U, Wr, device)
     total = float(np.sum(np.maximum(w, 0.0)))
     energy = float(np.sum(w[:r]) / total)
     defect = np.max(np.abs(phi.T @ phi - np.eye(r)))
@@ -272,5 +299,5 @@ def build_problem(cfg: Config, device: int = 0, n_snapshots=None, k=None, solver
             raise RuntimeError(f"generate_snapshots: sample {bad} failed to reach the snapshot tolerance")
     finally:
         s.close()
-    phi, w, _ = compute_pod(x, kk)
+    phi, w, _ = compute_pod(x, kk, device=device)
     return Problem(cfg, mesh, rp, ci, f, phi, w, it)

@@ -20,7 +20,8 @@ if ws > 1:
     from paper_2207_02543_b200.partition import PartitionedSolver
     uid = [PartitionedSolver.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, 0)
-    res, _ = c5.run(a.config, ws, [rank], uid[0], a.snapshots, a.batch, a.k)
+    res, _ = c5.run(a.config, ws, [rank], uid[0], a.snapshots, a.batch, a.k,
+                    device=int(os.environ['LOCAL_RANK']))
 else:
     res, _ = c5.run(a.config, a.world, None, None, a.snapshots, a.batch, a.k)
 res.pop('history')
