@@ -78,3 +78,22 @@ def test_nccl_transport_single_rank(gpu):
         out.append((xs[0], it))
         P.close()
     assert np.array_equal(out[0][1], out[1][1]) and np.array_equal(out[0][0], out[1][0])
+
+
+def test_c5_driver_end_to_end_small(gpu):
+    """paper_2207_02543_b200/c5.py on a small hex8 config: distributed offline
+    stage (bootstrap-coarse snapshot solves, Gram partials and Phi rows on the
+    tensor cores, summed over partitions) and the row-partitioned query solve;
+    1 vs 2 partitions agree (same global colouring, D11 association only)."""
+    from paper_2207_02543_b200 import c5
+    PR.CONFIGS["c98"] = PR.Config("c98", 3, 12, 6, 6, (2.0, 1.0, 1.0), 6, 8, 1, 30)
+    try:
+        res1, x1 = c5.run("c98", world=1, n_snapshots=8, snap_batch=4, log=lambda *a: None)
+        res2, x2 = c5.run("c98", world=2, n_snapshots=8, snap_batch=4, log=lambda *a: None)
+    finally:
+        PR.CONFIGS.pop("c98")
+    assert res1["converged"] and res2["converged"]
+    assert abs(res1["iterations"] - res2["iterations"]) <= 1
+    u1 = x1[0][0]
+    u2 = np.concatenate([x2[0][0], x2[1][0]])
+    assert np.linalg.norm(u1 - u2) <= 1e-7 * np.linalg.norm(u1)
