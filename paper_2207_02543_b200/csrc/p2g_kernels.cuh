@@ -178,22 +178,8 @@ P2G_PRAGMA(unroll P2G_UNROLL)
     }
 }
 
-// L2-coherent (L1-bypassing) vector load: values other warps of the same
-// kernel publish (the dataflow sweep)
-template <int V>
-__device__ __forceinline__ void ldv_cg(double (&d)[V], const double* p) {
-    if constexpr (V == 1) {
-        d[0] = __ldcg(p);
-    } else {
-        const double2 t = __ldcg(reinterpret_cast<const double2*>(p));
-        d[0] = t.x;
-        d[V - 1] = t.y;
-    }
-}
-
-// acc[v] -= vals*X sequentially (gauss_seidel_sweep's `sum -= K_ij u_j`, S == 1 only);
-// CG: gather X through L2 only
-template <class Sh, bool CG = false>
+// acc[v] -= vals*X sequentially (gauss_seidel_sweep's `sum -= K_ij u_j`, S == 1 only)
+template <class Sh>
 __device__ __forceinline__ void row_sub(const Mat& A, const double* X, int b0, int k0, int k1,
                                         double (&acc)[Sh::V]) {
     const unsigned Bp = (unsigned)A.Bp;
@@ -204,10 +190,7 @@ P2G_PRAGMA(unroll P2G_UNROLL)
         const unsigned c = (unsigned)__ldg(A.ci + k);
         double a[Sh::V], x[Sh::V];
         ldv_stream<Sh::V>(a, vb + (unsigned)(k - k0) * Bp);
-        if constexpr (CG)
-            ldv_cg<Sh::V>(x, Xb + c * Bp);
-        else
-            ldv<Sh::V>(x, Xb + c * Bp);
+        ldv<Sh::V>(x, Xb + c * Bp);
 #pragma unroll
         for (int v = 0; v < Sh::V; ++v) acc[v] = __dsub_rn(acc[v], __dmul_rn(a[v], x[v]));
     }
@@ -599,105 +582,6 @@ __global__ void P2G_CLUSTER P2G_ROWK k_gs_backward(Mat A, const double* __restri
         }
     }
     if constexpr (LAST) cluster_partial<Sh>(rs, part_rs, A.Bp, accumulate != 0);
-}
-
-// Dataflow backward sweep (experimental, P2G_DATAFLOW=1; S == 1 shapes): ONE
-// persistent launch per sweep instead of one per colour.  Warps walk the nodes
-// in sweep order (colours C-1 .. 0, colour-major numbering) grid-stride; a
-// node first waits until its neighbours of higher colour -- node index >=
-// the next colour's first node -- have published (done[y] == 1, acquire),
-// then updates its rows (gathers through L2: other SMs' fresh values) and
-// publishes (fence + release).  Every dependency points to an earlier
-// position of every warp's own sequence and the grid is exactly the resident
-// CTA count, so the sweep cannot deadlock; a spin bound reports a stall via
-// *err instead of hanging.  done[] is cleared (memset) before each sweep.
-constexpr int kMaxColorsDF = 64;
-struct ColourOffsets {
-    int C;
-    int off[kMaxColorsDF + 1];  // first node of each colour (+ total)
-};
-
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_gpu(int* p, int v) {
-    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-template <class Sh, bool LAST>
-__global__ void P2G_CLUSTER P2G_ROWK k_gs_backward_df(Mat A, const double* __restrict__ f,
-                                                      const double* xlo, double* s,
-                                                      const int* active, ColourOffsets co,
-                                                      int* done, double* part_rs, int* err) {
-    static_assert(Sh::S == 1 && Sh::R == 1, "dataflow sweep: batched tiles only");
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int b0 = blockIdx.y * Sh::T + lane * Sh::V;
-    bool m[Sh::V], any;
-    lane_mask<Sh>(active, b0, m, any);
-    const int nn = co.off[co.C];
-    int* dn = done + (size_t)blockIdx.y * nn;
-    double rs[Sh::V];
-#pragma unroll
-    for (int v = 0; v < Sh::V; ++v) rs[v] = 0.0;
-    const int W = gridDim.x * kWarps;
-    for (int q = blockIdx.x * kWarps + warp; q < nn; q += W) {
-        // position q of the sweep order -> node; hi = first node of the next colour
-        int c = co.C - 1, cum = 0;
-        while (q >= cum + (co.off[c + 1] - co.off[c])) {
-            cum += co.off[c + 1] - co.off[c];
-            --c;
-        }
-        const int node = co.off[c] + (q - cum);
-        const int hi = co.off[c + 1];
-        {
-            const int i0 = node * A.bs;
-            const int kb = __ldg(A.rp + i0), ke = __ldg(A.rp + i0 + 1);
-            for (int e = kb + lane; e < ke; e += 32) {
-                const int y = __ldg(A.ci + e) / A.bs;
-                if (y >= hi) {
-                    unsigned spins = 0;
-                    while (ld_acquire_gpu(dn + y) == 0) {
-                        if (++spins > (1u << 24)) {
-                            atomicExch(err, 1);
-                            break;
-                        }
-                    }
-                }
-            }
-            __syncwarp();
-        }
-        for (int cc = A.bs - 1; cc >= 0; --cc) {
-            const int i = node * A.bs + cc;
-            if (any) {
-                const int kb = __ldg(A.rp + i), kd = __ldg(A.dpos + i), ke = __ldg(A.rp + i + 1);
-                double acc[Sh::V], d[Sh::V], out[Sh::V], fi[Sh::V];
-                ldv<Sh::V>(acc, f + (size_t)i * A.Bp + b0);
-#pragma unroll
-                for (int v = 0; v < Sh::V; ++v) fi[v] = acc[v];
-                if (xlo != s)  // out of place: s' is read-only during the sweep
-                    row_sub<Sh>(A, xlo, b0, kb, kd, acc);
-                else
-                    row_sub<Sh, true>(A, xlo, b0, kb, kd, acc);
-                row_sub<Sh, true>(A, s, b0, kd + 1, ke, acc);
-                ldv<Sh::V>(d, A.vals + (size_t)kd * A.Bp + b0);
-#pragma unroll
-                for (int v = 0; v < Sh::V; ++v) out[v] = __ddiv_rn(acc[v], d[v]);
-                stv<Sh::V>(s + (size_t)i * A.Bp + b0, out, m);
-                if constexpr (LAST) {
-#pragma unroll
-                    for (int v = 0; v < Sh::V; ++v) rs[v] = __dadd_rn(rs[v], __dmul_rn(fi[v], out[v]));
-                }
-            }
-        }
-        __syncwarp();
-        if (lane == 0) {
-            __threadfence();
-            st_release_gpu(dn + node, 1);
-        }
-    }
-    if constexpr (LAST) cluster_partial<Sh>(rs, part_rs, A.Bp, false);
 }
 
 // Kp recurrence (D9), replacing the SpMV and the p update of the next

@@ -97,8 +97,6 @@ struct p2g_handle {
     int64_t hist_cap_alloc = 0;
     SolveParams* d_prm = nullptr;
     unsigned* d_flag_ticket = nullptr;  // [any-active flag, CTA ticket] of k_finalize
-    int* d_done = nullptr;              // dataflow sweep: per-node published flags
-    int* d_df_err = nullptr;            // dataflow sweep: stall report
     // partials
     int nb_cap = 0;
     double *d_part_dot = nullptr, *d_part_rr = nullptr, *d_part_ff = nullptr,
@@ -227,14 +225,6 @@ int upload_phi(p2g_handle* h, const std::vector<double>& phi, int64_t rows, int 
     CU(cudaMemcpy(h->d_phit, pt.data(), sizeof(double) * pt.size(), cudaMemcpyHostToDevice));
     h->phi_ks = ks;
     return P2G_OK;
-}
-
-bool dataflow_on() {
-    static const bool e = [] {
-        const char* v = std::getenv("P2G_DATAFLOW");
-        return v && v[0] == '1';
-    }();
-    return e;
 }
 
 bool kp_recurrence(const p2g_handle* h) {
@@ -442,38 +432,6 @@ struct Run {
         return P2G_OK;
     }
 
-    // one dataflow backward sweep over all colours (k_gs_backward_df)
-    static int gs_backward_df(p2g_handle* h, const double* f, const double* xlo, double* s,
-                              bool last, int* rs_rows) {
-        if constexpr (Sh::S == 1) {
-            Mat A = mat_of(h);
-            const int nn = static_cast<int>(h->pat.n / h->pat.bs);
-            const int ty = h->Bp / Sh::T;
-            REQ(h->pat.ncolors <= kMaxColorsDF, P2G_EINVAL, "dataflow sweep: too many colours");
-            ColourOffsets co;
-            co.C = h->pat.ncolors;
-            for (int c = 0; c <= co.C; ++c) co.off[c] = static_cast<int>(h->pat.color_rows[c] / h->pat.bs);
-            TRY(ensure(h, h->d_done, (size_t)nn * ty));
-            if (!h->d_df_err) {
-                TRY(ensure(h, h->d_df_err, 1));
-                CU(cudaMemset(h->d_df_err, 0, sizeof(int)));
-            }
-            CU(cudaMemsetAsync(h->d_done, 0, sizeof(int) * (size_t)nn * ty, h->stream));
-            auto fn = last ? k_gs_backward_df<Sh, true> : k_gs_backward_df<Sh, false>;
-            // every CTA of the grid (all instance tiles) must be co-resident
-            int64_t gx = resident_ctas(h, (const void*)fn, true) / ty;
-            gx = gx / kCluster * kCluster;
-            REQ(gx >= kCluster, P2G_EINVAL, "dataflow sweep: too many instance tiles");
-            dim3 g((unsigned)gx, (unsigned)ty);
-            fn<<<g, kBlock, 0, h->stream>>>(A, f, xlo, s, h->d_active, co, h->d_done,
-                                            last ? h->d_part_rs : nullptr, h->d_df_err);
-            if (last) *rs_rows = g.x / kCluster;
-            count_launch(h, KC_BWD);
-            CU(cudaGetLastError());
-        }
-        return P2G_OK;
-    }
-
     // Kp / p / pKp by the recurrence (D9); returns the partial row count
     static int kp_update(p2g_handle* h, const double* s_new, const double* s_prol, int* nb_out) {
         Mat A = mat_of(h);
@@ -657,12 +615,8 @@ struct Run {
                 // LAST backward sweep reads its L part from s' and writes d_s2
                 const bool oop = last && kp_recurrence(h);
                 double* out = oop ? h->d_s2 : cur;
-                if (dataflow_on() && Sh::S == 1) {
-                    TRY(gs_backward_df(h, rr, cur, out, last, &rs_row));
-                } else {
-                    for (int c = C - 1; c >= 0; --c)
-                        TRY(gs_backward(h, rr, cur, out, c, last, &rs_row, c == C - 1));
-                }
+                for (int c = C - 1; c >= 0; --c)
+                    TRY(gs_backward(h, rr, cur, out, c, last, &rs_row, c == C - 1));
                 if (oop) {
                     h->s_prol = cur;
                     cur = out;
@@ -1209,11 +1163,6 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
     cudaEventElapsedTime(&ms_loop, h->ev[1], h->ev[2]);
     h->last_ms[0] = ms_all;
     h->last_ms[1] = ms_loop;
-    if (h->d_df_err) {
-        int dfe = 0;
-        CU(cudaMemcpy(&dfe, h->d_df_err, sizeof(int), cudaMemcpyDeviceToHost));
-        REQ(dfe == 0, P2G_ECUDA, "dataflow sweep stalled (spin bound exceeded)");
-    }
     int64_t maxit = 0;
     for (int b = 0; b < h->B; ++b) maxit = std::max<int64_t>(maxit, it[b]);
     if (eager_iters < 0)
@@ -1315,8 +1264,6 @@ int p2g_destroy(p2g_handle* h) {
     dfree(h->d_vals);
     dfree(h->d_phi);
     dfree(h->d_phit);
-    dfree(h->d_done);
-    dfree(h->d_df_err);
     dfree(h->d_sg_widths);
     dfree(h->d_sg_W);
     dfree(h->d_sg_b);
