@@ -44,7 +44,10 @@ constexpr int kCluster = 8;
 // Streaming row kernels are latency bound unless the SM is full: cap them at
 // 32 registers so 8 CTAs x 8 warps (100% occupancy) stay resident (the
 // difference between 4.4 and 6.3 TB/s for the batched SpMV, tools/spmv_lab.cu).
-#define P2G_ROWK __launch_bounds__(kBlock, Sh::W == 1 ? 6 : P2G_MINB)
+#ifndef P2G_B1_MINB
+#define P2G_B1_MINB 8  // single-instance shapes: CTAs per SM (small spills beat fewer warps)
+#endif
+#define P2G_ROWK __launch_bounds__(kBlock, Sh::W == 1 ? P2G_B1_MINB : P2G_MINB)
 #ifndef P2G_UNROLL
 #define P2G_UNROLL 4  // entries of a row in flight per warp (row loops)
 #endif

@@ -844,6 +844,8 @@ int alloc_batch(p2g_handle* h) {
 int choose_shape(p2g_handle* h, int B) {
     if (B == 1) {
         h->shape = SH_B1A;  // 4 rows x 8 slots per warp (more rows in flight than a warp per row)
+        const char* b1 = std::getenv("P2G_B1_SHAPE");  // tuning knob: "b" = a warp per row
+        if (b1 && b1[0] == 'b') h->shape = SH_B1B;
         h->Bp = 1;
     } else if (B <= 8) {
         h->shape = SH_B8;

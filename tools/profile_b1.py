@@ -5,7 +5,11 @@ sys.path.insert(0, '.')
 from paper_2207_02543_b200 import problems as PR, _lib as L
 from paper_2207_02543_b200.solver import BatchSolver
 
-for dims in [(2, 64, 32, 1, 2.0), (3, 80, 80, 80, 1.0), (3, 128, 128, 128, 1.0)]:
+CASES = [(2, 64, 32, 1, 2.0), (3, 80, 80, 80, 1.0), (3, 128, 128, 128, 1.0)]
+if len(sys.argv) > 1:  # e.g. "3,80": one case
+    d, m_ = map(int, sys.argv[1].split(","))
+    CASES = [c for c in CASES if c[0] == d and c[1] == m_]
+for dims in CASES:
     dim, nx, ny, nz, Lx = dims
     m = PR.Mesh(dim, nx, ny, nz, Lx, 1.0, 1.0)
     rp, ci = m.pattern()
