@@ -319,3 +319,42 @@ def test_pod2g_solve_matches_oracle(gpu, B):
         err = np.linalg.norm(x[b][perm] - ref_m.u) / np.linalg.norm(ref_m.u)
         assert err <= X_RTOL, err
     s.close()
+
+
+def test_tma_staged_restriction_prolongation_variant(gpu, monkeypatch):
+    """The TMA-staged (cp.async.bulk + mbarrier) tensor-core restriction and
+    prolongation (P2G_TMA=1, the measured alternative to the register-fed
+    kernels) give the same preconditioner and solves."""
+    monkeypatch.setenv("P2G_TMA", "1")
+    B = 40
+    m, rp, ci, f, V, phi = small_problem(B=B, k=12)
+    s = make_solver(m, rp, ci, V, phi)
+    perm, prp, pci, pV, pf, pphi = perm_system(s, rp, ci, V, f, phi)
+    R = np.random.default_rng(8).standard_normal((B, m.n))
+    S = s.precond_apply(R)
+    for b in (0, B - 1):
+        s_ref = _oracle_apply(prp, pci, pV[b], pphi, R[b][perm])
+        assert np.linalg.norm(S[b][perm] - s_ref) <= 1e-11 * np.linalg.norm(s_ref)
+    F = np.broadcast_to(f, (B, m.n)).copy()
+    x, it, conv, status, hist = s.solve(F, None, 1e-8, 2000, x0_mode=L.X0_REDUCED)
+    x0_ref, _, _ = ORC.reduced_solve(prp, pci, pV[0], pf, pphi)
+    ref = ORC.pcg_pod2g(prp, pci, pV[0], pf, pphi, x0_ref, 1e-8, 2000)
+    assert np.all(conv) and abs(int(it[0]) - ref.iters) <= 1
+    s.close()
+
+
+def test_two_instance_tiles(gpu):
+    """B = 70: two 64-instance tiles (grid.y = 2) through every kernel,
+    including the tensor-core restriction / prolongation and the coarse solve."""
+    B = 70
+    m, rp, ci, f, V, phi = small_problem(B=B, k=10, nx=32, ny=16)
+    s = make_solver(m, rp, ci, V, phi)
+    perm, prp, pci, pV, pf, pphi = perm_system(s, rp, ci, V, f, phi)
+    F = np.broadcast_to(f, (B, m.n)).copy()
+    x, it, conv, status, hist = s.solve(F, None, 1e-8, 2000, x0_mode=L.X0_REDUCED)
+    assert np.all(conv) and np.all(status == 0)
+    for b in (0, 63, 64, 69):
+        x0_ref, _, _ = ORC.reduced_solve(prp, pci, pV[b], pf, pphi)
+        ref = ORC.pcg_pod2g(prp, pci, pV[b], pf, pphi, x0_ref, 1e-8, 2000)
+        _check_solve(x[b], it[b], conv[b], status[b], hist[b], None, ref, 1e-8)
+    s.close()
