@@ -703,6 +703,373 @@ __global__ void P2G_CLUSTER P2G_ROWK k_jacobi(Mat A, const double* __restrict__ 
     if constexpr (LAST) cluster_partial<Sh>(rs, part_rs, A.Bp, false);
 }
 
+// ================================================ node-blocked row kernels
+// FEM vector problems: every node's BS rows share one column pattern made of
+// whole node blocks (checked on the host, p2g_pattern.cpp build_node_table).
+// A warp then walks a node's neighbour NODES once for all BS rows:
+//   * one x gather (BS consecutive rows of X) serves BS matrix rows,
+//   * the neighbour list is one lane-parallel load (lane j = neighbour j,
+//     staged in shared memory), prefetched one node ahead,
+// so the per-node latency chain shrinks from BS x (row length / unroll)
+// dependent ci -> gather rounds to about (neighbours / unroll) rounds.
+// Every row still combines its terms in ascending column order with the same
+// separately rounded operations, so results are bit-identical to the row
+// kernels above (and to the reference's row sums).
+// Used for the one-instance-per-lane shapes (S == 1).
+struct NodeTab {
+    const int4* info;  // per node {kb0 = first value of row 0, rowlen, pos = own slot, nnb}
+    const int* ncol;   // [nodes][nmax] neighbour node ids, ascending
+    int nmax;
+};
+
+#ifndef P2G_BLK_UNR_L
+#define P2G_BLK_UNR_L 1  // neighbour nodes in flight, all-row passes
+#endif
+#ifndef P2G_BLK_UNR_U
+#define P2G_BLK_UNR_U 2  // neighbour nodes in flight, one-row passes
+#endif
+
+__device__ __forceinline__ void node_fetch(const NodeTab& T, int node, int lane, int4& inf, int& nc) {
+    inf = __ldg(T.info + node);
+    nc = lane < T.nmax ? __ldg(T.ncol + (size_t)node * T.nmax + lane) : 0;
+}
+
+// acc[c] (-= if SUB else +=) vals(row c, slot j, comp cc) * X[ncol_j*BS + cc]
+// for slots j in [j0, j1), rows c in [C0, C1), cc ascending.  DIFF: the
+// operand is X - X0 (Kp recurrence).  vb = values of row 0 of the node at
+// this lane's instances; nc = the warp's neighbour list in shared memory.
+template <class Sh, int BS, int C0, int C1, bool SUB, bool DIFF, int UNR>
+__device__ __forceinline__ void blk_pass(const double* vb, unsigned rowlen, unsigned Bp,
+                                         const double* X, const double* X0, const int* nc, int j0,
+                                         int j1, double (&acc)[BS][Sh::V]) {
+    constexpr int V = Sh::V;
+#pragma unroll UNR
+    for (int j = j0; j < j1; ++j) {
+        const unsigned xo = (unsigned)nc[j] * (unsigned)BS * Bp;
+        double x[BS][V];
+#pragma unroll
+        for (int cc = 0; cc < BS; ++cc) {
+            ldv<V>(x[cc], X + xo + cc * Bp);
+            if constexpr (DIFF) {
+                double x0[V];
+                ldv<V>(x0, X0 + xo + cc * Bp);
+#pragma unroll
+                for (int v = 0; v < V; ++v) x[cc][v] = __dsub_rn(x[cc][v], x0[v]);
+            }
+        }
+#pragma unroll
+        for (int c = C0; c < C1; ++c) {
+#pragma unroll
+            for (int cc = 0; cc < BS; ++cc) {
+                double a[V];
+                ldv_stream<V>(a, vb + ((unsigned)c * rowlen + (unsigned)(j * BS + cc)) * Bp);
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const double pr = __dmul_rn(a[v], x[cc][v]);
+                    acc[c][v] = SUB ? __dsub_rn(acc[c][v], pr) : __dadd_rn(acc[c][v], pr);
+                }
+            }
+        }
+    }
+}
+
+// one row (values at vr = that row's first value): acc -= vals * X over slots [j0, j1)
+template <class Sh, int BS, int UNR>
+__device__ __forceinline__ void blk_pass_row(const double* vr, unsigned Bp, const double* X,
+                                             const int* nc, int j0, int j1, double (&acc)[Sh::V]) {
+    constexpr int V = Sh::V;
+#pragma unroll UNR
+    for (int j = j0; j < j1; ++j) {
+        const unsigned xo = (unsigned)nc[j] * (unsigned)BS * Bp;
+#pragma unroll
+        for (int cc = 0; cc < BS; ++cc) {
+            double x[V], a[V];
+            ldv<V>(x, X + xo + cc * Bp);
+            ldv_stream<V>(a, vr + (unsigned)(j * BS + cc) * Bp);
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[v] = __dsub_rn(acc[v], __dmul_rn(a[v], x[v]));
+        }
+    }
+}
+
+// node loop with the next node's table entry prefetched; body(node, inf, nc)
+#define P2G_BLK_NODE_LOOP(T, nb, ne, ...)                                                    \
+    {                                                                                         \
+        __shared__ int sh_nc_[kWarps][32];                                                    \
+        const int lane_ = threadIdx.x & 31, warp_ = threadIdx.x >> 5;                         \
+        const int stride_ = gridDim.x * kWarps;                                               \
+        int node_ = (nb) + blockIdx.x * kWarps + warp_;                                       \
+        int4 inf_n_ = make_int4(0, 0, 0, 0);                                                  \
+        int nc_n_ = 0;                                                                        \
+        if (node_ < (ne)) node_fetch(T, node_, lane_, inf_n_, nc_n_);                         \
+        for (; node_ < (ne); node_ += stride_) {                                              \
+            __syncwarp();                                                                     \
+            sh_nc_[warp_][lane_] = nc_n_;                                                     \
+            const int4 inf = inf_n_;                                                          \
+            __syncwarp();                                                                     \
+            if (node_ + stride_ < (ne)) node_fetch(T, node_ + stride_, lane_, inf_n_, nc_n_); \
+            const int node = node_;                                                           \
+            const int* nc = sh_nc_[warp_];                                                    \
+            __VA_ARGS__                                                                       \
+        }                                                                                     \
+    }
+
+// Forward GS colour phase, first sweep from s = 0 (L part only), all BS rows
+// of a node together: lower neighbour nodes, then the node's own lower
+// components (new values), then the division (smoothers.hpp:31-44).
+template <class Sh, int BS>
+__global__ void P2G_ROWK k_gs_forward_blk(Mat A, NodeTab T, const double* __restrict__ f, double* s,
+                                          const int* active, int nb, int ne) {
+    constexpr int V = Sh::V;
+    LaneGeo<Sh> G;
+    const int b0 = blockIdx.y * Sh::T + G.w * V;
+    bool m[V], any;
+    lane_mask<Sh>(active, b0, m, any);
+    const unsigned Bp = (unsigned)A.Bp;
+    P2G_BLK_NODE_LOOP(T, nb, ne, {
+        if (any) {
+            const double* vb = A.vals + (size_t)inf.x * Bp + b0;
+            const unsigned rl = (unsigned)inf.y, pos = (unsigned)inf.z;
+            double* sb = s + (size_t)node * BS * Bp + b0;
+            double acc[BS][V];
+#pragma unroll
+            for (int c = 0; c < BS; ++c) ldv<V>(acc[c], f + ((size_t)node * BS + c) * Bp + b0);
+            blk_pass<Sh, BS, 0, BS, true, false, P2G_BLK_UNR_L>(vb, rl, Bp, s + b0, nullptr, nc, 0,
+                                                                (int)pos, acc);
+            double sn[BS][V];
+#pragma unroll
+            for (int c = 0; c < BS; ++c) {
+#pragma unroll
+                for (int cc = 0; cc < c; ++cc) {
+                    double a[V];
+                    ldv_stream<V>(a, vb + (c * rl + pos * BS + cc) * Bp);
+#pragma unroll
+                    for (int v = 0; v < V; ++v)
+                        acc[c][v] = __dsub_rn(acc[c][v], __dmul_rn(a[v], sn[cc][v]));
+                }
+                double d[V];
+                ldv<V>(d, vb + (c * rl + pos * BS + c) * Bp);
+#pragma unroll
+                for (int v = 0; v < V; ++v) sn[c][v] = __ddiv_rn(acc[c][v], d[v]);
+                stv<V>(sb + c * Bp, sn[c], m);
+            }
+        }
+    })
+}
+
+// Backward GS colour phase (gauss_seidel_sweep_backward, smoothers.hpp:56-70),
+// rows of a node descending.  Row c's terms in column order are: lower nodes
+// and own components < c (old values, xlo), own components > c (this node's
+// new values), upper nodes (new values, s).  Pass 1 runs the lower nodes for
+// all rows at once; each row then takes its own pass over the upper nodes
+// after the new components it needs (gathers of s hit L1 on the repeat).
+// xlo == s: in place; xlo = s' (D9): out of place.  LAST: r.s partial.
+template <class Sh, int BS, bool LAST>
+__global__ void P2G_CLUSTER P2G_ROWK k_gs_backward_blk(Mat A, NodeTab T, const double* __restrict__ f,
+                                                       const double* xlo, double* s,
+                                                       const int* active, int nb, int ne,
+                                                       double* part_rs, int accumulate) {
+    constexpr int V = Sh::V;
+    LaneGeo<Sh> G;
+    const int b0 = blockIdx.y * Sh::T + G.w * V;
+    bool m[V], any;
+    lane_mask<Sh>(active, b0, m, any);
+    double rs[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) rs[v] = 0.0;
+    const unsigned Bp = (unsigned)A.Bp;
+    P2G_BLK_NODE_LOOP(T, nb, ne, {
+        if (any) {
+            const double* vb = A.vals + (size_t)inf.x * Bp + b0;
+            const unsigned rl = (unsigned)inf.y, pos = (unsigned)inf.z;
+            const int nnb = inf.w;
+            const size_t ro = (size_t)node * BS * Bp + b0;
+            double acc[BS][V], fi[BS][V];
+#pragma unroll
+            for (int c = 0; c < BS; ++c) {
+                ldv<V>(fi[c], f + ro + c * Bp);
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[c][v] = fi[c][v];
+            }
+            blk_pass<Sh, BS, 0, BS, true, false, P2G_BLK_UNR_L>(vb, rl, Bp, xlo + b0, nullptr, nc, 0,
+                                                                (int)pos, acc);
+            // own components below each row (old values)
+            if constexpr (BS > 1) {
+                double xo[BS - 1][V];
+#pragma unroll
+                for (int cc = 0; cc < BS - 1; ++cc) ldv<V>(xo[cc], xlo + ro + cc * Bp);
+#pragma unroll
+                for (int c = 1; c < BS; ++c) {
+#pragma unroll
+                    for (int cc = 0; cc < c; ++cc) {
+                        double a[V];
+                        ldv_stream<V>(a, vb + (c * rl + pos * BS + cc) * Bp);
+#pragma unroll
+                        for (int v = 0; v < V; ++v)
+                            acc[c][v] = __dsub_rn(acc[c][v], __dmul_rn(a[v], xo[cc][v]));
+                    }
+                }
+            }
+            double sn[BS][V];
+#pragma unroll
+            for (int c = BS - 1; c >= 0; --c) {
+#pragma unroll
+                for (int cc = c + 1; cc < BS; ++cc) {
+                    double a[V];
+                    ldv_stream<V>(a, vb + (c * rl + pos * BS + cc) * Bp);
+#pragma unroll
+                    for (int v = 0; v < V; ++v)
+                        acc[c][v] = __dsub_rn(acc[c][v], __dmul_rn(a[v], sn[cc][v]));
+                }
+                // one-row pass over the upper nodes
+                blk_pass_row<Sh, BS, P2G_BLK_UNR_U>(vb + c * rl * Bp, Bp, s + b0, nc, (int)pos + 1,
+                                                    nnb, acc[c]);
+                double d[V];
+                ldv<V>(d, vb + (c * rl + pos * BS + c) * Bp);
+#pragma unroll
+                for (int v = 0; v < V; ++v) sn[c][v] = __ddiv_rn(acc[c][v], d[v]);
+                stv<V>(s + ro + c * Bp, sn[c], m);
+                if constexpr (LAST) {
+#pragma unroll
+                    for (int v = 0; v < V; ++v) rs[v] = __dadd_rn(rs[v], __dmul_rn(fi[c][v], sn[c][v]));
+                }
+            }
+        }
+    })
+    if constexpr (LAST) cluster_partial<Sh>(rs, part_rs, A.Bp, accumulate != 0);
+}
+
+// Kp recurrence (D9, see k_kp_update) with node blocking: the L part of all
+// BS rows (lower nodes, then own components < c) of s - s'.
+template <class Sh, int BS>
+__global__ void P2G_CLUSTER P2G_ROWK k_kp_update_blk(Mat A, NodeTab T, const double* __restrict__ r,
+                                                     const double* __restrict__ s,
+                                                     const double* __restrict__ sp,
+                                                     double* __restrict__ Kp, double* __restrict__ p,
+                                                     const double* beta, const int* active,
+                                                     double* part) {
+    constexpr int V = Sh::V;
+    LaneGeo<Sh> G;
+    const int b0 = blockIdx.y * Sh::T + G.w * V;
+    bool m[V], any;
+    lane_mask<Sh>(active, b0, m, any);
+    double bt[V], dacc[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        bt[v] = beta[b0 + v];
+        dacc[v] = 0.0;
+    }
+    const unsigned Bp = (unsigned)A.Bp;
+    const int nn = A.n / BS;
+    P2G_BLK_NODE_LOOP(T, 0, nn, {
+        if (any) {
+            const double* vb = A.vals + (size_t)inf.x * Bp + b0;
+            const unsigned rl = (unsigned)inf.y, pos = (unsigned)inf.z;
+            const size_t ro = (size_t)node * BS * Bp + b0;
+            double acc[BS][V];
+#pragma unroll
+            for (int c = 0; c < BS; ++c)
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[c][v] = 0.0;
+            blk_pass<Sh, BS, 0, BS, false, true, P2G_BLK_UNR_L>(vb, rl, Bp, s + b0, sp + b0, nc, 0,
+                                                                 (int)pos, acc);
+            if constexpr (BS > 1) {
+                double xd[BS - 1][V];
+#pragma unroll
+                for (int cc = 0; cc < BS - 1; ++cc) {
+                    double x1[V], x0[V];
+                    ldv<V>(x1, s + ro + cc * Bp);
+                    ldv<V>(x0, sp + ro + cc * Bp);
+#pragma unroll
+                    for (int v = 0; v < V; ++v) xd[cc][v] = __dsub_rn(x1[v], x0[v]);
+                }
+#pragma unroll
+                for (int c = 1; c < BS; ++c) {
+#pragma unroll
+                    for (int cc = 0; cc < c; ++cc) {
+                        double a[V];
+                        ldv_stream<V>(a, vb + (c * rl + pos * BS + cc) * Bp);
+#pragma unroll
+                        for (int v = 0; v < V; ++v)
+                            acc[c][v] = __dadd_rn(acc[c][v], __dmul_rn(a[v], xd[cc][v]));
+                    }
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < BS; ++c) {
+                const size_t o = ro + c * Bp;
+                double ri[V], si[V], kpi[V], pi[V];
+                ldv<V>(ri, r + o);
+                ldv<V>(si, s + o);
+                ldv<V>(kpi, Kp + o);
+                ldv<V>(pi, p + o);
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    kpi[v] = __dadd_rn(__dadd_rn(ri[v], acc[c][v]), __dmul_rn(bt[v], kpi[v]));
+                    pi[v] = __dadd_rn(si[v], __dmul_rn(bt[v], pi[v]));
+                    dacc[v] = __dadd_rn(dacc[v], __dmul_rn(pi[v], kpi[v]));
+                }
+                stv<V>(Kp + o, kpi, m);
+                stv<V>(p + o, pi, m);
+            }
+        }
+    })
+    cluster_partial<Sh>(dacc, part, A.Bp, false);
+}
+
+// Residual after one forward sweep from zero, t = -U u (RES_UPPER, D6), node
+// blocked: row c's U part is own components > c, then the upper nodes.
+template <class Sh, int BS>
+__global__ void P2G_CLUSTER P2G_ROWK k_residual_upper_blk(Mat A, NodeTab T, const double* __restrict__ u,
+                                                          double* __restrict__ t,
+                                                          const int* active) {
+    constexpr int V = Sh::V;
+    LaneGeo<Sh> G;
+    const int b0 = blockIdx.y * Sh::T + G.w * V;
+    bool m[V], any;
+    lane_mask<Sh>(active, b0, m, any);
+    const unsigned Bp = (unsigned)A.Bp;
+    const int nn = A.n / BS;
+    P2G_BLK_NODE_LOOP(T, 0, nn, {
+        if (any) {
+            const double* vb = A.vals + (size_t)inf.x * Bp + b0;
+            const unsigned rl = (unsigned)inf.y, pos = (unsigned)inf.z;
+            const int nnb = inf.w;
+            const size_t ro = (size_t)node * BS * Bp + b0;
+            double acc[BS][V];
+#pragma unroll
+            for (int c = 0; c < BS; ++c)
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[c][v] = 0.0;
+            if constexpr (BS > 1) {
+                double xo[BS][V];
+#pragma unroll
+                for (int cc = 1; cc < BS; ++cc) ldv<V>(xo[cc], u + ro + cc * Bp);
+#pragma unroll
+                for (int c = 0; c < BS - 1; ++c) {
+#pragma unroll
+                    for (int cc = c + 1; cc < BS; ++cc) {
+                        double a[V];
+                        ldv_stream<V>(a, vb + (c * rl + pos * BS + cc) * Bp);
+#pragma unroll
+                        for (int v = 0; v < V; ++v)
+                            acc[c][v] = __dadd_rn(acc[c][v], __dmul_rn(a[v], xo[cc][v]));
+                    }
+                }
+            }
+            blk_pass<Sh, BS, 0, BS, false, false, P2G_BLK_UNR_L>(vb, rl, Bp, u + b0, nullptr, nc,
+                                                                  (int)pos + 1, nnb, acc);
+#pragma unroll
+            for (int c = 0; c < BS; ++c) {
+                double ti[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) ti[v] = -acc[c][v];
+                stv<V>(t + ro + c * Bp, ti, m);
+            }
+        }
+    })
+}
+
 // Restriction c = Phi^T t (PodBasis::project, pod.hpp:27-35) of a vector
 // t[n][Bp] (the residual, or f itself for reduced_solve, pod.hpp:171).
 // Lanes: R = 32/W rows x W instance lanes x V instances; each lane keeps the

@@ -205,4 +205,47 @@ std::string build_coloured_pattern(int64_t n, const uint64_t* rp, const uint64_t
     return "";
 }
 
+bool build_node_table(int64_t n, int bs, const std::vector<int32_t>& rp,
+                      const std::vector<int32_t>& ci, const std::vector<int32_t>& dpos,
+                      std::vector<int32_t>& info, std::vector<int32_t>& ncol, int& nmax) {
+    info.clear();
+    ncol.clear();
+    nmax = 0;
+    if (bs < 1 || n % bs != 0) return false;
+    const int64_t nn = n / bs;
+    for (int64_t a = 0; a < nn; ++a) {
+        const int64_t r0 = a * bs;
+        const int32_t len = rp[r0 + 1] - rp[r0];
+        if (len <= 0 || len % bs != 0 || len / bs > 32) return false;
+        nmax = std::max(nmax, len / bs);
+    }
+    info.resize(4 * nn);
+    ncol.assign(nn * nmax, 0);
+    for (int64_t a = 0; a < nn; ++a) {
+        const int64_t r0 = a * bs;
+        const int32_t kb = rp[r0], len = rp[r0 + 1] - rp[r0], nnb = len / bs;
+        int32_t pos = -1;
+        for (int32_t j = 0; j < nnb; ++j) {
+            const int32_t c0 = ci[kb + j * bs];
+            if (c0 % bs != 0) return false;
+            if (c0 == r0) pos = j;
+            ncol[a * nmax + j] = c0 / bs;
+            for (int c = 0; c < bs; ++c) {
+                const int64_t kc = kb + (int64_t)c * len;
+                if (rp[r0 + c + 1] - rp[r0 + c] != len || rp[r0 + c] != kc) return false;
+                for (int cc = 0; cc < bs; ++cc)
+                    if (ci[kc + j * bs + cc] != c0 + cc) return false;
+            }
+        }
+        if (pos < 0) return false;
+        for (int c = 0; c < bs; ++c)
+            if (dpos[r0 + c] != kb + (int64_t)c * len + pos * bs + c) return false;
+        info[4 * a + 0] = kb;
+        info[4 * a + 1] = len;
+        info[4 * a + 2] = pos;
+        info[4 * a + 3] = nnb;
+    }
+    return true;
+}
+
 }  // namespace p2g

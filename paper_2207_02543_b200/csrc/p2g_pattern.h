@@ -38,4 +38,16 @@ std::vector<int32_t> order_colours(int ncol, const std::vector<double>& W);
 std::string build_coloured_pattern(int64_t n, const uint64_t* row_offsets,
                                    const uint64_t* col_indices, int bs, ColouredPattern& out);
 
+// Node-blocked view of a (coloured) local pattern for the node-blocked row
+// kernels (NodeTab, p2g_kernels.cuh).  Returns false unless every node's bs
+// rows share one ascending column list made of whole node blocks
+// (bs consecutive columns starting at a multiple of bs) with at most 32
+// neighbour nodes.  info[4a..4a+3] = {first value of row 0 of node a, row
+// length, slot of node a in its own list, neighbour count}; ncol[a*nmax + j]
+// = neighbour node j of node a (column / bs).  Columns may point past the
+// owned rows (ghost nodes of a partitioned handle).
+bool build_node_table(int64_t n, int bs, const std::vector<int32_t>& rp,
+                      const std::vector<int32_t>& ci, const std::vector<int32_t>& dpos,
+                      std::vector<int32_t>& info, std::vector<int32_t>& ncol, int& nmax);
+
 }  // namespace p2g

@@ -66,6 +66,11 @@ struct p2g_handle {
     bool own_stream = true;
     int *d_rp = nullptr, *d_ci = nullptr, *d_dpos = nullptr;
     int64_t *d_vperm = nullptr, *d_perm = nullptr;
+    // node-blocked view (build_node_table); node_blk == false: row kernels only
+    bool node_blk = false;
+    int nmax = 0;
+    int4* d_ninfo = nullptr;
+    int* d_ncol = nullptr;
 
     // batch
     int B = 0, Bp = 0, shape = SH_B64;
@@ -303,6 +308,18 @@ struct Run {
 
     static int nnodes(p2g_handle* h) { return static_cast<int>(h->pat.n / h->pat.bs); }
 
+    // node-blocked kernels: one-instance-per-lane shapes on node-blocked patterns
+    static bool blk(const p2g_handle* h) { return Sh::S == 1 && h->node_blk; }
+    static NodeTab ntab(const p2g_handle* h) { return NodeTab{h->d_ninfo, h->d_ncol, h->nmax}; }
+#define P2G_BS_SWITCH(bs, ...)          \
+    if ((bs) == 2) {                    \
+        constexpr int BS = 2;           \
+        __VA_ARGS__                     \
+    } else {                            \
+        constexpr int BS = 3;           \
+        __VA_ARGS__                     \
+    }
+
     // the two producers of pKp partials (k_spmv<DOT>, k_kp_update) share one
     // grid so k_alpha always reduces the same number of partial rows
     static dim3 dot_grid(p2g_handle* h) {
@@ -391,6 +408,18 @@ struct Run {
         const int nb = static_cast<int>(h->pat.color_rows[c] / h->pat.bs);
         const int ne = static_cast<int>(h->pat.color_rows[c + 1] / h->pat.bs);
         if (ne <= nb) return P2G_OK;
+        if constexpr (Sh::S == 1) {
+            if (first && blk(h)) {
+                P2G_BS_SWITCH(h->pat.bs, {
+                    auto fn = k_gs_forward_blk<Sh, BS>;
+                    dim3 g = node_grid<Sh>(h, ne - nb, (const void*)fn);
+                    fn<<<g, kBlock, 0, h->stream>>>(A, ntab(h), f, s, h->d_active, nb, ne);
+                })
+                count_launch(h, KC_FWD);
+                CU(cudaGetLastError());
+                return P2G_OK;
+            }
+        }
         if (first) {
             auto fn = k_gs_forward<Sh, true>;
             dim3 g = node_grid<Sh>(h, ne - nb, (const void*)fn);
@@ -416,6 +445,27 @@ struct Run {
         int64_t maxc = 1;
         for (int q = 0; q < h->pat.ncolors; ++q)
             maxc = std::max<int64_t>(maxc, (h->pat.color_rows[q + 1] - h->pat.color_rows[q]) / h->pat.bs);
+        if constexpr (Sh::S == 1) {
+            if (blk(h)) {
+                P2G_BS_SWITCH(h->pat.bs, {
+                    if (last) {
+                        auto fn = k_gs_backward_blk<Sh, BS, true>;
+                        dim3 g = node_grid<Sh>(h, maxc, (const void*)fn, true);
+                        fn<<<g, kBlock, 0, h->stream>>>(A, ntab(h), f, xlo, s, h->d_active, nb, ne,
+                                                        h->d_part_rs, first_phase ? 0 : 1);
+                        *rs_rows = g.x / kCluster;
+                    } else {
+                        auto fn = k_gs_backward_blk<Sh, BS, false>;
+                        dim3 g = node_grid<Sh>(h, maxc, (const void*)fn, true);
+                        fn<<<g, kBlock, 0, h->stream>>>(A, ntab(h), f, xlo, s, h->d_active, nb, ne,
+                                                        nullptr, 0);
+                    }
+                })
+                count_launch(h, KC_BWD);
+                CU(cudaGetLastError());
+                return P2G_OK;
+            }
+        }
         if (last) {
             auto fn = k_gs_backward<Sh, true>;
             dim3 g = node_grid<Sh>(h, maxc, (const void*)fn, true);
@@ -435,10 +485,21 @@ struct Run {
     // Kp / p / pKp by the recurrence (D9); returns the partial row count
     static int kp_update(p2g_handle* h, const double* s_new, const double* s_prol, int* nb_out) {
         Mat A = mat_of(h);
-        auto fn = k_kp_update<Sh>;
         dim3 g = dot_grid(h);
-        fn<<<g, kBlock, 0, h->stream>>>(A, h->d_r, s_new, s_prol, h->d_Kp, h->d_p, h->d_beta,
-                                        h->d_active, h->d_part_dot);
+        bool done = false;
+        if constexpr (Sh::S == 1) {
+            if (blk(h)) {
+                P2G_BS_SWITCH(h->pat.bs, {
+                    k_kp_update_blk<Sh, BS><<<g, kBlock, 0, h->stream>>>(
+                        A, ntab(h), h->d_r, s_new, s_prol, h->d_Kp, h->d_p, h->d_beta, h->d_active,
+                        h->d_part_dot);
+                })
+                done = true;
+            }
+        }
+        if (!done)
+            k_kp_update<Sh><<<g, kBlock, 0, h->stream>>>(A, h->d_r, s_new, s_prol, h->d_Kp, h->d_p,
+                                                         h->d_beta, h->d_active, h->d_part_dot);
         if (nb_out) *nb_out = g.x / kCluster;
         count_launch(h, KC_SPMV);
         CU(cudaGetLastError());
@@ -473,7 +534,19 @@ struct Run {
         const double* t = f;
         if (form != RES_VECTOR) {
             double* tb = h->d_t;
-            if (form == RES_UPPER) {
+            bool done = false;
+            if constexpr (Sh::S == 1) {
+                if (form == RES_UPPER && blk(h) && h->pat.bs == 2) {  // hex8: row kernel faster
+                    P2G_BS_SWITCH(h->pat.bs, {
+                        auto fn = k_residual_upper_blk<Sh, BS>;
+                        dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn, true);
+                        fn<<<g, kBlock, 0, h->stream>>>(A, ntab(h), s, tb, h->d_active);
+                    })
+                    done = true;
+                }
+            }
+            if (done) {
+            } else if (form == RES_UPPER) {
                 auto fn = k_residual<Sh, RES_UPPER>;
                 dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn, true);
                 fn<<<g, kBlock, 0, h->stream>>>(A, f, s, tb, h->d_active, nullptr, nullptr);
@@ -1262,6 +1335,8 @@ int p2g_destroy(p2g_handle* h) {
     dfree(h->d_ci);
     dfree(h->d_dpos);
     dfree(h->d_vperm);
+    dfree(h->d_ninfo);
+    dfree(h->d_ncol);
     dfree(h->d_perm);
     dfree(h->d_vals);
     dfree(h->d_phi);
@@ -1290,6 +1365,26 @@ int p2g_destroy(p2g_handle* h) {
 }
 
 const char* p2g_last_error(const p2g_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+// node-blocked kernels (NodeTab): batched one-instance-per-lane shapes, bs 2 / 3
+// (P2G_NO_NODEBLK=1 keeps the row kernels, for A/B measurements)
+int upload_node_table(p2g_handle* h) {
+    h->node_blk = false;
+    h->nmax = 0;
+    const int bs = h->pat.bs;
+    if ((bs != 2 && bs != 3) || std::getenv("P2G_NO_NODEBLK")) return P2G_OK;
+    std::vector<int32_t> info, ncol;
+    int nmax = 0;
+    if (!build_node_table(h->pat.n, bs, h->pat.rp, h->pat.ci, h->pat.dpos, info, ncol, nmax))
+        return P2G_OK;
+    TRY(dalloc(h, h->d_ninfo, info.size() / 4));
+    TRY(dalloc(h, h->d_ncol, ncol.size()));
+    CU(cudaMemcpy(h->d_ninfo, info.data(), sizeof(int32_t) * info.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_ncol, ncol.data(), sizeof(int32_t) * ncol.size(), cudaMemcpyHostToDevice));
+    h->nmax = nmax;
+    h->node_blk = true;
+    return P2G_OK;
+}
 
 int p2g_set_pattern(p2g_handle* h, int64_t n, const uint64_t* row_offsets,
                     const uint64_t* col_indices, int32_t block_size) {
@@ -1320,7 +1415,7 @@ int p2g_set_pattern(p2g_handle* h, int64_t n, const uint64_t* row_offsets,
                   cudaMemcpyHostToDevice));
     CU(cudaMemcpy(h->d_perm, h->pat.perm.data(), sizeof(int64_t) * h->pat.perm.size(),
                   cudaMemcpyHostToDevice));
-    return P2G_OK;
+    return upload_node_table(h);
 }
 
 int p2g_set_values(p2g_handle* h, int32_t batch, const double* values) {
@@ -2283,7 +2378,7 @@ int p2g_part_set_pattern(p2g_part* P, int rank, int64_t n_global, const int64_t*
         return P2G_OK;
     };
     if (up(h->d_rp, pat.rp) || up(h->d_ci, pat.ci) || up(h->d_dpos, pat.dpos) ||
-        up(h->d_vperm, pat.vperm) || up(h->d_perm, pat.perm)) {
+        up(h->d_vperm, pat.vperm) || up(h->d_perm, pat.perm) || upload_node_table(h)) {
         P->err = h->err;
         return P2G_ECUDA;
     }

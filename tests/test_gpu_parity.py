@@ -358,3 +358,31 @@ def test_two_instance_tiles(gpu):
         ref = ORC.pcg_pod2g(prp, pci, pV[b], pf, pphi, x0_ref, 1e-8, 2000)
         _check_solve(x[b], it[b], conv[b], status[b], hist[b], None, ref, 1e-8)
     s.close()
+
+
+@pytest.mark.parametrize("dims,B", [(2, 40), (2, 64), (3, 33)])
+def test_node_blocked_kernels_bit_identical_to_row_kernels(gpu, monkeypatch, dims, B):
+    """The node-blocked row kernels (NodeTab: forward sweep from zero, backward
+    sweep, upper residual, Kp recurrence) keep every row's ascending-column
+    operation order, so the preconditioner is bit-identical to the row
+    kernels' (P2G_NO_NODEBLK=1), and solves take the same iterations."""
+    if dims == 2:
+        m, rp, ci, f, V, phi = small_problem(B=B, k=10, nx=32, ny=16)
+    else:
+        m, rp, ci, f, V, phi = small_problem(dim=3, nx=5, ny=5, nz=5, Lx=1, Ly=1, Lz=1, B=B, k=8)
+    R = np.random.default_rng(11).standard_normal((B, m.n))
+    F = np.broadcast_to(f, (B, m.n)).copy()
+    out = []
+    for off in (False, True):
+        if off:
+            monkeypatch.setenv("P2G_NO_NODEBLK", "1")
+        s = make_solver(m, rp, ci, V, phi)
+        S = s.precond_apply(R)
+        x, it, conv, status, hist = s.solve(F, None, 1e-8, 2000, x0_mode=L.X0_REDUCED)
+        out.append((S, x, it, status))
+        s.close()
+    (S1, x1, it1, st1), (S0, x0, it0, st0) = out
+    assert np.array_equal(S1, S0)
+    assert np.all(st1 == 0) and np.all(st0 == 0)
+    assert np.all(np.abs(it1 - it0) <= 1)
+    assert np.linalg.norm(x1 - x0) <= 1e-10 * np.linalg.norm(x0)
