@@ -247,9 +247,13 @@ def main():
         cv_h = np.zeros(B, dtype=np.int32)
         st_h = np.zeros(B, dtype=np.int32)
 
-        def step_e2e():
+        def step_e2e(prefetch_next=False):
+            # consumes the copy started during the previous solve, if any
             rc = lib.p2g_set_values(s._h, B, C.cast(vals_h.data_ptr(), Dp))
             assert rc == 0, rc
+            if prefetch_next:  # next batch's values cross the link while this one solves
+                rc = lib.p2g_prefetch_values(s._h, B, C.cast(vals_h.data_ptr(), Dp))
+                assert rc == 0, rc
             s.set_basis(prob.phi)
             s.setup()
             rc = lib.p2g_solve(s._h, C.cast(b_h.data_ptr(), Dp), None, L.X0_REDUCED, cfg.tol,
@@ -263,12 +267,13 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(args.steps):
-            step_e2e()
+        for i in range(args.steps):
+            step_e2e(prefetch_next=pin and i + 1 < args.steps)
         e1.record(stream)
         barrier()
         ems = D.max_over_ranks(e0.elapsed_time(e1), dev)
         e2e = {"value": total_solves / (ems / 1e3), "unit": UNIT, "pinned": pin,
+               "pipelined": bool(pin and args.steps > 1),
                "h2d_bytes_per_step": int(values.nbytes + F.nbytes),
                "d2h_bytes_per_step": int(F.nbytes + 3 * 4 * B)}
 

@@ -30,6 +30,7 @@ SIGNATURES = [
     ("p2g_set_pattern", C.c_int, [H, C.c_int64, U64, U64, C.c_int32]),
     ("p2g_set_values", C.c_int, [H, C.c_int32, D]),
     ("p2g_set_values_device", C.c_int, [H, C.c_int32, C.c_void_p]),
+    ("p2g_prefetch_values", C.c_int, [H, C.c_int32, D]),
     ("p2g_set_basis", C.c_int, [H, C.c_int32, D]),
     ("p2g_setup", C.c_int, [H, C.c_void_p, I32]),
     ("p2g_initial_guess", C.c_int, [H, D, D]),

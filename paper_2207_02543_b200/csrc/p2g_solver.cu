@@ -110,6 +110,13 @@ struct p2g_handle {
     // staging
     double* d_stage = nullptr;
     size_t stage_bytes = 0;
+    // p2g_prefetch_values: next batch's values copied on a side stream
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t pref_ev = nullptr;
+    double* d_pref = nullptr;
+    size_t pref_cap = 0;
+    const double* pref_host = nullptr;
+    int pref_B = 0;
 
     // setup
     p2g_config cfg{};
@@ -1330,6 +1337,12 @@ int p2g_destroy(p2g_handle* h) {
     if (!h) return P2G_EINVAL;
     cudaSetDevice(h->device);
     cudaStreamSynchronize(h->stream);
+    if (h->cstream) {
+        cudaStreamSynchronize(h->cstream);
+        cudaStreamDestroy(h->cstream);
+        cudaEventDestroy(h->pref_ev);
+    }
+    dfree(h->d_pref);
     destroy_graph(h);
     dfree(h->d_rp);
     dfree(h->d_ci);
@@ -1421,7 +1434,40 @@ int p2g_set_pattern(p2g_handle* h, int64_t n, const uint64_t* row_offsets,
 int p2g_set_values(p2g_handle* h, int32_t batch, const double* values) {
     if (!h) return P2G_EINVAL;
     CU(cudaSetDevice(h->device));
+    if (values && values == h->pref_host && batch == h->pref_B) {
+        // consume the prefetched copy: the relayout waits for it on the stream
+        h->pref_host = nullptr;
+        CU(cudaStreamWaitEvent(h->stream, h->pref_ev, 0));
+        return set_values_impl(h, batch, nullptr, h->d_pref);
+    }
     return set_values_impl(h, batch, values, nullptr);
+}
+
+int p2g_prefetch_values(p2g_handle* h, int32_t batch, const double* values) {
+    if (!h) return P2G_EINVAL;
+    CU(cudaSetDevice(h->device));
+    REQ(h->have_pattern, P2G_ESTATE, "p2g_prefetch_values: pattern not set");
+    REQ(batch >= 1 && values, P2G_EINVAL, "p2g_prefetch_values: null values");
+    if (!h->cstream) {
+        CU(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&h->pref_ev, cudaEventDisableTiming));
+    }
+    const size_t bytes = (size_t)batch * h->pat.nnz * sizeof(double);
+    if (h->pref_cap < bytes) {
+        CU(cudaEventSynchronize(h->pref_ev));  // an earlier prefetch may still be copying
+        // the solve stream may still read the old buffer (a consumed prefetch)
+        CU(cudaStreamSynchronize(h->stream));
+        dfree(h->d_pref);
+        CU(cudaMalloc(&h->d_pref, bytes));
+        h->pref_cap = bytes;
+    }
+    // d_pref is free: p2g_set_values synchronises its stream after the relayout
+    // of a consumed prefetch, and successive prefetches are ordered on cstream
+    CU(cudaMemcpyAsync(h->d_pref, values, bytes, cudaMemcpyHostToDevice, h->cstream));
+    CU(cudaEventRecord(h->pref_ev, h->cstream));
+    h->pref_host = values;
+    h->pref_B = batch;
+    return P2G_OK;
 }
 
 int p2g_set_values_device(p2g_handle* h, int32_t batch, const double* d_values) {

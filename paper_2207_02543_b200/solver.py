@@ -139,6 +139,15 @@ class BatchSolver:
         self._check(self._L.p2g_set_values(self._h, v.shape[0], _d(v)), "set_values")
         self.B = v.shape[0]
 
+    def prefetch_values(self, values):
+        """p2g_prefetch_values: start the copy of the next batch's values; a
+        later set_values with the SAME array consumes it.  Keep `values`
+        alive and unchanged until then."""
+        if values.dtype != np.float64 or not values.flags.c_contiguous or values.ndim != 2:
+            raise ValueError("prefetch_values: C-contiguous float64 [B][nnz] required")
+        self._check(self._L.p2g_prefetch_values(self._h, values.shape[0], _d(values)),
+                    "prefetch_values")
+
     def set_values_device(self, ptr: int, batch: int):
         self._check(self._L.p2g_set_values_device(self._h, batch, C.c_void_p(ptr)),
                     "set_values_device")

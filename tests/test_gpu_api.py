@@ -155,3 +155,42 @@ def test_run_to_run_bitwise_determinism(gpu):
     assert np.array_equal(out[0][4], out[1][4], equal_nan=True)
     # identical instances in one batch give identical results
     assert np.all(out[0][0] == out[0][0][0])
+
+
+def test_prefetched_values_pipeline(gpu):
+    """p2g_prefetch_values: the next batch's values copied during the current
+    solve, consumed by p2g_set_values with the same buffer -- results equal
+    the direct upload bit for bit; a different buffer is uploaded directly."""
+    g = golden("q4c1.npz")
+    B = 40
+    scale = np.linspace(0.5, 2.0, B)[:, None]
+    V1 = np.ascontiguousarray(np.repeat(g["v"][None, :], B, axis=0) * scale)
+    V2 = np.ascontiguousarray(V1[::-1])
+    F = np.repeat(g["f"][None, :], B, axis=0)
+
+    def run(s, V):
+        s.set_values(V)
+        s.set_basis(g["phi"])
+        s.setup()
+        return s.solve(F, None, 1e-8, 1000, x0_mode=L.X0_REDUCED)
+
+    ref = BatchSolver(0)
+    ref.set_pattern(g["rp"], g["ci"], 2)
+    x1, it1 = run(ref, V1)[:2]
+    x2, it2 = run(ref, V2)[:2]
+    ref.close()
+    s = BatchSolver(0)
+    s.set_pattern(g["rp"], g["ci"], 2)
+    s.prefetch_values(V1)
+    s.set_values(V1)                 # consumes the prefetch
+    s.prefetch_values(V2)            # in flight during the solve of V1
+    s.set_basis(g["phi"])
+    s.setup()
+    y1, jt1 = s.solve(F, None, 1e-8, 1000, x0_mode=L.X0_REDUCED)[:2]
+    y2, jt2 = run(s, V2)[:2]         # consumes the V2 prefetch
+    s.prefetch_values(V1)
+    y3, jt3 = run(s, V2)[:2]         # not the prefetched buffer: direct upload
+    s.close()
+    assert np.array_equal(x1, y1) and np.array_equal(it1, jt1)
+    assert np.array_equal(x2, y2) and np.array_equal(it2, jt2)
+    assert np.array_equal(x2, y3)
