@@ -941,8 +941,17 @@ __global__ void P2G_CLUSTER P2G_ROWK k_gs_backward_blk(Mat A, NodeTab T, const d
 
 // Kp recurrence (D9, see k_kp_update) with node blocking: the L part of all
 // BS rows (lower nodes, then own components < c) of s - s'.
+// Q4 (BS = 2): fewer, fatter warps with 4 neighbour nodes in flight pay here
+// (c2: 96 vs 101 us per iteration); hex8 keeps 4 CTAs/SM (c4: 3.68 vs 4.06 ms)
+#ifndef P2G_KP_MINB
+#define P2G_KP_MINB 2
+#endif
+#ifndef P2G_KP_UNR
+#define P2G_KP_UNR 4
+#endif
 template <class Sh, int BS>
-__global__ void P2G_CLUSTER P2G_ROWK k_kp_update_blk(Mat A, NodeTab T, const double* __restrict__ r,
+__global__ void P2G_CLUSTER
+__launch_bounds__(kBlock, Sh::W == 1 ? P2G_B1_MINB : (BS == 2 ? P2G_KP_MINB : P2G_MINB)) k_kp_update_blk(Mat A, NodeTab T, const double* __restrict__ r,
                                                      const double* __restrict__ s,
                                                      const double* __restrict__ sp,
                                                      double* __restrict__ Kp, double* __restrict__ p,
@@ -971,8 +980,8 @@ __global__ void P2G_CLUSTER P2G_ROWK k_kp_update_blk(Mat A, NodeTab T, const dou
             for (int c = 0; c < BS; ++c)
 #pragma unroll
                 for (int v = 0; v < V; ++v) acc[c][v] = 0.0;
-            blk_pass<Sh, BS, 0, BS, false, true, P2G_BLK_UNR_L>(vb, rl, Bp, s + b0, sp + b0, nc, 0,
-                                                                 (int)pos, acc);
+            blk_pass<Sh, BS, 0, BS, false, true, (BS == 2 ? P2G_KP_UNR : P2G_BLK_UNR_L)>(
+                vb, rl, Bp, s + b0, sp + b0, nc, 0, (int)pos, acc);
             if constexpr (BS > 1) {
                 double xd[BS - 1][V];
 #pragma unroll

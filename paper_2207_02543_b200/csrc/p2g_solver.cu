@@ -331,7 +331,12 @@ struct Run {
     // grid so k_alpha always reduces the same number of partial rows
     static dim3 dot_grid(p2g_handle* h) {
         const dim3 a = node_grid<Sh>(h, nnodes(h), (const void*)k_spmv<Sh, true>, true);
-        const dim3 b = node_grid<Sh>(h, nnodes(h), (const void*)k_kp_update<Sh>, true);
+        const void* kp = (const void*)k_kp_update<Sh>;
+        if constexpr (Sh::S == 1) {
+            if (blk(h)) kp = h->pat.bs == 2 ? (const void*)k_kp_update_blk<Sh, 2>
+                                            : (const void*)k_kp_update_blk<Sh, 3>;
+        }
+        const dim3 b = node_grid<Sh>(h, nnodes(h), kp, true);
         return a.x <= b.x ? a : b;
     }
 

@@ -1,2 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -5 gpurun_out/pytest_gpu.log
-timeout 600 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo bench=$?; cat gpurun_out/bench_c2.json; tail -3 gpurun_out/bench_c2.err
+./tools/ab_variants.sh c2 xp5 2>&1
