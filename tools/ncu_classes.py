@@ -17,13 +17,13 @@ sys.path.insert(0, "tools")
 from ncu_summary import load  # noqa: E402
 
 CLASSES = [
-    ("spmv_dot", r"^(void )?k_(spmv|kp_update)\b"),
+    ("spmv_dot", r"^(void )?k_(spmv|kp_update|kp_update_blk)\b"),
     ("update_presmooth", r"^(void )?k_(update_pre|update_rows|jacobi)\b"),
-    ("gs_forward", r"^(void )?k_gs_forward\b"),
-    ("residual_restrict", r"^(void )?k_(residual|restrict_vec|restrict_tiled|restrict_reg|restrict_mma)\b"),
+    ("gs_forward", r"^(void )?k_gs_forward(_blk)?\b"),
+    ("residual_restrict", r"^(void )?k_(residual|residual_upper_blk|restrict_vec|restrict_tiled|restrict_reg|restrict_mma)\b"),
     ("coarse_solve", r"^(void )?k_coarse\b"),
     ("prolong", r"^(void )?k_prolong(_tiled|_reg|_mma)?\b"),
-    ("gs_backward", r"^(void )?k_gs_backward\b"),
+    ("gs_backward", r"^(void )?k_gs_backward(_blk)?\b"),
     ("scalar_reduce", r"^(void )?k_(alpha|finalize|set_cond|reduce_rows|sum_parts)\b"),
     ("p_update", r"^(void )?k_pupdate\b"),
 ]
