@@ -2,7 +2,8 @@
 p2g_profile_iteration (bench.py's roofline).
 
   full <report.ncu-rep> [--json out]   one --set full capture of
-        `NO_SOLVE=1 python tools/ncu_iter.py c2 2`: the launches from the last
+        `python tools/ncu_iter.py c2 2` (a 3-iteration solve first: profile_iteration
+        needs the Krylov state): the launches from the last
         k_alpha to the end are one Kp-recurrence PCG iteration; prints the
         per-kernel table and writes per_iteration_dram_bytes per class.
   launches <launches.csv> [--json out]  a --metrics gpu__time_duration.sum
@@ -17,15 +18,15 @@ sys.path.insert(0, "tools")
 from ncu_summary import load  # noqa: E402
 
 CLASSES = [
-    ("spmv_dot", r"^(void )?k_(spmv|kp_update|kp_update_blk)\b"),
-    ("update_presmooth", r"^(void )?k_(update_pre|update_rows|jacobi)\b"),
-    ("gs_forward", r"^(void )?k_gs_forward(_blk)?\b"),
-    ("residual_restrict", r"^(void )?k_(residual|residual_upper_blk|restrict_vec|restrict_tiled|restrict_reg|restrict_mma)\b"),
-    ("coarse_solve", r"^(void )?k_coarse\b"),
-    ("prolong", r"^(void )?k_prolong(_tiled|_reg|_mma)?\b"),
-    ("gs_backward", r"^(void )?k_gs_backward(_blk)?\b"),
-    ("scalar_reduce", r"^(void )?k_(alpha|finalize|set_cond|reduce_rows|sum_parts)\b"),
-    ("p_update", r"^(void )?k_pupdate\b"),
+    ("spmv_dot", r"^(void )?(p2g::)?k_(spmv|kp_update|kp_update_blk)\b"),
+    ("update_presmooth", r"^(void )?(p2g::)?k_(update_pre|update_rows|jacobi)\b"),
+    ("gs_forward", r"^(void )?(p2g::)?k_gs_forward(_blk)?\b"),
+    ("residual_restrict", r"^(void )?(p2g::)?k_(residual|residual_upper_blk|restrict_vec|restrict_tiled|restrict_reg|restrict_mma)\b"),
+    ("coarse_solve", r"^(void )?(p2g::)?k_coarse\b"),
+    ("prolong", r"^(void )?(p2g::)?k_prolong(_tiled|_reg|_mma)?\b"),
+    ("gs_backward", r"^(void )?(p2g::)?k_gs_backward(_blk)?\b"),
+    ("scalar_reduce", r"^(void )?(p2g::)?k_(alpha|finalize|set_cond|reduce_rows|sum_parts)\b"),
+    ("p_update", r"^(void )?(p2g::)?k_pupdate\b"),
 ]
 
 
@@ -57,7 +58,7 @@ def load_any(path):
 
 def full(path, out):
     rep = load_any(path)
-    last = max(i for i, d in enumerate(rep) if re.search(r"^(void )?k_alpha\b", d["kernel"]))
+    last = max(i for i, d in enumerate(rep) if re.search(r"^(void )?(p2g::)?k_alpha\b", d["kernel"]))
     it = rep[last:]
     agg = {}
     print("%-60s %9s %9s %9s %7s %6s %5s" % ("kernel (one iteration)", "us", "dram_MB", "GB/s",

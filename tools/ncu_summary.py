@@ -42,10 +42,10 @@ def load(path):
                 except ValueError:
                     x = None
                 if x is not None and k == "us":
-                    x = x / 1000.0 if u == "nsecond" else (x * 1000 if u == "msecond" else x)
+                    x = x / 1000.0 if u in ("nsecond", "ns") else (x * 1000 if u in ("msecond", "ms") else x)
                 if x is not None and k.endswith("_MB"):
-                    x = x / 1e6 if u == "byte" else (x / 1e3 if u == "Kbyte" else
-                                                     (x * 1e3 if u == "Gbyte" else x))
+                    x = x / 1e6 if u in ("byte", "B") else (x / 1e3 if u in ("Kbyte", "KB") else
+                                                            (x * 1e3 if u in ("Gbyte", "GB") else x))
                 d[k] = x
         res.append(d)
     return res
