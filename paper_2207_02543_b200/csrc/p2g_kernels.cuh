@@ -716,6 +716,35 @@ __global__ void P2G_CLUSTER P2G_ROWK k_jacobi(Mat A, const double* __restrict__ 
 // separately rounded operations, so results are bit-identical to the row
 // kernels above (and to the reference's row sums).
 // Used for the one-instance-per-lane shapes (S == 1).
+// Optional read-only (non-coherent) loads for the node-blocked kernels (RO):
+// the values and every x gather are never written by the kernel that reads
+// them (other colours' rows, or a row read by the thread that later
+// overwrites it), so ld.global.nc may be issued ahead of the kernel's own
+// stores.  Measured: it pays only in the Q4 Kp recurrence (c2 93 vs 97 us);
+// the sweeps are unchanged (c2) or slower (c4 forward 3.12 vs 2.93 ms).
+template <int V, bool RO>
+__device__ __forceinline__ void ldv_ro(double (&d)[V], const double* p) {
+    if constexpr (!RO) {
+        ldv<V>(d, p);
+    } else if constexpr (V == 1) {
+        d[0] = __ldg(p);
+    } else {
+        const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+        d[0] = t.x;
+        d[1] = t.y;
+    }
+}
+template <int V, bool RO>
+__device__ __forceinline__ void ldv_vals(double (&d)[V], const double* p) {
+    if constexpr (!RO) {
+        ldv_stream<V>(d, p);
+    } else if constexpr (V == 1) {
+        asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(d[0]) : "l"(p));
+    } else {
+        asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(d[0]), "=d"(d[1]) : "l"(p));
+    }
+}
+
 struct NodeTab {
     const int4* info;  // per node {kb0 = first value of row 0, rowlen, pos = own slot, nnb}
     const int* ncol;   // [nodes][nmax] neighbour node ids, ascending
@@ -738,7 +767,7 @@ __device__ __forceinline__ void node_fetch(const NodeTab& T, int node, int lane,
 // for slots j in [j0, j1), rows c in [C0, C1), cc ascending.  DIFF: the
 // operand is X - X0 (Kp recurrence).  vb = values of row 0 of the node at
 // this lane's instances; nc = the warp's neighbour list in shared memory.
-template <class Sh, int BS, int C0, int C1, bool SUB, bool DIFF, int UNR>
+template <class Sh, int BS, int C0, int C1, bool SUB, bool DIFF, int UNR, bool RO = false>
 __device__ __forceinline__ void blk_pass(const double* vb, unsigned rowlen, unsigned Bp,
                                          const double* X, const double* X0, const int* nc, int j0,
                                          int j1, double (&acc)[BS][Sh::V]) {
@@ -749,10 +778,10 @@ __device__ __forceinline__ void blk_pass(const double* vb, unsigned rowlen, unsi
         double x[BS][V];
 #pragma unroll
         for (int cc = 0; cc < BS; ++cc) {
-            ldv<V>(x[cc], X + xo + cc * Bp);
+            ldv_ro<V, RO>(x[cc], X + xo + cc * Bp);
             if constexpr (DIFF) {
                 double x0[V];
-                ldv<V>(x0, X0 + xo + cc * Bp);
+                ldv_ro<V, RO>(x0, X0 + xo + cc * Bp);
 #pragma unroll
                 for (int v = 0; v < V; ++v) x[cc][v] = __dsub_rn(x[cc][v], x0[v]);
             }
@@ -762,7 +791,7 @@ __device__ __forceinline__ void blk_pass(const double* vb, unsigned rowlen, unsi
 #pragma unroll
             for (int cc = 0; cc < BS; ++cc) {
                 double a[V];
-                ldv_stream<V>(a, vb + ((unsigned)c * rowlen + (unsigned)(j * BS + cc)) * Bp);
+                ldv_vals<V, RO>(a, vb + ((unsigned)c * rowlen + (unsigned)(j * BS + cc)) * Bp);
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
                     const double pr = __dmul_rn(a[v], x[cc][v]);
@@ -784,8 +813,8 @@ __device__ __forceinline__ void blk_pass_row(const double* vr, unsigned Bp, cons
 #pragma unroll
         for (int cc = 0; cc < BS; ++cc) {
             double x[V], a[V];
-            ldv<V>(x, X + xo + cc * Bp);
-            ldv_stream<V>(a, vr + (unsigned)(j * BS + cc) * Bp);
+            ldv_ro<V, false>(x, X + xo + cc * Bp);
+            ldv_vals<V, false>(a, vr + (unsigned)(j * BS + cc) * Bp);
 #pragma unroll
             for (int v = 0; v < V; ++v) acc[v] = __dsub_rn(acc[v], __dmul_rn(a[v], x[v]));
         }
@@ -833,7 +862,7 @@ __global__ void P2G_ROWK k_gs_forward_blk(Mat A, NodeTab T, const double* __rest
             double* sb = s + (size_t)node * BS * Bp + b0;
             double acc[BS][V];
 #pragma unroll
-            for (int c = 0; c < BS; ++c) ldv<V>(acc[c], f + ((size_t)node * BS + c) * Bp + b0);
+            for (int c = 0; c < BS; ++c) ldv_ro<V, false>(acc[c], f + ((size_t)node * BS + c) * Bp + b0);
             blk_pass<Sh, BS, 0, BS, true, false, P2G_BLK_UNR_L>(vb, rl, Bp, s + b0, nullptr, nc, 0,
                                                                 (int)pos, acc);
             double sn[BS][V];
@@ -842,13 +871,13 @@ __global__ void P2G_ROWK k_gs_forward_blk(Mat A, NodeTab T, const double* __rest
 #pragma unroll
                 for (int cc = 0; cc < c; ++cc) {
                     double a[V];
-                    ldv_stream<V>(a, vb + (c * rl + pos * BS + cc) * Bp);
+                    ldv_vals<V, false>(a, vb + (c * rl + pos * BS + cc) * Bp);
 #pragma unroll
                     for (int v = 0; v < V; ++v)
                         acc[c][v] = __dsub_rn(acc[c][v], __dmul_rn(a[v], sn[cc][v]));
                 }
                 double d[V];
-                ldv<V>(d, vb + (c * rl + pos * BS + c) * Bp);
+                ldv_ro<V, false>(d, vb + (c * rl + pos * BS + c) * Bp);
 #pragma unroll
                 for (int v = 0; v < V; ++v) sn[c][v] = __ddiv_rn(acc[c][v], d[v]);
                 stv<V>(sb + c * Bp, sn[c], m);
@@ -887,7 +916,7 @@ __global__ void P2G_CLUSTER P2G_ROWK k_gs_backward_blk(Mat A, NodeTab T, const d
             double acc[BS][V], fi[BS][V];
 #pragma unroll
             for (int c = 0; c < BS; ++c) {
-                ldv<V>(fi[c], f + ro + c * Bp);
+                ldv_ro<V, false>(fi[c], f + ro + c * Bp);
 #pragma unroll
                 for (int v = 0; v < V; ++v) acc[c][v] = fi[c][v];
             }
@@ -897,13 +926,13 @@ __global__ void P2G_CLUSTER P2G_ROWK k_gs_backward_blk(Mat A, NodeTab T, const d
             if constexpr (BS > 1) {
                 double xo[BS - 1][V];
 #pragma unroll
-                for (int cc = 0; cc < BS - 1; ++cc) ldv<V>(xo[cc], xlo + ro + cc * Bp);
+                for (int cc = 0; cc < BS - 1; ++cc) ldv_ro<V, false>(xo[cc], xlo + ro + cc * Bp);
 #pragma unroll
                 for (int c = 1; c < BS; ++c) {
 #pragma unroll
                     for (int cc = 0; cc < c; ++cc) {
                         double a[V];
-                        ldv_stream<V>(a, vb + (c * rl + pos * BS + cc) * Bp);
+                        ldv_vals<V, false>(a, vb + (c * rl + pos * BS + cc) * Bp);
 #pragma unroll
                         for (int v = 0; v < V; ++v)
                             acc[c][v] = __dsub_rn(acc[c][v], __dmul_rn(a[v], xo[cc][v]));
@@ -916,7 +945,7 @@ __global__ void P2G_CLUSTER P2G_ROWK k_gs_backward_blk(Mat A, NodeTab T, const d
 #pragma unroll
                 for (int cc = c + 1; cc < BS; ++cc) {
                     double a[V];
-                    ldv_stream<V>(a, vb + (c * rl + pos * BS + cc) * Bp);
+                    ldv_vals<V, false>(a, vb + (c * rl + pos * BS + cc) * Bp);
 #pragma unroll
                     for (int v = 0; v < V; ++v)
                         acc[c][v] = __dsub_rn(acc[c][v], __dmul_rn(a[v], sn[cc][v]));
@@ -925,7 +954,7 @@ __global__ void P2G_CLUSTER P2G_ROWK k_gs_backward_blk(Mat A, NodeTab T, const d
                 blk_pass_row<Sh, BS, P2G_BLK_UNR_U>(vb + c * rl * Bp, Bp, s + b0, nc, (int)pos + 1,
                                                     nnb, acc[c]);
                 double d[V];
-                ldv<V>(d, vb + (c * rl + pos * BS + c) * Bp);
+                ldv_ro<V, false>(d, vb + (c * rl + pos * BS + c) * Bp);
 #pragma unroll
                 for (int v = 0; v < V; ++v) sn[c][v] = __ddiv_rn(acc[c][v], d[v]);
                 stv<V>(s + ro + c * Bp, sn[c], m);
@@ -958,6 +987,7 @@ __launch_bounds__(kBlock, Sh::W == 1 ? P2G_B1_MINB : (BS == 2 ? P2G_KP_MINB : P2
                                                      const double* beta, const int* active,
                                                      double* part) {
     constexpr int V = Sh::V;
+    constexpr bool KRO = BS == 2;  // read-only loads pay on Q4 only
     LaneGeo<Sh> G;
     const int b0 = blockIdx.y * Sh::T + G.w * V;
     bool m[V], any;
@@ -980,15 +1010,15 @@ __launch_bounds__(kBlock, Sh::W == 1 ? P2G_B1_MINB : (BS == 2 ? P2G_KP_MINB : P2
             for (int c = 0; c < BS; ++c)
 #pragma unroll
                 for (int v = 0; v < V; ++v) acc[c][v] = 0.0;
-            blk_pass<Sh, BS, 0, BS, false, true, (BS == 2 ? P2G_KP_UNR : P2G_BLK_UNR_L)>(
+            blk_pass<Sh, BS, 0, BS, false, true, (BS == 2 ? P2G_KP_UNR : P2G_BLK_UNR_L), KRO>(
                 vb, rl, Bp, s + b0, sp + b0, nc, 0, (int)pos, acc);
             if constexpr (BS > 1) {
                 double xd[BS - 1][V];
 #pragma unroll
                 for (int cc = 0; cc < BS - 1; ++cc) {
                     double x1[V], x0[V];
-                    ldv<V>(x1, s + ro + cc * Bp);
-                    ldv<V>(x0, sp + ro + cc * Bp);
+                    ldv_ro<V, KRO>(x1, s + ro + cc * Bp);
+                    ldv_ro<V, KRO>(x0, sp + ro + cc * Bp);
 #pragma unroll
                     for (int v = 0; v < V; ++v) xd[cc][v] = __dsub_rn(x1[v], x0[v]);
                 }
@@ -997,7 +1027,7 @@ __launch_bounds__(kBlock, Sh::W == 1 ? P2G_B1_MINB : (BS == 2 ? P2G_KP_MINB : P2
 #pragma unroll
                     for (int cc = 0; cc < c; ++cc) {
                         double a[V];
-                        ldv_stream<V>(a, vb + (c * rl + pos * BS + cc) * Bp);
+                        ldv_vals<V, KRO>(a, vb + (c * rl + pos * BS + cc) * Bp);
 #pragma unroll
                         for (int v = 0; v < V; ++v)
                             acc[c][v] = __dadd_rn(acc[c][v], __dmul_rn(a[v], xd[cc][v]));
@@ -1008,10 +1038,10 @@ __launch_bounds__(kBlock, Sh::W == 1 ? P2G_B1_MINB : (BS == 2 ? P2G_KP_MINB : P2
             for (int c = 0; c < BS; ++c) {
                 const size_t o = ro + c * Bp;
                 double ri[V], si[V], kpi[V], pi[V];
-                ldv<V>(ri, r + o);
-                ldv<V>(si, s + o);
-                ldv<V>(kpi, Kp + o);
-                ldv<V>(pi, p + o);
+                ldv_ro<V, KRO>(ri, r + o);
+                ldv_ro<V, KRO>(si, s + o);
+                ldv_ro<V, KRO>(kpi, Kp + o);
+                ldv_ro<V, KRO>(pi, p + o);
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
                     kpi[v] = __dadd_rn(__dadd_rn(ri[v], acc[c][v]), __dmul_rn(bt[v], kpi[v]));
@@ -1053,13 +1083,13 @@ __global__ void P2G_CLUSTER P2G_ROWK k_residual_upper_blk(Mat A, NodeTab T, cons
             if constexpr (BS > 1) {
                 double xo[BS][V];
 #pragma unroll
-                for (int cc = 1; cc < BS; ++cc) ldv<V>(xo[cc], u + ro + cc * Bp);
+                for (int cc = 1; cc < BS; ++cc) ldv_ro<V, false>(xo[cc], u + ro + cc * Bp);
 #pragma unroll
                 for (int c = 0; c < BS - 1; ++c) {
 #pragma unroll
                     for (int cc = c + 1; cc < BS; ++cc) {
                         double a[V];
-                        ldv_stream<V>(a, vb + (c * rl + pos * BS + cc) * Bp);
+                        ldv_vals<V, false>(a, vb + (c * rl + pos * BS + cc) * Bp);
 #pragma unroll
                         for (int v = 0; v < V; ++v)
                             acc[c][v] = __dadd_rn(acc[c][v], __dmul_rn(a[v], xo[cc][v]));

@@ -15,6 +15,7 @@
 #include "p2g_pattern.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 #include <string>
 
@@ -129,7 +130,34 @@ std::string build_coloured_pattern(int64_t n, const uint64_t* rp, const uint64_t
     }
     if (ncol > 64) return "p2g_set_pattern: more than 64 node colours";
 
-    // class coupling: the mean strength of the adjacent node pairs between two
+    // wavefront colouring (experiment: P2G_WAVE_COLOURS=C): colour = level mod C
+    // with level = the node's level in natural-order Gauss-Seidel's dependency
+    // DAG, classes run in level order -- as C grows, natural order.
+    bool wave = false;
+    if (const char* w = std::getenv("P2G_WAVE_COLOURS")) {
+        const int C = std::atoi(w);
+        if (C >= 2 && C <= 64) {
+            std::vector<int64_t> lev(nn, 0);
+            for (int64_t a = 0; a < nn; ++a)
+                for (int64_t q = nadj_off[a]; q < nadj_off[a + 1] && nadj[q] < a; ++q)
+                    lev[a] = std::max(lev[a], lev[nadj[q]] + 1);
+            bool ok = true;
+            for (int64_t a = 0; a < nn && ok; ++a)
+                for (int64_t q = nadj_off[a]; q < nadj_off[a + 1]; ++q)
+                    if (lev[a] % C == lev[nadj[q]] % C) { ok = false; break; }
+            if (ok) {
+                int64_t mx = 0;
+                for (int64_t a = 0; a < nn; ++a) {
+                    color[a] = static_cast<int32_t>(lev[a] % C);
+                    mx = std::max(mx, lev[a]);
+                }
+                ncol = static_cast<int>(std::min<int64_t>(C, mx + 1));
+                wave = true;
+            }
+        }
+    }
+
+    if (!wave)  // class coupling: the mean strength of the adjacent node pairs between two
     // classes, strength = common neighbours (pattern-only: Q4 edge / diagonal
     // neighbours share 4 / 2, hex8 face / edge / corner neighbours 16 / 10 /
     // 6); sampled on large graphs

@@ -1,7 +1,9 @@
-mkdir -p gpurun_out/prof
-nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active --format=csv
-timeout 1500 ncu -f --set full --import-source on --clock-control none --graph-profiling graph --launch-skip 31 --launch-count 15 -o /tmp/iter python tools/ncu_iter.py c2 1 > gpurun_out/prof/ncu_full.log 2>&1; echo full=$?; tail -2 gpurun_out/prof/ncu_full.log
-ls -la /tmp/iter.ncu-rep
-ncu -i /tmp/iter.ncu-rep --page raw --csv | gzip > gpurun_out/prof/iter_raw.csv.gz
-python tools/ncu_sass.py /tmp/iter.ncu-rep k_gs_backward_blk 30 > gpurun_out/prof/sass_bwd.txt 2>&1
-S=$(stat -c %s /tmp/iter.ncu-rep); if [ $S -lt 40000000 ]; then cp /tmp/iter.ncu-rep gpurun_out/prof/; fi
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -3 gpurun_out/pytest_gpu.log
+for C in 0 16; do
+  if [ $C = 0 ]; then unset P2G_WAVE_COLOURS; else export P2G_WAVE_COLOURS=$C; fi
+  echo "== c3 wave $C"
+  timeout 900 python bench.py --config c3 --no-cpu --no-e2e --steps 1 --warmup 1 | python -c "
+import json,sys; d=json.load(sys.stdin); c=d['config']; r=d['roofline']
+print('solves/s %.2f  ms/step %.1f  it mean %.1f max %d  iter_ms %.3f' % (d['value'], d['ms_per_step'], c['iterations_mean'], c['iterations_max'], r['iteration_ms']))
+print({k: round(v['ms']*1e3,1) for k,v in r['classes'].items()})"
+done
