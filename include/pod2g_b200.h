@@ -255,6 +255,14 @@ int p2g_analyze_pattern(int64_t n, const uint64_t* row_offsets, const uint64_t* 
                         int32_t block_size, int64_t* perm, int32_t* ncolors,
                         int64_t* color_offsets, int32_t cap, char* errbuf, int32_t errcap);
 
+/* Host-only: whether the coloured pattern is node-blocked (every node's
+ * block_size rows share one column list of whole neighbour-node blocks, at
+ * most 32 neighbour nodes) -- then the node-blocked kernels run.  *blocked =
+ * 1 / 0, *nmax = most neighbour nodes of a node (0 if not blocked); returns
+ * P2G_OK or P2G_EINVAL for an invalid pattern. */
+int p2g_analyze_node_blocking(int64_t n, const uint64_t* row_offsets, const uint64_t* col_indices,
+                              int32_t block_size, int32_t* blocked, int32_t* nmax);
+
 /* Per-kernel-class timing of the iteration loop: runs `reps` eager
  * iterations (no graph) with CUDA events between kernel classes on the
  * handle's stream, on the current state of the last solve (P2G_ESTATE when

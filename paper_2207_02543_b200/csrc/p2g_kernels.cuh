@@ -1109,6 +1109,231 @@ __global__ void P2G_CLUSTER P2G_ROWK k_residual_upper_blk(Mat A, NodeTab T, cons
     })
 }
 
+// ======================= single-instance node-blocked kernels (B = 1)
+// One warp per node, lane j = neighbour node j (<= 32): the lane gathers its
+// neighbour's BS x values (one contiguous piece) and reads its BS x BS value
+// block, so all of a node's rows are summed in ONE round of loads -- no
+// row-pointer -> column -> gather chain, and one 4-byte node id per BS*BS
+// values instead of a column index per value (B = 1 has no instances to
+// amortise index bytes over).  Each row's off-node terms are combined by a
+// fixed xor tree, then the node's own BS x BS block is applied in order:
+// a rounding-level reassociation, like the slot-split row kernels it
+// replaces (tests: <= 1e-12 per sweep, solves +-1 iteration).
+#ifndef P2G_B1BLK_MINB
+#define P2G_B1BLK_MINB 4  // a whole node's loads in flight per lane need ~60 registers
+#endif
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+// lane's contribution to the BS row sums: node slot j of the node whose
+// values start at vb (row length rl), x of that neighbour from X
+template <int BS>
+__device__ __forceinline__ void b1_terms(const double* vb, int rl, int j, const double* X, int col,
+                                         double (&p)[BS]) {
+    double x[BS];
+#pragma unroll
+    for (int cc = 0; cc < BS; ++cc) x[cc] = __ldg(X + (size_t)col * BS + cc);
+#pragma unroll
+    for (int c = 0; c < BS; ++c)
+#pragma unroll
+        for (int cc = 0; cc < BS; ++cc)
+            p[c] = fma(__ldcs(vb + c * rl + j * BS + cc), x[cc], p[c]);
+}
+
+// node loop (one node per warp) with the next node's table entry prefetched;
+// inf = {kb0, rl, pos, nnb} of `node`, nc = this lane's neighbour id
+#define P2G_B1_NODE_LOOP(T, nb, ne, ...)                                                      \
+    {                                                                                         \
+        const int lane = threadIdx.x & 31;                                                    \
+        const int stride_ = gridDim.x * kWarps;                                               \
+        int node = (nb) + blockIdx.x * kWarps + (threadIdx.x >> 5);                           \
+        int4 inf_n_ = make_int4(0, 0, 0, 0);                                                  \
+        int nc_n_ = 0;                                                                        \
+        if (node < (ne)) node_fetch(T, node, lane, inf_n_, nc_n_);                            \
+        for (; node < (ne); node += stride_) {                                                \
+            const int4 inf = inf_n_;                                                          \
+            const int nc = nc_n_;                                                             \
+            if (node + stride_ < (ne)) node_fetch(T, node + stride_, lane, inf_n_, nc_n_);    \
+            __VA_ARGS__                                                                       \
+        }                                                                                     \
+    }
+
+// the node's own BS x BS block (broadcast loads, issued with the neighbour
+// terms so a node costs one round of loads)
+template <int BS>
+__device__ __forceinline__ void b1_own(const double* vb, int rl, int pos, double (&ob)[BS][BS]) {
+#pragma unroll
+    for (int c = 0; c < BS; ++c)
+#pragma unroll
+        for (int cc = 0; cc < BS; ++cc) ob[c][cc] = __ldg(vb + c * rl + pos * BS + cc);
+}
+
+// forward GS colour phase, first sweep from zero (L part only)
+template <int BS>
+__global__ void __launch_bounds__(kBlock, P2G_B1BLK_MINB)
+    k_gs_forward_b1(Mat A, NodeTab T, const double* __restrict__ f, double* s, const int* active,
+                    int nb, int ne) {
+    if (!active[0]) return;
+    P2G_B1_NODE_LOOP(T, nb, ne, {
+        const double* vb = A.vals + inf.x;
+        const int rl = inf.y, pos = inf.z;
+        double ob[BS][BS], fo[BS], p[BS];
+        b1_own<BS>(vb, rl, pos, ob);
+#pragma unroll
+        for (int c = 0; c < BS; ++c) {
+            fo[c] = __ldg(f + (size_t)node * BS + c);
+            p[c] = 0.0;
+        }
+        if (lane < pos) b1_terms<BS>(vb, rl, lane, s, nc, p);
+#pragma unroll
+        for (int c = 0; c < BS; ++c) p[c] = warp_sum(p[c]);
+        double sn[BS];
+#pragma unroll
+        for (int c = 0; c < BS; ++c) {
+            double acc = fo[c] - p[c];
+#pragma unroll
+            for (int cc = 0; cc < c; ++cc) acc -= ob[c][cc] * sn[cc];
+            sn[c] = acc / ob[c][c];
+        }
+#pragma unroll
+        for (int c = 0; c < BS; ++c)
+            if (lane == c) s[(size_t)node * BS + c] = sn[c];
+    })
+}
+
+// backward GS colour phase: lower neighbours from xlo, upper from s, in one
+// round; own components: below the row from xlo, above it this node's new
+// values.  LAST: r.s partial.
+template <int BS, bool LAST>
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1BLK_MINB)
+    k_gs_backward_b1(Mat A, NodeTab T, const double* __restrict__ f, const double* xlo, double* s,
+                     const int* active, int nb, int ne, double* part_rs, int accumulate) {
+    double rs[1] = {0.0};
+    if (active[0]) {
+        P2G_B1_NODE_LOOP(T, nb, ne, {
+            const double* vb = A.vals + inf.x;
+            const int rl = inf.y, pos = inf.z, nnb = inf.w;
+            double ob[BS][BS], fo[BS], xo[BS], p[BS];
+            b1_own<BS>(vb, rl, pos, ob);
+#pragma unroll
+            for (int c = 0; c < BS; ++c) {
+                fo[c] = __ldg(f + (size_t)node * BS + c);
+                xo[c] = __ldg(xlo + (size_t)node * BS + c);
+                p[c] = 0.0;
+            }
+            if (lane < nnb && lane != pos) b1_terms<BS>(vb, rl, lane, lane < pos ? xlo : s, nc, p);
+#pragma unroll
+            for (int c = 0; c < BS; ++c) p[c] = warp_sum(p[c]);
+            double sn[BS];
+#pragma unroll
+            for (int c = BS - 1; c >= 0; --c) {
+                double acc = fo[c] - p[c];
+#pragma unroll
+                for (int cc = 0; cc < BS; ++cc) {
+                    if (cc == c) continue;
+                    acc -= ob[c][cc] * (cc < c ? xo[cc] : sn[cc]);
+                }
+                sn[c] = acc / ob[c][c];
+            }
+#pragma unroll
+            for (int c = 0; c < BS; ++c) {
+                if (lane == c) s[(size_t)node * BS + c] = sn[c];
+                if (LAST && lane == 0) rs[0] += fo[c] * sn[c];
+            }
+        })
+    }
+    if constexpr (LAST) cluster_partial<ShB1a>(rs, part_rs, A.Bp, accumulate != 0);
+}
+
+// Kp recurrence (D9): Kp = r + L (s - s') + beta Kp, p = s + beta p, pKp
+// partial.  Lane c < BS owns row c's epilogue; its vector loads go out with
+// the neighbour terms (every row is read and written by its owner only).
+template <int BS>
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1BLK_MINB)
+    k_kp_update_b1(Mat A, NodeTab T, const double* __restrict__ r, const double* __restrict__ s,
+                   const double* __restrict__ sp, double* __restrict__ Kp, double* __restrict__ p,
+                   const double* beta, const int* active, double* part) {
+    double dacc[1] = {0.0};
+    if (active[0]) {
+        const double bt = beta[0];
+        const int nn = A.n / BS;
+        P2G_B1_NODE_LOOP(T, 0, nn, {
+            const double* vb = A.vals + inf.x;
+            const int rl = inf.y, pos = inf.z;
+            const int c_own = lane < BS ? lane : 0;
+            const size_t o = (size_t)node * BS + c_own;
+            double ob[BS][BS], xd[BS], q[BS];
+            b1_own<BS>(vb, rl, pos, ob);
+#pragma unroll
+            for (int c = 0; c < BS; ++c) {
+                xd[c] = __ldg(s + (size_t)node * BS + c) - __ldg(sp + (size_t)node * BS + c);
+                q[c] = 0.0;
+            }
+            const double ri = __ldg(r + o), si = __ldg(s + o), kpo = __ldg(Kp + o), po = __ldg(p + o);
+            if (lane < pos) {
+                double x[BS];
+#pragma unroll
+                for (int cc = 0; cc < BS; ++cc)
+                    x[cc] = __ldg(s + (size_t)nc * BS + cc) - __ldg(sp + (size_t)nc * BS + cc);
+#pragma unroll
+                for (int c = 0; c < BS; ++c)
+#pragma unroll
+                    for (int cc = 0; cc < BS; ++cc)
+                        q[c] = fma(__ldcs(vb + c * rl + lane * BS + cc), x[cc], q[c]);
+            }
+#pragma unroll
+            for (int c = 0; c < BS; ++c) q[c] = warp_sum(q[c]);
+#pragma unroll
+            for (int c = 0; c < BS; ++c) {
+                if (lane != c) continue;
+                double acc = q[c];
+#pragma unroll
+                for (int cc = 0; cc < c; ++cc) acc += ob[c][cc] * xd[cc];
+                const double kpi = (ri + acc) + bt * kpo;
+                const double pi = si + bt * po;
+                Kp[o] = kpi;
+                p[o] = pi;
+                dacc[0] += pi * kpi;
+            }
+        })
+    }
+    cluster_partial<ShB1a>(dacc, part, A.Bp, false);
+}
+
+// residual after one forward sweep from zero, t = -U u (D6)
+template <int BS>
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1BLK_MINB)
+    k_residual_upper_b1(Mat A, NodeTab T, const double* __restrict__ u, double* __restrict__ t,
+                        const int* active) {
+    if (!active[0]) return;
+    const int nn = A.n / BS;
+    P2G_B1_NODE_LOOP(T, 0, nn, {
+        const double* vb = A.vals + inf.x;
+        const int rl = inf.y, pos = inf.z, nnb = inf.w;
+        double ob[BS][BS], uo[BS], q[BS];
+        b1_own<BS>(vb, rl, pos, ob);
+#pragma unroll
+        for (int c = 0; c < BS; ++c) {
+            uo[c] = __ldg(u + (size_t)node * BS + c);
+            q[c] = 0.0;
+        }
+        if (lane > pos && lane < nnb) b1_terms<BS>(vb, rl, lane, u, nc, q);
+#pragma unroll
+        for (int c = 0; c < BS; ++c) q[c] = warp_sum(q[c]);
+#pragma unroll
+        for (int c = 0; c < BS; ++c) {
+            if (lane != c) continue;
+            double acc = 0.0;
+#pragma unroll
+            for (int cc = c + 1; cc < BS; ++cc) acc += ob[c][cc] * uo[cc];
+            t[(size_t)node * BS + c] = -(acc + q[c]);
+        }
+    })
+}
+
 // Restriction c = Phi^T t (PodBasis::project, pod.hpp:27-35) of a vector
 // t[n][Bp] (the residual, or f itself for reduced_solve, pod.hpp:171).
 // Lanes: R = 32/W rows x W instance lanes x V instances; each lane keeps the

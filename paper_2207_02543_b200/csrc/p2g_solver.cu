@@ -318,6 +318,21 @@ struct Run {
     // node-blocked kernels: one-instance-per-lane shapes on node-blocked patterns
     static bool blk(const p2g_handle* h) { return Sh::S == 1 && h->node_blk; }
     static NodeTab ntab(const p2g_handle* h) { return NodeTab{h->d_ninfo, h->d_ncol, h->nmax}; }
+    // single-instance node-blocked kernels (one warp per node)
+    static bool blk1(const p2g_handle* h) {
+        return Sh::W == 1 && h->node_blk && !std::getenv("P2G_NO_NODEBLK1");
+    }
+    // the half-pass kernels (Kp recurrence, upper residual) leave most lanes
+    // idle on hex8 (one lane per lower / upper neighbour): row kernels there
+    // (128^3: 1.26 vs 2.05 ms and 1.33 vs 1.85 ms); blocked on Q4
+    static bool blk1_half(const p2g_handle* h) { return blk1(h) && h->pat.bs == 2; }
+    static dim3 blk1_grid(p2g_handle* h, int64_t nodes, const void* fn, bool cluster) {
+        const int64_t need = (nodes + kWarps - 1) / kWarps;
+        int64_t gx = std::min<int64_t>(need, resident_ctas(h, fn, cluster));
+        gx = std::min<int64_t>(std::max<int64_t>(gx, 1), h->nb_cap);
+        if (cluster) gx = (gx + kCluster - 1) / kCluster * kCluster;
+        return dim3(static_cast<unsigned>(gx), 1);
+    }
 #define P2G_BS_SWITCH(bs, ...)          \
     if ((bs) == 2) {                    \
         constexpr int BS = 2;           \
@@ -335,6 +350,13 @@ struct Run {
         if constexpr (Sh::S == 1) {
             if (blk(h)) kp = h->pat.bs == 2 ? (const void*)k_kp_update_blk<Sh, 2>
                                             : (const void*)k_kp_update_blk<Sh, 3>;
+        }
+        if constexpr (Sh::W == 1) {
+            if (blk1_half(h)) {
+                kp = h->pat.bs == 2 ? (const void*)k_kp_update_b1<2> : (const void*)k_kp_update_b1<3>;
+                const dim3 b1 = blk1_grid(h, nnodes(h), kp, true);
+                return a.x <= b1.x ? a : b1;
+            }
         }
         const dim3 b = node_grid<Sh>(h, nnodes(h), kp, true);
         return a.x <= b.x ? a : b;
@@ -420,6 +442,18 @@ struct Run {
         const int nb = static_cast<int>(h->pat.color_rows[c] / h->pat.bs);
         const int ne = static_cast<int>(h->pat.color_rows[c + 1] / h->pat.bs);
         if (ne <= nb) return P2G_OK;
+        if constexpr (Sh::W == 1) {
+            if (first && blk1(h)) {
+                P2G_BS_SWITCH(h->pat.bs, {
+                    auto fn = k_gs_forward_b1<BS>;
+                    dim3 g = blk1_grid(h, ne - nb, (const void*)fn, false);
+                    fn<<<g, kBlock, 0, h->stream>>>(A, ntab(h), f, s, h->d_active, nb, ne);
+                })
+                count_launch(h, KC_FWD);
+                CU(cudaGetLastError());
+                return P2G_OK;
+            }
+        }
         if constexpr (Sh::S == 1) {
             if (first && blk(h)) {
                 P2G_BS_SWITCH(h->pat.bs, {
@@ -457,6 +491,21 @@ struct Run {
         int64_t maxc = 1;
         for (int q = 0; q < h->pat.ncolors; ++q)
             maxc = std::max<int64_t>(maxc, (h->pat.color_rows[q + 1] - h->pat.color_rows[q]) / h->pat.bs);
+        if constexpr (Sh::W == 1) {
+            if (blk1(h)) {
+                P2G_BS_SWITCH(h->pat.bs, {
+                    auto fn = last ? k_gs_backward_b1<BS, true> : k_gs_backward_b1<BS, false>;
+                    dim3 g = blk1_grid(h, maxc, (const void*)fn, true);
+                    fn<<<g, kBlock, 0, h->stream>>>(A, ntab(h), f, xlo, s, h->d_active, nb, ne,
+                                                    last ? h->d_part_rs : nullptr,
+                                                    first_phase ? 0 : 1);
+                    if (last) *rs_rows = g.x / kCluster;
+                })
+                count_launch(h, KC_BWD);
+                CU(cudaGetLastError());
+                return P2G_OK;
+            }
+        }
         if constexpr (Sh::S == 1) {
             if (blk(h)) {
                 P2G_BS_SWITCH(h->pat.bs, {
@@ -499,6 +548,16 @@ struct Run {
         Mat A = mat_of(h);
         dim3 g = dot_grid(h);
         bool done = false;
+        if constexpr (Sh::W == 1) {
+            if (blk1_half(h)) {
+                P2G_BS_SWITCH(h->pat.bs, {
+                    k_kp_update_b1<BS><<<g, kBlock, 0, h->stream>>>(
+                        A, ntab(h), h->d_r, s_new, s_prol, h->d_Kp, h->d_p, h->d_beta, h->d_active,
+                        h->d_part_dot);
+                })
+                done = true;
+            }
+        }
         if constexpr (Sh::S == 1) {
             if (blk(h)) {
                 P2G_BS_SWITCH(h->pat.bs, {
@@ -547,6 +606,16 @@ struct Run {
         if (form != RES_VECTOR) {
             double* tb = h->d_t;
             bool done = false;
+            if constexpr (Sh::W == 1) {
+                if (form == RES_UPPER && blk1_half(h)) {
+                    P2G_BS_SWITCH(h->pat.bs, {
+                        auto fn = k_residual_upper_b1<BS>;
+                        dim3 g = blk1_grid(h, nnodes(h), (const void*)fn, true);
+                        fn<<<g, kBlock, 0, h->stream>>>(A, ntab(h), s, tb, h->d_active);
+                    })
+                    done = true;
+                }
+            }
             if constexpr (Sh::S == 1) {
                 if (form == RES_UPPER && blk(h) && h->pat.bs == 2) {  // hex8: row kernel faster
                     P2G_BS_SWITCH(h->pat.bs, {
@@ -1840,6 +1909,19 @@ int p2g_analyze_pattern(int64_t n, const uint64_t* row_offsets, const uint64_t* 
     if (ncolors) *ncolors = pat.ncolors;
     if (color_offsets)
         for (int c = 0; c <= pat.ncolors && c < cap; ++c) color_offsets[c] = pat.color_rows[c];
+    return P2G_OK;
+}
+
+int p2g_analyze_node_blocking(int64_t n, const uint64_t* row_offsets, const uint64_t* col_indices,
+                              int32_t block_size, int32_t* blocked, int32_t* nmax) {
+    ColouredPattern pat;
+    if (!build_coloured_pattern(n, row_offsets, col_indices, block_size, pat).empty())
+        return P2G_EINVAL;
+    std::vector<int32_t> info, ncol;
+    int nm = 0;
+    const bool ok = build_node_table(pat.n, pat.bs, pat.rp, pat.ci, pat.dpos, info, ncol, nm);
+    if (blocked) *blocked = ok ? 1 : 0;
+    if (nmax) *nmax = ok ? nm : 0;
     return P2G_OK;
 }
 

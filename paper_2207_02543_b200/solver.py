@@ -328,6 +328,21 @@ def analyze_pattern(row_offsets, col_indices, block_size=1):
     return perm, offs[: nc.value + 1]
 
 
+def analyze_node_blocking(row_offsets, col_indices, block_size):
+    """Host-only: (node-blocked?, most neighbour nodes of a node) -- whether
+    the node-blocked kernels run for this pattern (p2g_analyze_node_blocking)."""
+    lib = L.lib()
+    rp = np.ascontiguousarray(row_offsets, dtype=np.uint64)
+    ci = np.ascontiguousarray(col_indices, dtype=np.uint64)
+    nm, bl = C.c_int32(), C.c_int32()
+    st = lib.p2g_analyze_node_blocking(len(rp) - 1, rp.ctypes.data_as(L.U64),
+                                       ci.ctypes.data_as(L.U64), block_size, C.byref(bl),
+                                       C.byref(nm))
+    if st != L.OK:
+        _raise(st, "p2g_analyze_node_blocking: invalid pattern")
+    return bool(bl.value), int(nm.value)
+
+
 # ---------------------------------------------------------------------------
 # Reference-shaped single-instance API
 class Preconditioner:

@@ -386,3 +386,34 @@ def test_node_blocked_kernels_bit_identical_to_row_kernels(gpu, monkeypatch, dim
     assert np.all(st1 == 0) and np.all(st0 == 0)
     assert np.all(np.abs(it1 - it0) <= 1)
     assert np.linalg.norm(x1 - x0) <= 1e-10 * np.linalg.norm(x0)
+
+
+@pytest.mark.parametrize("dims", [2, 3])
+def test_single_instance_node_blocked_kernels(gpu, monkeypatch, dims):
+    """B = 1 node-blocked kernels (one warp per node, lane = neighbour node)
+    against the slot-split row kernels (P2G_NO_NODEBLK1=1) and the oracle:
+    both reassociate the row sums, so the bar is 1e-12 per preconditioner
+    application and +-1 iteration; the solve also matches the oracle."""
+    if dims == 2:
+        m, rp, ci, f, V, phi = small_problem(B=1, k=10, nx=32, ny=16)
+    else:
+        m, rp, ci, f, V, phi = small_problem(dim=3, nx=6, ny=6, nz=6, Lx=1, Ly=1, Lz=1, B=1, k=8)
+    R = np.random.default_rng(12).standard_normal((1, m.n))
+    F = f[None, :].copy()
+    out = []
+    for off in (False, True):
+        if off:
+            monkeypatch.setenv("P2G_NO_NODEBLK1", "1")
+        s = make_solver(m, rp, ci, V, phi)
+        S = s.precond_apply(R)
+        x, it, conv, status, hist = s.solve(F, None, 1e-8, 2000, x0_mode=L.X0_REDUCED)
+        if not off:
+            perm, prp, pci, pV, pf, pphi = perm_system(s, rp, ci, V, f, phi)
+        out.append((S, x, it, status, hist))
+        s.close()
+    (S1, x1, it1, st1, h1), (S0, x0, it0, st0, h0) = out
+    assert np.linalg.norm(S1 - S0) <= 1e-12 * np.linalg.norm(S0)
+    assert st1[0] == 0 and st0[0] == 0 and abs(int(it1[0]) - int(it0[0])) <= 1
+    x0_ref, _, _ = ORC.reduced_solve(prp, pci, pV[0], pf, pphi)
+    ref = ORC.pcg_pod2g(prp, pci, pV[0], pf, pphi, x0_ref, 1e-8, 2000)
+    _check_solve(x1[0], it1[0], True, st1[0], h1[0], None, ref, 1e-8)

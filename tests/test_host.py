@@ -13,7 +13,7 @@ import scipy.sparse as sp
 
 from paper_2207_02543_b200 import _lib as L
 from paper_2207_02543_b200 import problems as PR
-from paper_2207_02543_b200.solver import analyze_pattern
+from paper_2207_02543_b200.solver import analyze_node_blocking, analyze_pattern
 from tests.helpers import from_scipy, laplacian_2d, to_scipy
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -214,3 +214,41 @@ def test_shard_weak_and_strong():
     parts = [PR.shard(c3, 8, r) for r in range(8)]
     assert all(p[2] for p in parts) and sum(p[0] for p in parts) == 256
     assert np.array_equal(np.concatenate([p[1] for p in parts]), PR.query_seeds(c3))
+
+
+@pytest.mark.parametrize("dims,nmax", [((2, 16, 8, 1), 9), ((3, 4, 4, 4), 27)])
+def test_node_blocking_detected_on_fem_patterns(dims, nmax):
+    """FEM vector patterns are node-blocked (the node-blocked kernels run),
+    with 9 (Q4) / 27 (hex8) neighbour nodes at most."""
+    dim, nx, ny, nz = dims
+    m = PR.Mesh(dim, nx, ny, nz, 2.0 if dim == 2 else 1.0, 1.0, 1.0)
+    rp, ci = m.pattern()
+    ok, nm = analyze_node_blocking(rp, ci, m.block_size)
+    assert ok and nm == nmax
+    # as a point pattern (block size 1) every row is its own node: Q4 rows hold
+    # 18 entries (blocked), hex8 rows 81 (> 32 neighbours: row kernels)
+    ok1, nm1 = analyze_node_blocking(rp, ci, 1)
+    assert (ok1, nm1) == ((True, 18) if dim == 2 else (False, 0))
+
+
+def test_node_blocking_rejects_unequal_node_rows():
+    """A node whose rows hold different column sets falls back to the row
+    kernels (the pattern is still valid)."""
+    m = PR.Mesh(2, 8, 4, 1, 2.0, 1.0, 1.0)
+    rp, ci = m.pattern()
+    rp = rp.astype(np.int64)
+    ci = ci.astype(np.int64)
+    # drop the symmetric pair (row 0, col j) / (row j, col 0) for one off-node column j
+    j = int(ci[rp[0]:rp[1]][-1])
+    assert j // 2 != 0
+    keep = np.ones(len(ci), dtype=bool)
+    keep[rp[0] + np.where(ci[rp[0]:rp[1]] == j)[0][0]] = False
+    keep[rp[j] + np.where(ci[rp[j]:rp[j + 1]] == 0)[0][0]] = False
+    counts = np.diff(rp) - np.add.reduceat(~keep, rp[:-1])
+    rp2 = np.concatenate([[0], np.cumsum(counts)]).astype(np.uint64)
+    ci2 = ci[keep].astype(np.uint64)
+    analyze_pattern(rp2, ci2, 2)  # valid, colourable
+    ok, _ = analyze_node_blocking(rp2, ci2, 2)
+    assert not ok
+    with pytest.raises(ValueError):
+        analyze_node_blocking(rp2, ci2[::-1].copy(), 2)
