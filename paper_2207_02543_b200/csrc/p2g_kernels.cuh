@@ -1334,6 +1334,135 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1BLK_MINB)
     })
 }
 
+// Half-pass kernels for wide nodes (hex8: up to 26 lower or upper neighbour
+// nodes): TWO nodes per warp, one per 16-lane half, lane l of a half taking
+// neighbour slots l and l + 16 -- twice the busy lanes of one node per warp
+// when only the lower (or upper) neighbours take part.
+__device__ __forceinline__ double half_sum(double x) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+#define P2G_B1H_NODE_LOOP(T, nn, ...)                                                          \
+    {                                                                                          \
+        const int lane = threadIdx.x & 31, hl = lane & 15;                                     \
+        const int stride_ = gridDim.x * kWarps * 2;                                            \
+        for (int base_ = (blockIdx.x * kWarps + (threadIdx.x >> 5)) * 2; base_ < (nn);         \
+             base_ += stride_) {                                                               \
+            const int node = base_ + (lane >> 4);                                              \
+            const bool valid = node < (nn);                                                    \
+            int4 inf = make_int4(0, 0, 0, 0);                                                  \
+            int nc0 = 0, nc1 = 0;                                                              \
+            if (valid) {                                                                       \
+                inf = __ldg(T.info + node);                                                    \
+                const int* nl = T.ncol + (size_t)node * T.nmax;                                \
+                if (hl < T.nmax) nc0 = __ldg(nl + hl);                                         \
+                if (hl + 16 < T.nmax) nc1 = __ldg(nl + hl + 16);                               \
+            }                                                                                  \
+            __VA_ARGS__                                                                        \
+        }                                                                                      \
+    }
+
+template <int BS>
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1BLK_MINB)
+    k_kp_update_b1h(Mat A, NodeTab T, const double* __restrict__ r, const double* __restrict__ s,
+                    const double* __restrict__ sp, double* __restrict__ Kp, double* __restrict__ p,
+                    const double* beta, const int* active, double* part) {
+    double dacc[1] = {0.0};
+    if (active[0]) {
+        const double bt = beta[0];
+        const int nn = A.n / BS;
+        P2G_B1H_NODE_LOOP(T, nn, {
+            const double* vb = A.vals + inf.x;
+            const int rl = inf.y, pos = inf.z;
+            double ob[BS][BS], xd[BS], q[BS];
+            const int c_own = hl < BS ? hl : 0;
+            const size_t o = (size_t)node * BS + c_own;
+            double ri = 0, si = 0, kpo = 0, po = 0;
+#pragma unroll
+            for (int c = 0; c < BS; ++c) q[c] = 0.0;
+            if (valid) {
+                b1_own<BS>(vb, rl, pos, ob);
+#pragma unroll
+                for (int c = 0; c < BS; ++c)
+                    xd[c] = __ldg(s + (size_t)node * BS + c) - __ldg(sp + (size_t)node * BS + c);
+                ri = __ldg(r + o), si = __ldg(s + o), kpo = __ldg(Kp + o), po = __ldg(p + o);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int j = hl + 16 * h;
+                    if (j < pos) {
+                        const int col = h ? nc1 : nc0;
+                        double x[BS];
+#pragma unroll
+                        for (int cc = 0; cc < BS; ++cc)
+                            x[cc] = __ldg(s + (size_t)col * BS + cc) - __ldg(sp + (size_t)col * BS + cc);
+#pragma unroll
+                        for (int c = 0; c < BS; ++c)
+#pragma unroll
+                            for (int cc = 0; cc < BS; ++cc)
+                                q[c] = fma(__ldcs(vb + c * rl + j * BS + cc), x[cc], q[c]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < BS; ++c) q[c] = half_sum(q[c]);
+            if (valid) {
+#pragma unroll
+                for (int c = 0; c < BS; ++c) {
+                    if (hl != c) continue;
+                    double acc = q[c];
+#pragma unroll
+                    for (int cc = 0; cc < c; ++cc) acc += ob[c][cc] * xd[cc];
+                    const double kpi = (ri + acc) + bt * kpo;
+                    const double pi = si + bt * po;
+                    Kp[o] = kpi;
+                    p[o] = pi;
+                    dacc[0] += pi * kpi;
+                }
+            }
+        })
+    }
+    cluster_partial<ShB1a>(dacc, part, A.Bp, false);
+}
+
+template <int BS>
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1BLK_MINB)
+    k_residual_upper_b1h(Mat A, NodeTab T, const double* __restrict__ u, double* __restrict__ t,
+                         const int* active) {
+    if (!active[0]) return;
+    const int nn = A.n / BS;
+    P2G_B1H_NODE_LOOP(T, nn, {
+        const double* vb = A.vals + inf.x;
+        const int rl = inf.y, pos = inf.z, nnb = inf.w;
+        double ob[BS][BS], uo[BS], q[BS];
+#pragma unroll
+        for (int c = 0; c < BS; ++c) q[c] = 0.0;
+        if (valid) {
+            b1_own<BS>(vb, rl, pos, ob);
+#pragma unroll
+            for (int c = 0; c < BS; ++c) uo[c] = __ldg(u + (size_t)node * BS + c);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = hl + 16 * h;
+                if (j > pos && j < nnb) b1_terms<BS>(vb, rl, j, u, h ? nc1 : nc0, q);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < BS; ++c) q[c] = half_sum(q[c]);
+        if (valid) {
+#pragma unroll
+            for (int c = 0; c < BS; ++c) {
+                if (hl != c) continue;
+                double acc = 0.0;
+#pragma unroll
+                for (int cc = c + 1; cc < BS; ++cc) acc += ob[c][cc] * uo[cc];
+                t[(size_t)node * BS + c] = -(acc + q[c]);
+            }
+        }
+    })
+}
+
 // Restriction c = Phi^T t (PodBasis::project, pod.hpp:27-35) of a vector
 // t[n][Bp] (the residual, or f itself for reduced_solve, pod.hpp:171).
 // Lanes: R = 32/W rows x W instance lanes x V instances; each lane keeps the

@@ -326,6 +326,10 @@ struct Run {
     // idle on hex8 (one lane per lower / upper neighbour): row kernels there
     // (128^3: 1.26 vs 2.05 ms and 1.33 vs 1.85 ms); blocked on Q4
     static bool blk1_half(const p2g_handle* h) { return blk1(h) && h->pat.bs == 2; }
+    // hex8: two nodes per warp (16-lane halves) for the half passes
+    static bool blk1_hw(const p2g_handle* h) {
+        return blk1(h) && h->pat.bs == 3 && !std::getenv("P2G_NO_B1H");
+    }
     static dim3 blk1_grid(p2g_handle* h, int64_t nodes, const void* fn, bool cluster) {
         const int64_t need = (nodes + kWarps - 1) / kWarps;
         int64_t gx = std::min<int64_t>(need, resident_ctas(h, fn, cluster));
@@ -352,6 +356,11 @@ struct Run {
                                             : (const void*)k_kp_update_blk<Sh, 3>;
         }
         if constexpr (Sh::W == 1) {
+            if (blk1_hw(h)) {
+                kp = (const void*)k_kp_update_b1h<3>;
+                const dim3 b1 = blk1_grid(h, (nnodes(h) + 1) / 2, kp, true);
+                return a.x <= b1.x ? a : b1;
+            }
             if (blk1_half(h)) {
                 kp = h->pat.bs == 2 ? (const void*)k_kp_update_b1<2> : (const void*)k_kp_update_b1<3>;
                 const dim3 b1 = blk1_grid(h, nnodes(h), kp, true);
@@ -549,7 +558,12 @@ struct Run {
         dim3 g = dot_grid(h);
         bool done = false;
         if constexpr (Sh::W == 1) {
-            if (blk1_half(h)) {
+            if (blk1_hw(h)) {
+                k_kp_update_b1h<3><<<g, kBlock, 0, h->stream>>>(A, ntab(h), h->d_r, s_new, s_prol,
+                                                                 h->d_Kp, h->d_p, h->d_beta,
+                                                                 h->d_active, h->d_part_dot);
+                done = true;
+            } else if (blk1_half(h)) {
                 P2G_BS_SWITCH(h->pat.bs, {
                     k_kp_update_b1<BS><<<g, kBlock, 0, h->stream>>>(
                         A, ntab(h), h->d_r, s_new, s_prol, h->d_Kp, h->d_p, h->d_beta, h->d_active,
@@ -607,7 +621,12 @@ struct Run {
             double* tb = h->d_t;
             bool done = false;
             if constexpr (Sh::W == 1) {
-                if (form == RES_UPPER && blk1_half(h)) {
+                if (form == RES_UPPER && blk1_hw(h)) {
+                    auto fn = k_residual_upper_b1h<3>;
+                    dim3 g = blk1_grid(h, (nnodes(h) + 1) / 2, (const void*)fn, true);
+                    fn<<<g, kBlock, 0, h->stream>>>(A, ntab(h), s, tb, h->d_active);
+                    done = true;
+                } else if (form == RES_UPPER && blk1_half(h)) {
                     P2G_BS_SWITCH(h->pat.bs, {
                         auto fn = k_residual_upper_b1<BS>;
                         dim3 g = blk1_grid(h, nnodes(h), (const void*)fn, true);

@@ -1,4 +1,1 @@
-for i in 1 2; do timeout 300 python bench.py --config c1 --no-cpu --steps 5 | python -c "
-import json,sys; d=json.load(sys.stdin); print('blk', d['value'], d['e2e']['value'])"; done
-P2G_NO_NODEBLK1=1 timeout 300 python bench.py --config c1 --no-cpu --steps 5 | python -c "
-import json,sys; d=json.load(sys.stdin); print('row', d['value'], d['e2e']['value'])"
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -3 gpurun_out/pytest_gpu.log; grep -E "FAIL|Error" gpurun_out/pytest_gpu.log | head
