@@ -1344,14 +1344,14 @@ __device__ __forceinline__ double half_sum(double x) {
     return x;
 }
 
-#define P2G_B1H_NODE_LOOP(T, nn, ...)                                                          \
+#define P2G_B1H_NODE_LOOP(T, nb, ne, ...)                                                      \
     {                                                                                          \
         const int lane = threadIdx.x & 31, hl = lane & 15;                                     \
         const int stride_ = gridDim.x * kWarps * 2;                                            \
-        for (int base_ = (blockIdx.x * kWarps + (threadIdx.x >> 5)) * 2; base_ < (nn);         \
+        for (int base_ = (nb) + (blockIdx.x * kWarps + (threadIdx.x >> 5)) * 2; base_ < (ne);  \
              base_ += stride_) {                                                               \
             const int node = base_ + (lane >> 4);                                              \
-            const bool valid = node < (nn);                                                    \
+            const bool valid = node < (ne);                                                    \
             int4 inf = make_int4(0, 0, 0, 0);                                                  \
             int nc0 = 0, nc1 = 0;                                                              \
             if (valid) {                                                                       \
@@ -1364,6 +1364,98 @@ __device__ __forceinline__ double half_sum(double x) {
         }                                                                                      \
     }
 
+// forward sweep from zero, hex8, two nodes per warp (lower neighbours only)
+template <int BS>
+__global__ void __launch_bounds__(kBlock, P2G_B1BLK_MINB)
+    k_gs_forward_b1h(Mat A, NodeTab T, const double* __restrict__ f, double* s, const int* active,
+                     int nb, int ne) {
+    if (!active[0]) return;
+    P2G_B1H_NODE_LOOP(T, nb, ne, {
+        const int nd = node;
+        double ob[BS][BS], fo[BS], q[BS];
+#pragma unroll
+        for (int c = 0; c < BS; ++c) q[c] = 0.0;
+        const double* vb = A.vals + inf.x;
+        const int rl = inf.y, pos = inf.z;
+        if (valid) {
+            b1_own<BS>(vb, rl, pos, ob);
+#pragma unroll
+            for (int c = 0; c < BS; ++c) fo[c] = __ldg(f + (size_t)nd * BS + c);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = hl + 16 * h;
+                if (j < pos) b1_terms<BS>(vb, rl, j, s, h ? nc1 : nc0, q);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < BS; ++c) q[c] = half_sum(q[c]);
+        if (valid) {
+            double sn[BS];
+#pragma unroll
+            for (int c = 0; c < BS; ++c) {
+                double acc = fo[c] - q[c];
+#pragma unroll
+                for (int cc = 0; cc < c; ++cc) acc -= ob[c][cc] * sn[cc];
+                sn[c] = acc / ob[c][c];
+            }
+#pragma unroll
+            for (int c = 0; c < BS; ++c)
+                if (hl == c) s[(size_t)nd * BS + c] = sn[c];
+        }
+    })
+}
+
+// backward sweep, hex8, two nodes per warp (every neighbour: slots l, l + 16)
+template <int BS, bool LAST>
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1BLK_MINB)
+    k_gs_backward_b1h(Mat A, NodeTab T, const double* __restrict__ f, const double* xlo, double* s,
+                      const int* active, int nb, int ne, double* part_rs, int accumulate) {
+    double rs[1] = {0.0};
+    if (active[0]) {
+        P2G_B1H_NODE_LOOP(T, nb, ne, {
+            const double* vb = A.vals + inf.x;
+            const int rl = inf.y, pos = inf.z, nnb = inf.w;
+            double ob[BS][BS], fo[BS], xo[BS], q[BS];
+#pragma unroll
+            for (int c = 0; c < BS; ++c) q[c] = 0.0;
+            if (valid) {
+                b1_own<BS>(vb, rl, pos, ob);
+#pragma unroll
+                for (int c = 0; c < BS; ++c) {
+                    fo[c] = __ldg(f + (size_t)node * BS + c);
+                    xo[c] = __ldg(xlo + (size_t)node * BS + c);
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int j = hl + 16 * h;
+                    if (j < nnb && j != pos) b1_terms<BS>(vb, rl, j, j < pos ? xlo : s, h ? nc1 : nc0, q);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < BS; ++c) q[c] = half_sum(q[c]);
+            if (valid) {
+                double sn[BS];
+#pragma unroll
+                for (int c = BS - 1; c >= 0; --c) {
+                    double acc = fo[c] - q[c];
+#pragma unroll
+                    for (int cc = 0; cc < BS; ++cc) {
+                        if (cc == c) continue;
+                        acc -= ob[c][cc] * (cc < c ? xo[cc] : sn[cc]);
+                    }
+                    sn[c] = acc / ob[c][c];
+                }
+#pragma unroll
+                for (int c = 0; c < BS; ++c) {
+                    if (hl == c) s[(size_t)node * BS + c] = sn[c];
+                    if (LAST && hl == 0) rs[0] += fo[c] * sn[c];
+                }
+            }
+        })
+    }
+    if constexpr (LAST) cluster_partial<ShB1a>(rs, part_rs, A.Bp, accumulate != 0);
+}
+
 template <int BS>
 __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1BLK_MINB)
     k_kp_update_b1h(Mat A, NodeTab T, const double* __restrict__ r, const double* __restrict__ s,
@@ -1373,7 +1465,7 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1BLK_MINB)
     if (active[0]) {
         const double bt = beta[0];
         const int nn = A.n / BS;
-        P2G_B1H_NODE_LOOP(T, nn, {
+        P2G_B1H_NODE_LOOP(T, 0, nn, {
             const double* vb = A.vals + inf.x;
             const int rl = inf.y, pos = inf.z;
             double ob[BS][BS], xd[BS], q[BS];
@@ -1432,7 +1524,7 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1BLK_MINB)
                          const int* active) {
     if (!active[0]) return;
     const int nn = A.n / BS;
-    P2G_B1H_NODE_LOOP(T, nn, {
+    P2G_B1H_NODE_LOOP(T, 0, nn, {
         const double* vb = A.vals + inf.x;
         const int rl = inf.y, pos = inf.z, nnb = inf.w;
         double ob[BS][BS], uo[BS], q[BS];

@@ -452,6 +452,14 @@ struct Run {
         const int ne = static_cast<int>(h->pat.color_rows[c + 1] / h->pat.bs);
         if (ne <= nb) return P2G_OK;
         if constexpr (Sh::W == 1) {
+            if (first && blk1_hw(h)) {
+                auto fn = k_gs_forward_b1h<3>;
+                dim3 g = blk1_grid(h, (ne - nb + 1) / 2, (const void*)fn, false);
+                fn<<<g, kBlock, 0, h->stream>>>(A, ntab(h), f, s, h->d_active, nb, ne);
+                count_launch(h, KC_FWD);
+                CU(cudaGetLastError());
+                return P2G_OK;
+            }
             if (first && blk1(h)) {
                 P2G_BS_SWITCH(h->pat.bs, {
                     auto fn = k_gs_forward_b1<BS>;
@@ -501,6 +509,16 @@ struct Run {
         for (int q = 0; q < h->pat.ncolors; ++q)
             maxc = std::max<int64_t>(maxc, (h->pat.color_rows[q + 1] - h->pat.color_rows[q]) / h->pat.bs);
         if constexpr (Sh::W == 1) {
+            if (blk1_hw(h) && !std::getenv("P2G_NO_B1H_BWD")) {
+                auto fn = last ? k_gs_backward_b1h<3, true> : k_gs_backward_b1h<3, false>;
+                dim3 g = blk1_grid(h, (maxc + 1) / 2, (const void*)fn, true);
+                fn<<<g, kBlock, 0, h->stream>>>(A, ntab(h), f, xlo, s, h->d_active, nb, ne,
+                                                last ? h->d_part_rs : nullptr, first_phase ? 0 : 1);
+                if (last) *rs_rows = g.x / kCluster;
+                count_launch(h, KC_BWD);
+                CU(cudaGetLastError());
+                return P2G_OK;
+            }
             if (blk1(h)) {
                 P2G_BS_SWITCH(h->pat.bs, {
                     auto fn = last ? k_gs_backward_b1<BS, true> : k_gs_backward_b1<BS, false>;
