@@ -148,6 +148,13 @@ def cpu_reference_run(prob, values, F, instances, jobs):
     return dt, it
 
 
+def workload_name(cfg):
+    """the config's workload label, shared by both arms"""
+    if cfg.dim == 2:
+        return f"{cfg.name}: Q4 plane-stress {cfg.nx}x{cfg.ny} cantilever"
+    return f"{cfg.name}: hex8 {cfg.nx}^3 elasticity"
+
+
 def main():
     args = parse()
     ws, rank, local = dist_env()
@@ -299,9 +306,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded KL lognormal modulus; generator in include/pod2g_gen.h)",
-            "config": {"workload": f"{cfg.name}: Q4 plane-stress {cfg.nx}x{cfg.ny} cantilever"
-                                   if cfg.dim == 2 else
-                                   f"{cfg.name}: hex8 {cfg.nx}^3 elasticity",
+            "config": {"workload": workload_name(cfg),
                        "n_dofs": n, "nnz": nnz, "pod_rank": int(prob.phi.shape[1]),
                        "instances_per_gpu": B, "tol": cfg.tol, "x0": "reduced_solve",
                        "smoother": "multicolour symmetric GS (node colours, D1)",
@@ -352,8 +357,10 @@ def reference_arm(args, cfg, PR, cores, ws):
         "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": f"{cfg.name}", "n_dofs": mesh.n, "nnz": mesh.nnz,
-                   "instances_per_step": ninst, "tol": cfg.tol},
+        "config": {"workload": workload_name(cfg), "n_dofs": mesh.n, "nnz": mesh.nnz,
+                   "pod_rank": int(prob.phi.shape[1]), "instances_per_step": ninst,
+                   "tol": cfg.tol, "x0": "reduced_solve",
+                   "smoother": "natural-order symmetric GS (reference default)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": f"{ninst} {cfg.name} instances per step, one per host core "
                                    f"(parallel_for), natural-order SGS, x0=reduced_solve"},
