@@ -148,6 +148,15 @@ def cpu_reference_run(prob, values, F, instances, jobs):
     return dt, it
 
 
+def pin_limit():
+    """largest value batch to pin (the pinned copy doubles its host footprint)"""
+    try:
+        import psutil
+        return int(min(64 << 30, 0.35 * psutil.virtual_memory().available))
+    except Exception:
+        return 16 << 30
+
+
 def workload_name(cfg):
     """the config's workload label, shared by both arms"""
     if cfg.dim == 2:
@@ -244,7 +253,7 @@ def main():
     # ---- e2e through the C-ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        pin = values.nbytes < (16 << 30)  # very large batches: pageable host memory
+        pin = values.nbytes < pin_limit()  # very large batches: pageable host memory
         vals_h = torch.from_numpy(values)
         b_h = torch.from_numpy(F)
         x_h = torch.empty_like(b_h)
