@@ -2019,13 +2019,19 @@ __global__ void __launch_bounds__(kBlock) k_prolong_mma(int n, int Bp, double* s
 // is 4 rows x 8 consecutive instances (4 x 64 B), a Phi fragment 4 or 8 rows
 // of the padded copy (L1 hits across the CTA's warps) -- with U k-steps (or
 // m-blocks) of loads issued ahead of their MMAs.
+#ifndef P2G_RESTRICT_U
+#define P2G_RESTRICT_U 4  // k-steps of T / Phi loads in flight per warp (KMAX <= 24)
+#endif
+#ifndef P2G_RESTRICT_MINB
+#define P2G_RESTRICT_MINB 4
+#endif
 template <int TB, int KMAX>
-__global__ void P2G_CLUSTER __launch_bounds__(kBlock, KMAX > 40 ? 2 : 4) k_restrict_reg(int n, int Bp,
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock, KMAX > 40 ? 2 : P2G_RESTRICT_MINB) k_restrict_reg(int n, int Bp,
                                                                         const double* __restrict__ t,
                                                                         const double* __restrict__ phit,
                                                                         int k, int ks, double* part) {
     constexpr int NB = TB / 8, KSPLIT = kWarps / NB, MBX = (KMAX + 7) / 8;
-    constexpr int U = KMAX <= 24 ? 4 : (KMAX <= 40 ? 2 : 1);  // k-steps of loads ahead
+    constexpr int U = KMAX <= 24 ? P2G_RESTRICT_U : (KMAX <= 40 ? 2 : 1);  // k-steps of loads ahead
     __shared__ double tot[KSPLIT][KMAX * TB];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, tg = lane & 3;

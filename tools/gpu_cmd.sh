@@ -1,1 +1,1 @@
-python -c "import __graft_entry__ as g; g.smoke()"
+./tools/ab_variants.sh c2 ru8 ru6 ru2 2>&1 | grep -E "==|resid|total"
