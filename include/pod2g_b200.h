@@ -131,11 +131,13 @@ int p2g_set_values(p2g_handle* h, int32_t batch, const double* values);
 /* Same, from device memory of the handle's device ([B][nnz]). */
 int p2g_set_values_device(p2g_handle* h, int32_t batch, const double* d_values);
 /* Pipelining for batch streams (the reference's caller loops over batches of
- * instances, bench.hpp:290-330): start the host->device copy of the NEXT
- * batch's values [B][nnz] on the handle's copy stream and return at once,
- * so it overlaps the current solve.  A later p2g_set_values with the same
- * pointer and batch consumes the copy (device relayout only).  The host
- * buffer must stay unchanged (and should be pinned) until then. */
+ * instances, bench.hpp:290-330): request the host->device copy of the NEXT
+ * batch's values [B][nnz] and return at once.  The copy runs on the handle's
+ * copy stream, started by the next p2g_solve right after it has uploaded its
+ * right-hand sides, so it overlaps that solve without delaying it.  A later
+ * p2g_set_values with the same pointer and batch consumes the copy (device
+ * relayout only; it starts the copy itself if no solve did).  The host
+ * buffer must stay valid and unchanged (and should be pinned) until then. */
 int p2g_prefetch_values(p2g_handle* h, int32_t batch, const double* values);
 
 /* POD basis Phi, n x k row-major (PodBasis::phi_r, pod.hpp:20; rank k).

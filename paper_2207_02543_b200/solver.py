@@ -138,6 +138,8 @@ class BatchSolver:
             raise ValueError("set_values: values must be [B][nnz]")
         self._check(self._L.p2g_set_values(self._h, v.shape[0], _d(v)), "set_values")
         self.B = v.shape[0]
+        if getattr(self, "_pref_keep", None) is v:
+            self._pref_keep = None  # consumed
 
     def prefetch_values(self, values):
         """p2g_prefetch_values: start the copy of the next batch's values; a
@@ -147,6 +149,7 @@ class BatchSolver:
             raise ValueError("prefetch_values: C-contiguous float64 [B][nnz] required")
         self._check(self._L.p2g_prefetch_values(self._h, values.shape[0], _d(values)),
                     "prefetch_values")
+        self._pref_keep = values  # the copy reads it asynchronously
 
     def set_values_device(self, ptr: int, batch: int):
         self._check(self._L.p2g_set_values_device(self._h, batch, C.c_void_p(ptr)),
