@@ -1530,6 +1530,8 @@ int p2g_set_pattern(p2g_handle* h, int64_t n, const uint64_t* row_offsets,
     const std::string msg = build_coloured_pattern(n, row_offsets, col_indices, block_size, pat);
     REQ(msg.empty(), P2G_EINVAL, msg);
     destroy_graph(h);
+    if (h->cstream) CU(cudaStreamSynchronize(h->cstream));
+    h->pref_host = nullptr;  // a prefetch sized for the old pattern is void
     h->pat = std::move(pat);
     h->have_pattern = true;
     h->have_values = false;

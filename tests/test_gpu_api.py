@@ -194,3 +194,11 @@ def test_prefetched_values_pipeline(gpu):
     assert np.array_equal(x1, y1) and np.array_equal(it1, jt1)
     assert np.array_equal(x2, y2) and np.array_equal(it2, jt2)
     assert np.array_equal(x2, y3)
+    # a new pattern voids a pending prefetch: the next set_values uploads directly
+    s = BatchSolver(0)
+    s.set_pattern(g["rp"], g["ci"], 2)
+    s.prefetch_values(V1)
+    s.set_pattern(g["rp"], g["ci"], 2)
+    y4 = run(s, V1)[0]
+    s.close()
+    assert np.array_equal(x1, y4)
