@@ -252,3 +252,23 @@ def test_node_blocking_rejects_unequal_node_rows():
     assert not ok
     with pytest.raises(ValueError):
         analyze_node_blocking(rp2, ci2[::-1].copy(), 2)
+
+
+def test_wavefront_colouring_knob_is_valid(monkeypatch):
+    """P2G_WAVE_COLOURS=C (measured and off by default): colour =
+    natural-order GS level mod C; classes are independent sets and the node's
+    dofs stay adjacent, like the default parity colouring."""
+    m = PR.Mesh(2, 16, 8, 1, 2.0, 1.0, 1.0)
+    rp, ci = m.pattern()
+    monkeypatch.setenv("P2G_WAVE_COLOURS", "8")
+    perm, offs = analyze_pattern(rp, ci, m.block_size)
+    assert len(offs) - 1 == 8
+    bs = m.block_size
+    colour = np.empty(m.n // bs, dtype=int)
+    for c in range(len(offs) - 1):
+        colour[perm[offs[c]:offs[c + 1]] // bs] = c
+    K = to_scipy(rp, ci, np.ones(len(ci)), m.n).tocoo()
+    a, b = K.row // bs, K.col // bs
+    off = a != b
+    assert np.all(colour[a[off]] != colour[b[off]])
+    assert np.all(perm[1::bs] == perm[0::bs] + 1)
