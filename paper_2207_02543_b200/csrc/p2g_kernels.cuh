@@ -755,7 +755,10 @@ struct NodeTab {
 #define P2G_BLK_UNR_L 1  // neighbour nodes in flight, all-row passes
 #endif
 #ifndef P2G_BLK_UNR_U
-#define P2G_BLK_UNR_U 2  // neighbour nodes in flight, one-row passes
+#define P2G_BLK_UNR_U 1  // neighbour nodes in flight, one-row passes, Q4 (c2: 168 vs 172 us at 2)
+#endif
+#ifndef P2G_BLK_UNR_U_HEX
+#define P2G_BLK_UNR_U_HEX 3  // the same for hex8 (c4: 6.30 vs 6.48 ms at 1)
 #endif
 
 __device__ __forceinline__ void node_fetch(const NodeTab& T, int node, int lane, int4& inf, int& nc) {
@@ -951,8 +954,8 @@ __global__ void P2G_CLUSTER P2G_ROWK k_gs_backward_blk(Mat A, NodeTab T, const d
                         acc[c][v] = __dsub_rn(acc[c][v], __dmul_rn(a[v], sn[cc][v]));
                 }
                 // one-row pass over the upper nodes
-                blk_pass_row<Sh, BS, P2G_BLK_UNR_U>(vb + c * rl * Bp, Bp, s + b0, nc, (int)pos + 1,
-                                                    nnb, acc[c]);
+                blk_pass_row<Sh, BS, (BS == 2 ? P2G_BLK_UNR_U : P2G_BLK_UNR_U_HEX)>(
+                    vb + c * rl * Bp, Bp, s + b0, nc, (int)pos + 1, nnb, acc[c]);
                 double d[V];
                 ldv_ro<V, false>(d, vb + (c * rl + pos * BS + c) * Bp);
 #pragma unroll
