@@ -911,12 +911,33 @@ struct Run {
                 dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)h->num_sms * occ)),
                        (unsigned)((Bt + MSh::T - 1) / MSh::T));
                 fn<<<g, kBlock, 0, h->stream>>>(A, h->d_phi, k, bofs, Bt, Y); ++h->launches_executed;
-                auto fr = k_restrict_cols<KM>;
-                dim3 g2((unsigned)std::min<int64_t>(occ_blocks, (n + kWarps - 1) / kWarps),
-                        (unsigned)((ncol + 31) / 32));
-                fr<<<g2, kBlock, 0, h->stream>>>(n, ncol, Y, h->d_phi, k, part); ++h->launches_executed;
+                // Phi^T Y: the restriction's DMMA kernel with Y's k*Bt columns as
+                // the "instances" (row stride ncol), one partial row per cluster
+                // (the [blk][a][ncol] layout k_reduce_ac reads); the CUDA-core
+                // k_restrict_cols remains for column counts off the 32 grid
+                int nblk = 0;
+                if (ncol % 32 == 0 && !std::getenv("P2G_AC_CUDACORE")) {
+                    auto launch = [&](auto fr, int TB) {
+                        const int64_t need = (n + 127) / 128;
+                        int64_t gx = std::min<int64_t>(need, resident_ctas(h, (const void*)fr, true));
+                        gx = std::min<int64_t>(std::max<int64_t>(gx, 1), occ_blocks);
+                        gx = std::max<int64_t>(gx / kCluster, 1) * kCluster;
+                        dim3 g2((unsigned)gx, (unsigned)(ncol / TB));
+                        fr<<<g2, kBlock, 0, h->stream>>>(n, ncol, Y, h->d_phit, k, h->phi_ks, part);
+                        nblk = (int)(gx / kCluster);
+                    };
+                    if (ncol % 64 == 0) launch(k_restrict_reg<64, KM>, 64);
+                    else launch(k_restrict_reg<32, KM>, 32);
+                } else {
+                    auto fr = k_restrict_cols<KM>;
+                    dim3 g2((unsigned)std::min<int64_t>(occ_blocks, (n + kWarps - 1) / kWarps),
+                            (unsigned)((ncol + 31) / 32));
+                    fr<<<g2, kBlock, 0, h->stream>>>(n, ncol, Y, h->d_phi, k, part);
+                    nblk = (int)g2.x;
+                }
+                ++h->launches_executed;
                 const int total = Bt * k * k;
-                k_reduce_ac<<<(total + 7) / 8, 256, 0, h->stream>>>(g2.x, k, Bt, bofs, part, h->d_Ac); ++h->launches_executed;
+                k_reduce_ac<<<(total + 7) / 8, 256, 0, h->stream>>>(nblk, k, Bt, bofs, part, h->d_Ac); ++h->launches_executed;
             });
             if (cudaGetLastError() != cudaSuccess) st = P2G_ECUDA;
         }
