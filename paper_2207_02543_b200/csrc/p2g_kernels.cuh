@@ -849,8 +849,15 @@ __device__ __forceinline__ void blk_pass_row(const double* vr, unsigned Bp, cons
 // Forward GS colour phase, first sweep from s = 0 (L part only), all BS rows
 // of a node together: lower neighbour nodes, then the node's own lower
 // components (new values), then the division (smoothers.hpp:31-44).
+#ifndef P2G_FWD_MINB
+#define P2G_FWD_MINB P2G_MINB
+#endif
+#ifndef P2G_FWD_UNR
+#define P2G_FWD_UNR P2G_BLK_UNR_L
+#endif
 template <class Sh, int BS>
-__global__ void P2G_ROWK k_gs_forward_blk(Mat A, NodeTab T, const double* __restrict__ f, double* s,
+__global__ void __launch_bounds__(kBlock, Sh::W == 1 ? P2G_B1_MINB : P2G_FWD_MINB)
+    k_gs_forward_blk(Mat A, NodeTab T, const double* __restrict__ f, double* s,
                                           const int* active, int nb, int ne) {
     constexpr int V = Sh::V;
     LaneGeo<Sh> G;
@@ -866,8 +873,8 @@ __global__ void P2G_ROWK k_gs_forward_blk(Mat A, NodeTab T, const double* __rest
             double acc[BS][V];
 #pragma unroll
             for (int c = 0; c < BS; ++c) ldv_ro<V, false>(acc[c], f + ((size_t)node * BS + c) * Bp + b0);
-            blk_pass<Sh, BS, 0, BS, true, false, P2G_BLK_UNR_L>(vb, rl, Bp, s + b0, nullptr, nc, 0,
-                                                                (int)pos, acc);
+            blk_pass<Sh, BS, 0, BS, true, false, P2G_FWD_UNR>(vb, rl, Bp, s + b0, nullptr, nc, 0,
+                                                              (int)pos, acc);
             double sn[BS][V];
 #pragma unroll
             for (int c = 0; c < BS; ++c) {
