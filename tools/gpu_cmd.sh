@@ -1,1 +1,5 @@
-./tools/ab_variants.sh c2 f5 f6 f8 2>&1 | grep -E "==|forward|total"
+#!/bin/bash
+# Default GPU check (run through gpurun): the GPU suite and one bench line.
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -2 gpurun_out/pytest_gpu.log
+timeout 600 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo bench=$?; cat gpurun_out/bench_c2.json
