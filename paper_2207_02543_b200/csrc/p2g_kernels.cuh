@@ -21,6 +21,13 @@
 // (csr.hpp:83-105, smoothers.hpp:26-72); with S > 1 the row is split over
 // slot lanes and combined by a fixed xor-shuffle tree.
 //
+// Node-blocked patterns (FEM vector problems, NodeTab): the sweeps, the upper
+// residual and the Kp recurrence walk a node's neighbour NODES instead of
+// its rows -- the *_blk kernels (S == 1 shapes: one gather per neighbour node
+// for all BS rows, same per-row operation order, bit-identical) and the *_b1
+// / *_b1h kernels (B == 1: lane = neighbour node, one node per warp or per
+// 16-lane half, rows combined by an xor tree).
+//
 // All reductions (dot products, Phi^T t) are deterministic: per-block partials
 // in a fixed order, then fixed-order warp sums.  No floating-point atomics.
 #pragma once
