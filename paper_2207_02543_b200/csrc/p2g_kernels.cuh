@@ -987,17 +987,21 @@ __global__ void P2G_CLUSTER P2G_ROWK k_gs_backward_blk(Mat A, NodeTab T, const d
 
 // Kp recurrence (D9, see k_kp_update) with node blocking: the L part of all
 // BS rows (lower nodes, then own components < c) of s - s'.
-// Q4 (BS = 2): fewer, fatter warps with 4 neighbour nodes in flight pay here
-// (c2: 96 vs 101 us per iteration); hex8 keeps 4 CTAs/SM (c4: 3.68 vs 4.06 ms)
+// fewer, fatter warps pay here: Q4 (BS = 2) at 2 CTAs/SM with 4 neighbour
+// nodes in flight (c2: 96 vs 101 us per iteration); hex8 at 2 CTAs/SM with
+// one (c4: 3.40 vs 3.70 ms; 4 nodes in flight spill)
 #ifndef P2G_KP_MINB
 #define P2G_KP_MINB 2
 #endif
 #ifndef P2G_KP_UNR
 #define P2G_KP_UNR 4
 #endif
+#ifndef P2G_KP_MINB_HEX
+#define P2G_KP_MINB_HEX 2  // hex8, one node in flight, 128 registers: c4 3.40 vs 3.70 ms at 4, 4.55 at 3
+#endif
 template <class Sh, int BS>
 __global__ void P2G_CLUSTER
-__launch_bounds__(kBlock, Sh::W == 1 ? P2G_B1_MINB : (BS == 2 ? P2G_KP_MINB : P2G_MINB)) k_kp_update_blk(Mat A, NodeTab T, const double* __restrict__ r,
+__launch_bounds__(kBlock, Sh::W == 1 ? P2G_B1_MINB : (BS == 2 ? P2G_KP_MINB : P2G_KP_MINB_HEX)) k_kp_update_blk(Mat A, NodeTab T, const double* __restrict__ r,
                                                      const double* __restrict__ s,
                                                      const double* __restrict__ sp,
                                                      double* __restrict__ Kp, double* __restrict__ p,
