@@ -862,8 +862,16 @@ __device__ __forceinline__ void blk_pass_row(const double* vr, unsigned Bp, cons
 #ifndef P2G_FWD_UNR
 #define P2G_FWD_UNR P2G_BLK_UNR_L
 #endif
+// hex8 sweeps: 2 CTAs/SM (128 registers, no spills) beat 4 (64, spilling)
+// and 3 -- c4 forward 2.82 / 2.93 / 3.05 ms, backward 6.10 / 6.30 / 6.49 ms
+#ifndef P2G_FWD_MINB_HEX
+#define P2G_FWD_MINB_HEX 2
+#endif
+#ifndef P2G_BWD_MINB_HEX
+#define P2G_BWD_MINB_HEX 2
+#endif
 template <class Sh, int BS>
-__global__ void __launch_bounds__(kBlock, Sh::W == 1 ? P2G_B1_MINB : P2G_FWD_MINB)
+__global__ void __launch_bounds__(kBlock, Sh::W == 1 ? P2G_B1_MINB : (BS == 2 ? P2G_FWD_MINB : P2G_FWD_MINB_HEX))
     k_gs_forward_blk(Mat A, NodeTab T, const double* __restrict__ f, double* s,
                                           const int* active, int nb, int ne) {
     constexpr int V = Sh::V;
@@ -911,7 +919,8 @@ __global__ void __launch_bounds__(kBlock, Sh::W == 1 ? P2G_B1_MINB : P2G_FWD_MIN
 // after the new components it needs (gathers of s hit L1 on the repeat).
 // xlo == s: in place; xlo = s' (D9): out of place.  LAST: r.s partial.
 template <class Sh, int BS, bool LAST>
-__global__ void P2G_CLUSTER P2G_ROWK k_gs_backward_blk(Mat A, NodeTab T, const double* __restrict__ f,
+__global__ void P2G_CLUSTER
+__launch_bounds__(kBlock, Sh::W == 1 ? P2G_B1_MINB : (BS == 2 ? P2G_MINB : P2G_BWD_MINB_HEX)) k_gs_backward_blk(Mat A, NodeTab T, const double* __restrict__ f,
                                                        const double* xlo, double* s,
                                                        const int* active, int nb, int ne,
                                                        double* part_rs, int accumulate) {
