@@ -1088,8 +1088,12 @@ __launch_bounds__(kBlock, Sh::W == 1 ? P2G_B1_MINB : (BS == 2 ? P2G_KP_MINB : P2
 
 // Residual after one forward sweep from zero, t = -U u (RES_UPPER, D6), node
 // blocked: row c's U part is own components > c, then the upper nodes.
+#ifndef P2G_RES_HEX_BLK
+#define P2G_RES_HEX_BLK 1  // hex8 upper residual node-blocked at 2 CTAs/SM (c4 2.88 vs 3.21 ms row kernel)
+#endif
 template <class Sh, int BS>
-__global__ void P2G_CLUSTER P2G_ROWK k_residual_upper_blk(Mat A, NodeTab T, const double* __restrict__ u,
+__global__ void P2G_CLUSTER
+__launch_bounds__(kBlock, Sh::W == 1 ? P2G_B1_MINB : (BS == 2 ? P2G_MINB : 2)) k_residual_upper_blk(Mat A, NodeTab T, const double* __restrict__ u,
                                                           double* __restrict__ t,
                                                           const int* active) {
     constexpr int V = Sh::V;

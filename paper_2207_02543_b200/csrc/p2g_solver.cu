@@ -655,7 +655,7 @@ struct Run {
                 }
             }
             if constexpr (Sh::S == 1) {
-                if (form == RES_UPPER && blk(h) && h->pat.bs == 2) {  // hex8: row kernel faster
+                if (form == RES_UPPER && blk(h) && (h->pat.bs == 2 || P2G_RES_HEX_BLK)) {
                     P2G_BS_SWITCH(h->pat.bs, {
                         auto fn = k_residual_upper_blk<Sh, BS>;
                         dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn, true);
