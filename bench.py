@@ -10,12 +10,20 @@ per-instance setup (A_c = Phi^T K Phi + LDL^T), x0, and the PCG loop.  The
 basis is the offline stage's product, uploaded once and shared by every batch
 (the reference shares it by shared_ptr across instances, pod.hpp:261-263).
 
-  python bench.py [--gpus N --steps K --warmup W --config c2 --impl ours|reference]
+  python bench.py [--gpus N --steps K --warmup W --config cN --impl ours|reference]
 
-N > 1 (torchrun): instance sharding, one 64-instance batch per rank with
-disjoint seeds (weak scaling, no data-path collective); max-over-ranks time.
+N > 1: one process per GPU.  Under torchrun (WORLD_SIZE set) WORLD_SIZE must
+equal --gpus; without it bench.py launches torchrun itself (127.0.0.1).  The
+default config is c2 at N = 1 (BASELINE.json configs[1], a 1-GPU config) and
+c4 at N > 1 (configs[3], the sharded hex8 batch): BASELINE's instance total
+(64 for c4, 256 for c3) is split across the ranks (strong scaling), no
+data-path collective; max-over-ranks time.
 --impl reference: the unmodified reference (oracle/_ref, compiled from
-/root/reference by oracle/Makefile) on the host cores, rank 0 only.
+/root/reference by oracle/Makefile) on the host cores, rank 0 only; its
+inputs come from the CPU-only generator library (libpod2g_gen.so), so that
+arm never loads the CUDA library.
+--dry-run: no GPU work; ranks (gloo) agree on the sharding and rank 0 prints
+the line's n_gpus / config (the CPU test of the multi-GPU plumbing).
 """
 from __future__ import annotations
 
@@ -43,12 +51,35 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default=None,
+                    help="c1..c5 (default: c2 at --gpus 1, c4 at --gpus > 1)")
+    ap.add_argument("--dry-run", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-instances", type=int, default=0,
                     help="instances in the CPU sample (default: one per host core, <= batch)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if a.config is None:
+        a.config = "c2" if a.gpus == 1 else "c4"
+    return a
+
+
+def free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(args):
+    """--gpus N outside torchrun: launch N ranks with torchrun on this node
+    (rendezvous on 127.0.0.1); rank 0 prints the line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def dist_env():
@@ -120,14 +151,15 @@ def hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(kclass):
-    """dram bytes per launch of the dominant kernel class from the committed
-    ncu --set full capture (profiles/ncu_summary.json), or None."""
-    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+def ncu_traffic(config, kclass):
+    """dram bytes per iteration of kernel class `kclass` on `config`, from the
+    committed ncu --set full capture of THAT config (profiles/ncu_traffic.json,
+    written by tools/ncu_classes.py), or None when that config has none."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as fh:
             d = json.load(fh)
-        return d["per_iteration_dram_bytes"].get(kclass)
+        return d[config]["per_iteration_dram_bytes"].get(kclass)
     except Exception:
         return None
 
@@ -164,9 +196,36 @@ def workload_name(cfg):
     return f"{cfg.name}: hex8 {cfg.nx}^3 elasticity"
 
 
+def dry_run(args, cfg, PR, ws, rank):
+    """The multi-GPU plumbing without a GPU: gloo ranks, sharding, gathers."""
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="env://")
+    from paper_2207_02543_b200 import dist as D
+    B, seeds, strong = PR.shard(cfg, ws, rank)
+    counts = D.gather_counts(np.array([B]))
+    first = D.gather_counts(np.array([int(seeds[0]) if B else -1]))
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": ws,
+                          "dry_run": True, "scaling": "strong" if strong else "weak",
+                          "config": {"workload": workload_name(cfg),
+                                     "instances_total": int(counts.sum()),
+                                     "instances_per_rank": counts.tolist(),
+                                     "first_seed_per_rank": first.tolist(),
+                                     "parallelism": f"instance-sharded x{ws}"}}), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        return spawn_ranks(args)
     ws, rank, local = dist_env()
+    if "WORLD_SIZE" in os.environ and ws != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}")
     if args.impl == "reference" and rank != 0:
         return 0  # the reference arm runs on rank 0 alone
 
@@ -175,7 +234,9 @@ def main():
     cores = os.cpu_count() or 1
 
     if args.impl == "reference":
-        return reference_arm(args, cfg, PR, cores, ws)
+        return reference_arm(args, cfg, PR, cores, args.gpus)
+    if args.dry_run:
+        return dry_run(args, cfg, PR, ws, rank)
 
     import torch
     import torch.distributed as dist
@@ -236,7 +297,7 @@ def main():
         barrier()
     launches = s.launch_counts()[1] - l0
     ms = D.max_over_ranks(ev0.elapsed_time(ev1), dev)
-    total_solves = (cfg.batch if strong else B * ws) * args.steps
+    total_solves = int(D.gather_counts(np.array([B]), dev).sum()) * args.steps
     value = total_solves / (ms / 1e3)
     iters = np.concatenate(iters_all)
 
@@ -317,7 +378,8 @@ def main():
             "data": "synthetic (seeded KL lognormal modulus; generator in include/pod2g_gen.h)",
             "config": {"workload": workload_name(cfg),
                        "n_dofs": n, "nnz": nnz, "pod_rank": int(prob.phi.shape[1]),
-                       "instances_per_gpu": B, "tol": cfg.tol, "x0": "reduced_solve",
+                       "instances_per_gpu": B, "instances_total": total_solves // args.steps,
+                       "tol": cfg.tol, "x0": "reduced_solve",
                        "smoother": "multicolour symmetric GS (node colours, D1)",
                        "l2": "inputs larger than L2 (values %.0f MB per GPU)" % (values.nbytes / 1e6),
                        "parallelism": f"instance-sharded x{ws}",
@@ -326,7 +388,7 @@ def main():
                        "all_converged": ok, "input_generation_s": round(gen_s, 2)},
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
-                         "traffic": ncu_traffic(dom_name),
+                         "traffic": ncu_traffic(cfg.name, dom_name),
                          "algorithmic_bytes_per_iteration": iter_bytes,
                          "iteration_ms": iter_ms,
                          "iteration_frac": iter_bytes / (iter_ms * 1e-3) / 1e9 / peak,

@@ -271,7 +271,7 @@ int p2g_analyze_node_blocking(int64_t n, const uint64_t* row_offsets, const uint
  * no solve ran since p2g_setup: a zero state has p'Kp = 0).  ms receives the
  * mean time per iteration of each class, bytes the algorithmic HBM bytes per
  * iteration of each class, names the class names (static). */
-#define P2G_NUM_KCLASS 9
+#define P2G_NUM_KCLASS 10
 int p2g_profile_iteration(p2g_handle* h, int32_t reps, double* ms, double* bytes,
                           const char** names);
 
@@ -321,7 +321,9 @@ int p2g_part_set_basis(p2g_part* p, int rank, int32_t k, const double* phi_own,
 /* collective over all hosted partitions (and all ranks) */
 int p2g_part_setup(p2g_part* p, const p2g_config* cfg, int32_t* status);
 /* b, x0, x: one pointer per hosted partition ([B][n_own]); iters / converged
- * / status / hist as p2g_solve (identical on every rank) */
+ * / status / hist as p2g_solve (identical on every rank).  x0_mode is
+ * P2G_X0_ZERO, P2G_X0_GIVEN or P2G_X0_REDUCED (no surrogate here); anything
+ * else is P2G_EINVAL. */
 int p2g_part_solve(p2g_part* p, const double* const* b, const double* const* x0, int32_t x0_mode,
                    double tol, int64_t max_iter, double* const* x, int64_t* iters,
                    int32_t* converged, int32_t* status, double* hist, int64_t hist_cap);

@@ -176,7 +176,8 @@ std::vector<double> reduced_solve(const Csr& K, const std::vector<double>& f, co
     h.check(p2g_set_basis(h.get(), static_cast<int32_t>(basis.rank), basis.phi_r.data.data()),
             "set_basis");
     int32_t st = P2G_OK;
-    p2g_setup(h.get(), nullptr, &st);
+    const int rc = p2g_setup(h.get(), nullptr, &st);
+    if (rc == P2G_EINVAL || rc == P2G_ECUDA || rc == P2G_ESTATE) h.check(rc, "setup");
     if (st == P2G_ESINGULAR)
         throw std::runtime_error("reduced_solve: reduced operator is singular for this basis");
     std::vector<double> x0(K.nrows);
@@ -207,15 +208,19 @@ std::vector<std::pair<std::vector<double>, SolveReport>> pcg_solve_batch(
     h.check(p2g_set_basis(h.get(), static_cast<int32_t>(basis.rank), basis.phi_r.data.data()),
             "set_basis");
     std::vector<int32_t> sst(B);
-    p2g_setup(h.get(), nullptr, sst.data());
+    const int src = p2g_setup(h.get(), nullptr, sst.data());
+    if (src == P2G_EINVAL || src == P2G_ECUDA || src == P2G_ESTATE) h.check(src, "setup");
     const int64_t cap = static_cast<int64_t>(max_iter) + 1;
     std::vector<double> X(B * n), hist(B * static_cast<std::size_t>(cap));
     std::vector<int64_t> it(B);
     std::vector<int32_t> conv(B), st(B);
     const auto t0 = std::chrono::steady_clock::now();
-    p2g_solve(h.get(), F.data(), nullptr, reduced_x0 ? P2G_X0_REDUCED : P2G_X0_ZERO, delta,
-              static_cast<int64_t>(max_iter), X.data(), it.data(), conv.data(), st.data(),
-              hist.data(), cap);
+    const int rc = p2g_solve(h.get(), F.data(), nullptr, reduced_x0 ? P2G_X0_REDUCED : P2G_X0_ZERO,
+                             delta, static_cast<int64_t>(max_iter), X.data(), it.data(),
+                             conv.data(), st.data(), hist.data(), cap);
+    // per-instance statuses come back in st[]; a call-level failure (EINVAL, ECUDA e.g. OOM,
+    // ESTATE) leaves X unwritten and must not pass as an all-zero "solution"
+    if (rc == P2G_EINVAL || rc == P2G_ECUDA || rc == P2G_ESTATE) h.check(rc, "pcg_solve_batch");
     const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     std::vector<std::pair<std::vector<double>, SolveReport>> out;
     for (std::size_t b = 0; b < B; ++b) {

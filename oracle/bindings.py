@@ -280,6 +280,8 @@ class Reference:
                                           _I64, _I32, _I32, C.c_int]
         L.ref_offline_basis.argtypes = [C.c_int64, _I64, _I64, C.c_int64, _D, C.c_int64, _D,
                                          C.c_double, C.c_int64, C.c_int, _D, _I64]
+        L.ref_compute_pod.argtypes = [C.c_int64, C.c_int64, _D, C.c_double, C.c_int64, _D,
+                                      _I64, _D, _D]
         L.ref_its_case.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
                                    C.c_int64, _I64, _I64, _I64, _I64, _I64, _D, _D, _D,
                                    C.c_int64]
@@ -465,6 +467,20 @@ class Reference:
         self._check(self.lib.ref_offline_basis(n, _i64(rp), _i64(ci), nnz, _d(values), N, _d(F),
                                                tol, rank, jobs, _d(phi), C.byref(r)))
         return np.ascontiguousarray(phi[:, : r.value])
+
+    def compute_pod(self, snapshots, rank=None, energy=None):
+        """pod2g::compute_pod (pod.hpp:73-148), RankTarget{rank} or EnergyTarget{energy}.
+        Returns (phi [d][r], Gram eigenvalues, energy fraction)."""
+        U = _f64(snapshots)
+        N, d = U.shape
+        target = float(rank) if energy is None else -float(energy)
+        phi = np.empty((d, N))
+        eig = np.empty(N)
+        r, en = C.c_int64(), C.c_double()
+        self._check(self.lib.ref_compute_pod(N, d, _d(U), target, N, _d(phi), C.byref(r),
+                                             _d(eig), C.byref(en)))
+        return np.ascontiguousarray(phi.reshape(-1)[: d * r.value].reshape(d, r.value)), eig, \
+            en.value
 
     def its_case(self, res=32, n_snapshots=100, offline_seed=42, bench_seed=7, inst=0, jobs=8):
         n, nnz, rank = C.c_int64(), C.c_int64(), C.c_int64()

@@ -317,6 +317,27 @@ int ref_offline_basis(int64_t n, const int64_t* rp, const int64_t* ci, int64_t n
     });
 }
 
+// compute_pod (pod.hpp:73-148) on caller-given snapshots [N][d].  target < 0
+// selects EnergyTarget{-target}, else RankTarget{target}.  phi receives d x r
+// (r <= cap_r), eig the N Gram eigenvalues (descending), energy the captured
+// energy fraction (PodBasis::energy_fraction).
+int ref_compute_pod(int64_t N, int64_t d, const double* U, double target, int64_t cap_r,
+                    double* phi, int64_t* rank_out, double* eig, double* energy) {
+    return guarded([&] {
+        std::vector<Vector> snaps(static_cast<size_t>(N));
+        for (int64_t i = 0; i < N; ++i) snaps[i].assign(U + i * d, U + (i + 1) * d);
+        const PodBasis b = target < 0 ? compute_pod(snaps, EnergyTarget{-target})
+                                      : compute_pod(snaps, RankTarget{static_cast<index_t>(target)});
+        if (static_cast<int64_t>(b.rank) > cap_r) throw std::invalid_argument("cap_r too small");
+        *rank_out = static_cast<int64_t>(b.rank);
+        std::memcpy(phi, b.phi_r.data.data(), sizeof(double) * b.phi_r.data.size());
+        if (eig)
+            for (size_t i = 0; i < b.eigenvalues.size() && static_cast<int64_t>(i) < N; ++i)
+                eig[i] = b.eigenvalues[i];
+        if (energy) *energy = b.energy_fraction;
+    });
+}
+
 // Known-answer case from the reference's own acceptance run: the `its`
 // problem (problems.hpp:99-177, make_its_problem :399-407) at resolution `res`,
 // offline basis exactly as run_offline builds it (bench.hpp:58-64: LHS seed,

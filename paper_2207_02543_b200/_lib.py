@@ -11,6 +11,7 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libpod2g_b200.so")
+GEN_PATH = os.path.join(HERE, "libpod2g_gen.so")
 
 D = C.POINTER(C.c_double)
 I64 = C.POINTER(C.c_int64)
@@ -74,7 +75,13 @@ SIGNATURES = [
     ("p2g_part_last_solve_ms", C.c_int, [H, D]),
     ("p2g_plan_partition", C.c_int, [C.c_int, C.c_int, I64, C.c_int64, U64, U64, C.c_int32, I32,
                                      I64, I64, I64, I64, C.c_char_p, C.c_int32]),
-    # pod2g_gen.h
+    # pod2g_gen.h, device-side assembly (in libpod2g_b200.so)
+    ("p2g_mesh_assemble_into", C.c_int, [H, H, C.c_int32, C.c_void_p, C.c_int32]),
+    ("p2g_part_assemble", C.c_int, [H, C.c_int, H, C.c_int32, C.c_void_p, C.c_int32]),
+]
+
+# pod2g_gen.h host generator: libpod2g_gen.so (CPU-only, no CUDA runtime)
+GEN_SIGNATURES = [
     ("p2g_mesh_create", C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_double,
                                   C.c_double, C.c_double, C.c_double, C.POINTER(H)]),
     ("p2g_mesh_destroy", None, [H]),
@@ -89,8 +96,6 @@ SIGNATURES = [
                                D, D]),
     ("p2g_kl_eigenvalues", C.c_int, [H, C.c_int32, C.c_double, C.c_int32, D]),
     ("p2g_normal_draws", C.c_int, [C.c_uint64, C.c_int64, D]),
-    ("p2g_mesh_assemble_into", C.c_int, [H, H, C.c_int32, C.c_void_p, C.c_int32]),
-    ("p2g_part_assemble", C.c_int, [H, C.c_int, H, C.c_int32, C.c_void_p, C.c_int32]),
 ]
 
 _lib = None
@@ -120,6 +125,25 @@ def lib():
     return _lib
 
 
+_gen = None
+
+
+def gen():
+    """Load the CPU-only generator library libpod2g_gen.so (once).  It links no
+    CUDA code: the reference arm of bench.py builds its inputs with it."""
+    global _gen
+    if _gen is None:
+        if not os.path.exists(GEN_PATH):
+            raise RuntimeError(f"{GEN_PATH} is missing: build it with `make -C {HERE}/csrc`")
+        G = C.CDLL(GEN_PATH)
+        for name, res, args in GEN_SIGNATURES:
+            fn = getattr(G, name)
+            fn.restype = res
+            fn.argtypes = args
+        _gen = G
+    return _gen
+
+
 class Config(C.Structure):
     """p2g_config (include/pod2g_b200.h)."""
     _fields_ = [("smoother", C.c_int32), ("pre_sweeps", C.c_int32), ("post_sweeps", C.c_int32),
@@ -134,4 +158,4 @@ RESIDUAL_FULL, RESIDUAL_UPPER = 0, 1
 KP_SPMV, KP_RECURRENCE = 0, 1
 X0_ZERO, X0_GIVEN, X0_REDUCED, X0_SURROGATE = 0, 1, 2, 3
 ACT_TANH, ACT_RELU = 0, 1
-NUM_KCLASS = 9
+NUM_KCLASS = 10

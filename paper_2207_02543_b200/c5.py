@@ -161,7 +161,13 @@ def run(cfg_name="c5", world=1, hosted=None, nccl_uid=None, n_snapshots=48, snap
     G = 0.5 * (G + G.T)
     w, V = np.linalg.eigh(G)
     order = np.argsort(-w, kind="stable")
-    w, V = w[order][:k], V[:, order][:, :k]
+    w, V = w[order], V[:, order]
+    # numerical-rank cutoff as compute_pod (pod.hpp:92-101): eigenvalues > 1e-12 lambda_max
+    r_num = int(np.count_nonzero(w > 1e-12 * w[0])) if w.size and w[0] > 0 else 0
+    if r_num < 1:
+        raise RuntimeError("c5 offline stage: snapshot Gram matrix has no positive eigenvalue")
+    k = min(k, r_num)
+    w, V = w[:k], V[:, :k]
     Wk = np.ascontiguousarray(V / np.sqrt(w))
     phi_own = {r: PR.combine_device(U[r], Wk, device) for r in hosted}
     phi_gh = {r: (PR.combine_device(U_gh[r], Wk, device) if U_gh[r].shape[1]

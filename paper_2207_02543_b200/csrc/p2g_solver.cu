@@ -43,11 +43,15 @@ enum Kclass {
     KC_PROLONG,
     KC_BWD,
     KC_REDUCE,
-    KC_PUPDATE
+    KC_PUPDATE,
+    KC_RESID
 };
+// one class per kernel family of the loop body (gs_forward / gs_backward: the
+// colour-phase launches of one sweep; scalar_reduce: k_alpha + k_finalize)
 const char* kKclassNames[P2G_NUM_KCLASS] = {"spmv_dot", "update_presmooth", "gs_forward",
-                                            "residual_restrict", "coarse_solve", "prolong",
-                                            "gs_backward", "scalar_reduce", "p_update"};
+                                            "restrict", "coarse_solve", "prolong",
+                                            "gs_backward", "scalar_reduce", "p_update",
+                                            "residual"};
 
 enum ShapeId { SH_B1A = 0, SH_B1B, SH_B8, SH_B32, SH_B64 };
 
@@ -99,7 +103,6 @@ struct p2g_handle {
     int *d_active = nullptr, *d_iters = nullptr, *d_status = nullptr, *d_setup_status = nullptr,
         *d_all = nullptr;
     double* d_hist = nullptr;
-    int64_t hist_cap_alloc = 0;
     SolveParams* d_prm = nullptr;
     unsigned* d_flag_ticket = nullptr;  // [any-active flag, CTA ticket] of k_finalize
     // partials
@@ -674,7 +677,7 @@ struct Run {
                 dim3 g = node_grid<Sh>(h, nnodes(h), (const void*)fn, true);
                 fn<<<g, kBlock, 0, h->stream>>>(A, f, s, tb, h->d_active, nullptr, nullptr);
             }
-            count_launch(h, KC_RESTRICT);
+            count_launch(h, KC_RESID);
             t = tb;
         }
         const int k = h->k;
@@ -1280,10 +1283,8 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
         "p2g_solve: reduced initial guess needs a basis");
     REQ(max_iter >= 0 && hist_cap >= 0, P2G_EINVAL, "p2g_solve: negative max_iter/hist_cap");
     const int64_t cap_dev = std::max<int64_t>(hist_cap, 1);
-    if (cap_dev > h->hist_cap_alloc || !h->d_hist) {
-        TRY(dalloc(h, h->d_hist, (size_t)cap_dev * h->Bp));
-        h->hist_cap_alloc = cap_dev;
-    }
+    // sized by bytes (ensure), so a later, larger batch on the same handle regrows it
+    TRY(ensure(h, h->d_hist, (size_t)cap_dev * h->Bp));
     if (cycle) {
         if (!h->cyc_exec || h->cyc_key != graph_key_of(h)) TRY(build_loop_graph(h, true));
     } else if (!h->loop_exec || h->graph_key != graph_key_of(h)) {
@@ -2052,16 +2053,18 @@ int p2g_profile_iteration(p2g_handle* h, int32_t reps, double* ms, double* bytes
     by[KC_UPDATE] = 48.0 * n * Bp + (gs ? 0.0 : 24.0 * n * Bp);  // u,p,r,Kp r/w (+ s,d for Jacobi)
     by[KC_FWD] = gs ? (8.0 * (zl + n) * Bp + 4.0 * (zl + n) + 4.0 * n + 24.0 * n * Bp * (C - 1) / C)
                     : 0.0;
-    by[KC_RESTRICT] = (gs && h->cfg.residual_form == P2G_RESIDUAL_UPPER && h->cfg.pre_sweeps == 1
-                           ? 8.0 * zl * Bp + 4.0 * zl + 4.0 * n
-                           : Mv + idx + 8.0 * n * Bp) +
-                      8.0 * n * Bp + 8.0 * n * k;
+    // residual: upper form t = -U s (U values, s read, t written); full form
+    // t = r - K s (all values, r and s read, t written)
+    by[KC_RESID] = gs && h->cfg.residual_form == P2G_RESIDUAL_UPPER && h->cfg.pre_sweeps == 1
+                       ? 8.0 * zl * Bp + 4.0 * zl + 4.0 * n + 16.0 * n * Bp
+                       : Mv + idx + 24.0 * n * Bp;
+    by[KC_RESTRICT] = 8.0 * n * Bp + 8.0 * n * k;  // t read, Phi read once
     by[KC_COARSE] = 0.0;
     by[KC_PROLONG] = 16.0 * n * Bp + 8.0 * n * k;
     by[KC_BWD] = Mv + idx + 24.0 * n * Bp;
     by[KC_REDUCE] = 0.0;
     by[KC_PUPDATE] = kp_recurrence(h) ? 0.0 : 24.0 * n * Bp;
-    if (h->k == 0) by[KC_RESTRICT] = by[KC_PROLONG] = 0.0;
+    if (h->k == 0) by[KC_RESID] = by[KC_RESTRICT] = by[KC_PROLONG] = 0.0;
     for (int q = 0; q < P2G_NUM_KCLASS; ++q) {
         if (ms) ms[q] = acc[q] / reps;
         if (bytes) bytes[q] = by[q];
@@ -2733,16 +2736,24 @@ int p2g_part_solve(p2g_part* P, const double* const* b, const double* const* x0,
         P->err = "p2g_part_solve: bad arguments";
         return P2G_EINVAL;
     }
+    if (x0_mode != P2G_X0_ZERO && x0_mode != P2G_X0_GIVEN && x0_mode != P2G_X0_REDUCED) {
+        P->err = "p2g_part_solve: x0_mode must be ZERO, GIVEN or REDUCED (no surrogate on the "
+                 "partitioned path)";
+        return P2G_EINVAL;
+    }
     const int64_t cap_dev = std::max<int64_t>(hist_cap, 1);
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
+    struct Events {  // destroyed on every exit path
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        Events() { cudaEventCreate(&e0); cudaEventCreate(&e1); }
+        ~Events() { cudaEventDestroy(e0); cudaEventDestroy(e1); }
+    } ev;
+    cudaEvent_t e0 = ev.e0, e1 = ev.e1;
     cudaEventRecord(e0, P->stream);
     for (size_t q = 0; q < P->parts.size(); ++q) {
         p2g_handle* h = P->parts[q].h;
-        if (cap_dev > h->hist_cap_alloc || !h->d_hist) {
-            if (dalloc(h, h->d_hist, (size_t)cap_dev * h->Bp) != P2G_OK) return P2G_ECUDA;
-            h->hist_cap_alloc = cap_dev;
+        if (ensure(h, h->d_hist, (size_t)cap_dev * h->Bp) != P2G_OK) {
+            P->err = h->err;
+            return P2G_ECUDA;
         }
         SolveParams prm{tol, (long long)max_iter, (long long)hist_cap};
         PCU(cudaMemcpyAsync(h->d_prm, &prm, sizeof(prm), cudaMemcpyHostToDevice, P->stream));
@@ -2765,8 +2776,6 @@ int p2g_part_solve(p2g_part* P, const double* const* b, const double* const* x0,
     // host-driven loop: instances deactivate on the device (exact stopping);
     // the host polls "any active" every kChunk iterations
     constexpr int kChunk = 8;
-    int* h_flag = nullptr;
-    PCU(cudaMallocHost(&h_flag, sizeof(int)));
     int64_t done = 0;
     const int Bp = P->parts[0].h->Bp;
     std::vector<int> act(Bp);
@@ -2781,7 +2790,6 @@ int p2g_part_solve(p2g_part* P, const double* const* b, const double* const* x0,
             PTRY(pdispatch(P, [&](auto R) -> int { return decltype(R)::iteration(P); }));
         done += kChunk;
     }
-    cudaFreeHost(h_flag);
     for (auto& L : P->parts) {
         p2g_handle* h = L.h;
         const dim3 g((unsigned)std::min<int64_t>((h->pat.n + 255) / 256, 1024), h->B);
@@ -2799,8 +2807,6 @@ int p2g_part_solve(p2g_part* P, const double* const* b, const double* const* x0,
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     P->last_ms = ms;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     p2g_handle* h = P->parts[0].h;
     std::vector<int> it(Bp), stt(Bp);
     std::vector<double> rel(Bp);

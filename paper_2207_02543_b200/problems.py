@@ -55,14 +55,15 @@ CONFIGS = {
 
 def shard(cfg: Config, world: int, rank: int):
     """Instance sharding across `world` GPUs (BASELINE.json: independent
-    instances, no communication).  Configs with more than one 64-instance
-    tile (c3: 256) split the batch (strong scaling); otherwise every rank
-    solves its own full batch with disjoint seeds (weak scaling).
-    Returns (instances_on_rank, seeds, strong)."""
+    instances, no communication).  A config's instance total (c2/c4: 64, c3:
+    256) is split contiguously across the ranks (strong scaling: the whole
+    job is BASELINE's batch at every world size).  Single-instance configs
+    (c1) run one replica per rank with disjoint seeds (weak scaling; c5 is
+    row-partitioned instead, c5.py).  Returns (instances_on_rank, seeds, strong)."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("shard: bad world/rank")
-    strong = cfg.batch > 64 and world > 1
-    if strong:
+    strong = world > 1 and cfg.batch >= world
+    if world == 1 or strong:
         base, extra = divmod(cfg.batch, world)
         count = base + (1 if rank < extra else 0)
         offset = rank * base + min(rank, extra)
@@ -87,7 +88,7 @@ class Mesh:
     """p2g_mesh: structured Q4 (dim 2) / hex8 (dim 3) elasticity generator."""
 
     def __init__(self, dim, nx, ny, nz=1, Lx=1.0, Ly=1.0, Lz=1.0, nu=NU):
-        self._L = L.lib()
+        self._L = L.gen()
         h = C.c_void_p()
         st = self._L.p2g_mesh_create(dim, nx, ny, nz, Lx, Ly, Lz, nu, C.byref(h))
         if st != 0:
@@ -193,7 +194,7 @@ class Mesh:
 
 def normal_draws(seed: int, count: int):
     out = np.empty(count)
-    L.lib().p2g_normal_draws(np.uint64(seed), count, out.ctypes.data_as(L.D))
+    L.gen().p2g_normal_draws(np.uint64(seed), count, out.ctypes.data_as(L.D))
     return out
 
 

@@ -31,12 +31,25 @@ def declared_functions():
 
 def test_library_exports_every_declared_symbol():
     lib = C.CDLL(L.LIB_PATH)
+    gen = C.CDLL(L.GEN_PATH)
     names = declared_functions()
     assert len(names) >= 30
-    missing = [n for n in names if not hasattr(lib, n)]
+    gen_names = {n for n, _, _ in L.GEN_SIGNATURES}
+    missing = [n for n in names if not hasattr(gen if n in gen_names else lib, n)]
     assert not missing, missing
-    bound = {n for n, _, _ in L.SIGNATURES}
+    bound = {n for n, _, _ in L.SIGNATURES} | gen_names
     assert set(names) <= bound, set(names) - bound
+
+
+def test_generator_library_is_cpu_only():
+    """libpod2g_gen.so (the seeded inputs) carries no CUDA code or runtime, so
+    the CPU reference arm never maps the CUDA library."""
+    import subprocess
+    out = subprocess.run(["ldd", L.GEN_PATH], capture_output=True, text=True).stdout
+    assert "cuda" not in out.lower() and "pod2g_b200" not in out, out
+    syms = subprocess.run(["nm", "-D", "--defined-only", L.GEN_PATH], capture_output=True,
+                          text=True).stdout
+    assert "cuda" not in syms.lower()
 
 
 def test_abi_version_and_status_strings():
@@ -206,14 +219,18 @@ def test_pattern_validation_errors():
 
 # ---------------------------------------------------------------- sharding
 def test_shard_weak_and_strong():
-    c2, c3 = PR.CONFIGS["c2"], PR.CONFIGS["c3"]
+    """BASELINE's instance totals are split across ranks (c2/c4: 64, c3: 256);
+    single-instance c1 runs one replica per rank with disjoint seeds."""
+    c1, c2, c3, c4 = (PR.CONFIGS[c] for c in ("c1", "c2", "c3", "c4"))
     n, seeds, strong = PR.shard(c2, 1, 0)
     assert n == 64 and not strong
-    all_seeds = np.concatenate([PR.shard(c2, 4, r)[1] for r in range(4)])
-    assert len(np.unique(all_seeds)) == 256  # weak: disjoint batches
-    parts = [PR.shard(c3, 8, r) for r in range(8)]
-    assert all(p[2] for p in parts) and sum(p[0] for p in parts) == 256
-    assert np.array_equal(np.concatenate([p[1] for p in parts]), PR.query_seeds(c3))
+    for cfg, world in ((c2, 4), (c3, 8), (c4, 2), (c4, 8), (c3, 3)):
+        parts = [PR.shard(cfg, world, r) for r in range(world)]
+        assert all(p[2] for p in parts) and sum(p[0] for p in parts) == cfg.batch
+        assert np.array_equal(np.concatenate([p[1] for p in parts]), PR.query_seeds(cfg))
+    reps = [PR.shard(c1, 4, r) for r in range(4)]
+    assert not any(p[2] for p in reps) and [p[0] for p in reps] == [1, 1, 1, 1]
+    assert len(np.unique(np.concatenate([p[1] for p in reps]))) == 4
 
 
 @pytest.mark.parametrize("dims,nmax", [((2, 16, 8, 1), 9), ((3, 4, 4, 4), 27)])

@@ -18,13 +18,14 @@ sys.path.insert(0, "tools")
 from ncu_summary import load  # noqa: E402
 
 CLASSES = [
-    ("spmv_dot", r"^(void )?(p2g::)?k_(spmv|kp_update|kp_update_blk)\b"),
+    ("spmv_dot", r"^(void )?(p2g::)?k_(spmv|kp_update\w*)\b"),
     ("update_presmooth", r"^(void )?(p2g::)?k_(update_pre|update_rows|jacobi)\b"),
-    ("gs_forward", r"^(void )?(p2g::)?k_gs_forward(_blk)?\b"),
-    ("residual_restrict", r"^(void )?(p2g::)?k_(residual|residual_upper_blk|restrict_vec|restrict_tiled|restrict_reg|restrict_mma)\b"),
+    ("gs_forward", r"^(void )?(p2g::)?k_gs_forward\w*\b"),
+    ("residual", r"^(void )?(p2g::)?k_residual\w*\b"),
+    ("restrict", r"^(void )?(p2g::)?k_(restrict_vec|restrict_tiled|restrict_reg|restrict_mma)\b"),
     ("coarse_solve", r"^(void )?(p2g::)?k_coarse\b"),
     ("prolong", r"^(void )?(p2g::)?k_prolong(_tiled|_reg|_mma)?\b"),
-    ("gs_backward", r"^(void )?(p2g::)?k_gs_backward(_blk)?\b"),
+    ("gs_backward", r"^(void )?(p2g::)?k_gs_backward\w*\b"),
     ("scalar_reduce", r"^(void )?(p2g::)?k_(alpha|finalize|set_cond|reduce_rows|sum_parts)\b"),
     ("p_update", r"^(void )?(p2g::)?k_pupdate\b"),
 ]
