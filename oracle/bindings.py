@@ -106,6 +106,7 @@ class Oracle:
                                          C.c_double, _D, _I64, _I32, _I32, C.c_int]
         L.or_surrogate_predict.argtypes = [C.c_int, _I64, C.c_int, _D, _D, _D, _D, _D, _D,
                                            C.c_int64, _D, C.c_int64, _D, _D]
+        L.or_permute_csr.argtypes = [C.c_int64, _I64, _I64, _D, _I64, C.c_int, _I64, _I64, _D]
         L.or_pod2g_solve.argtypes = [C.POINTER(_Csr), _D, C.c_int64, _D, _D, C.c_double,
                                      C.c_int64, C.c_int64, C.c_int64, _D, _I64, _I32, _D,
                                      C.c_int64, _I64]
@@ -251,6 +252,27 @@ class Oracle:
                                     conv.ctypes.data_as(_I32), status.ctypes.data_as(_I32),
                                     nthreads)
         return u, it, conv, status
+
+
+def permute_csr_fast(rp, ci, v, perm, threads=None):
+    """P K P^T as tests/helpers.permute_csr (new row i = old row perm[i],
+    columns sorted ascending, explicit zeros kept), in C with threads: for the
+    full-size systems.  rp / ci may be uint64 (viewed as int64, no copy)."""
+    def as_i64(a):
+        a = np.ascontiguousarray(a)
+        return a.view(np.int64) if a.dtype == np.uint64 else np.ascontiguousarray(a, dtype=np.int64)
+    rp, ci, perm = as_i64(rp), as_i64(ci), as_i64(perm)
+    v = _f64(v)
+    n = len(rp) - 1
+    nrp = np.empty(n + 1, dtype=np.int64)
+    nci = np.empty(len(ci), dtype=np.int64)
+    nv = np.empty(len(v))
+    L = Oracle().lib
+    st = L.or_permute_csr(n, _i64(rp), _i64(ci), _d(v), _i64(perm),
+                          int(threads or os.cpu_count() or 1), _i64(nrp), _i64(nci), _d(nv))
+    if st != 0:
+        raise ValueError("or_permute_csr: invalid permutation or arguments")
+    return nrp, nci, nv
 
 
 class Reference:

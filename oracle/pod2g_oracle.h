@@ -129,6 +129,11 @@ int or_surrogate_predict(int nlayers, const int64_t* widths, int act, const doub
                          const double* lat_mean, const double* lat_std, int64_t n,
                          const double* phi, int64_t B, const double* theta, double* x);
 
+/* csr_permute.c (test infrastructure, not a restatement): P K P^T with new
+ * row i = old row perm[i], columns sorted by new index; nrp n+1, nci/nv nnz */
+int or_permute_csr(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                   const int64_t* perm, int threads, int64_t* nrp, int64_t* nci, double* nv);
+
 #ifdef __cplusplus
 }
 #endif

@@ -41,3 +41,22 @@ def test_compute_pod_on_device_spans_the_host_basis(gpu):
     C = pd.T @ ph  # same orthonormal columns up to sign
     assert np.max(np.abs(np.abs(C) - np.eye(12))) <= 1e-8
     assert np.max(np.abs(pd.T @ pd - np.eye(12))) <= 1e-8
+
+
+def test_compute_pod_on_device_matches_reference_compute_pod(gpu):
+    """Row a16 on the GPU: Gram and Phi = U Psi Lambda^-1/2 on the FP64 tensor
+    cores, against the reference's own compute_pod (oracle/_ref) on the c1
+    solution snapshots."""
+    import scipy.sparse.linalg as spla
+    from oracle.bindings import Reference
+    from tests.helpers import to_scipy
+    from tests.test_pod_pin import compare
+    cfg = PR.CONFIGS["c1"]
+    m = PR.Mesh.for_config(cfg)
+    rp, ci = m.pattern()
+    f = m.rhs()
+    V = m.assemble(m.kl_field(PR.snapshot_seeds(cfg), cfg.kl_terms)[0])
+    U = np.stack([spla.spsolve(to_scipy(rp, ci, v, m.n).tocsc(), f) for v in V])
+    for k in (4, 10):
+        phi, w, energy = PR.compute_pod(U, k, device=0)
+        compare(U, phi, w, energy, Reference().compute_pod(U, rank=k), k)

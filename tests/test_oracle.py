@@ -248,3 +248,21 @@ def test_pod2g_solve_restatement_equals_reference():
         assert a.status == 0 and b.status == 0 and a.converged and b.converged
         assert a.iters == b.iters
         assert np.array_equal(a.history, b.history) and np.array_equal(a.u, b.u)
+
+
+def test_fast_permutation_equals_reference_permutation():
+    """oracle/csr_permute.c (used for the full-size c5 parity check) builds the
+    same P K P^T as tests/helpers.permute_csr, for any thread count."""
+    from oracle.bindings import permute_csr_fast
+    from paper_2207_02543_b200 import problems as PR
+    from tests.helpers import permute_csr
+    m = PR.Mesh(3, 5, 5, 5, 1.0, 1.0, 1.0)
+    rp, ci = m.pattern()
+    v = m.assemble(m.kl_field(np.array([3], dtype=np.uint64), 30)[0])[0]
+    perm = np.random.default_rng(0).permutation(m.n)
+    ref = permute_csr(rp, ci, v, perm)
+    for threads in (1, 3, 8):
+        got = permute_csr_fast(rp, ci, v, perm, threads=threads)
+        assert all(np.array_equal(a, b) for a, b in zip(ref, got))
+    with pytest.raises(ValueError):
+        permute_csr_fast(rp, ci, v, np.zeros(m.n, dtype=np.int64))
