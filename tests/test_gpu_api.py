@@ -41,6 +41,21 @@ def test_cpp_drop_in_example(gpu):
     assert r.returncode == 0, r.stdout + r.stderr
 
 
+def test_reference_pcg_solve_with_gpu_plugin(gpu):
+    """Row a13: pod2g_b200::RefPod2gPreconditioner (include/pod2g_b200_ref.hpp)
+    is a pod2g::Preconditioner (krylov.hpp:14-19).  oracle/_ref/ref_plugin_test
+    (compiled against the unmodified reference headers) drives it through the
+    reference's own pcg_solve (vs the reference on P K P^T: iterations +-1,
+    histories 1e-6, matched-iteration x 1e-8), run_pcg_benchmark's pod-2g
+    branch and run_monte_carlo, and the templated shim on pod2g::CsrMatrix."""
+    exe = os.path.join(os.path.dirname(HERE), "oracle", "_ref", "ref_plugin_test")
+    assert os.path.exists(exe), "build() compiles oracle/_ref/ref_plugin_test (make -C oracle plugin)"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "ref_plugin_test: ok" in r.stdout
+
+
 def test_python_reference_shaped_api(gpu):
     g = golden("q4c1.npz")
     n = len(g["rp"]) - 1
