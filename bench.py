@@ -54,6 +54,10 @@ def parse():
     ap.add_argument("--config", default=None,
                     help="c1..c5 (default: c2 at --gpus 1, c4 at --gpus > 1)")
     ap.add_argument("--dry-run", action="store_true")
+    ap.add_argument("--c5-snapshots", type=int, default=48,
+                    help="c5 offline stage: snapshot solves behind the k = 40 basis")
+    ap.add_argument("--c5-cpu-iters", type=int, default=2,
+                    help="c5 CPU baseline: reference PCG iterations timed (1 core)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-instances", type=int, default=0,
@@ -237,6 +241,8 @@ def main():
         return reference_arm(args, cfg, PR, cores, args.gpus)
     if args.dry_run:
         return dry_run(args, cfg, PR, ws, rank)
+    if cfg.name == "c5":
+        return c5_arm(args, cfg, ws, rank, local)
 
     import torch
     import torch.distributed as dist
@@ -404,6 +410,169 @@ def main():
     if ws > 1:
         dist.destroy_process_group()
     return 0
+
+
+def c5_arm(args, cfg, ws, rank, local):
+    """Config c5 (BASELINE.json configs[4]): ONE 12.4 M-dof hex8 system,
+    row-partitioned over the N GPUs (p2g_part_*: N = 1 one partition; N > 1
+    one partition per rank over NCCL, halo exchange + all-reduces).  A step =
+    one solve of the query instance: A_c + LDL^T setup, x0 = reduced_solve,
+    PCG to 1e-8.  value = solves/s (timed on the partition stream, max over
+    ranks); e2e = the same through host buffers (the rank's values uploaded
+    from pinned memory every step, b in, x out)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2207_02543_b200 import c5 as C5
+    from paper_2207_02543_b200 import dist as D
+    from paper_2207_02543_b200.partition import PartitionedSolver
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    uid = None
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://")
+        box = [PartitionedSolver.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, 0)
+        uid = box[0]
+
+    def log(*a):
+        if rank == 0:
+            print(*a, file=sys.stderr, flush=True)
+
+    t0 = time.perf_counter()
+    case = C5.prepare(cfg.name, ws, [rank] if ws > 1 else None, uid,
+                      n_snapshots=args.c5_snapshots, snap_batch=8, log=log, device=local)
+    case.query_values()
+    gen_s = time.perf_counter() - t0
+    P = case.P
+    stream = torch.cuda.ExternalStream(P.stream(), device=dev)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    its = []
+    for _ in range(args.warmup):
+        xs, it, conv, status, _ = case.solve()
+    barrier()
+    l0 = P.launch_counts()[1]
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ok = True
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            xs, it, conv, status, _ = case.solve()
+            ok &= bool(np.all(conv)) and bool(np.all(status == 0))
+            its.append(int(it[0]))
+        ev1.record(stream)
+        barrier()
+    per_iter, l1, loop_mode = P.launch_counts()
+    ms = D.max_over_ranks(ev0.elapsed_time(ev1), dev)
+    value = args.steps / (ms / 1e3)
+
+    prof = P.profile_iteration(3)
+    peak, peak_src = hbm_peak()
+    dom_name, (dom_ms, dom_bytes) = max(prof.items(), key=lambda kv: kv[1][0])
+    iter_ms = sum(v[0] for v in prof.values())
+    iter_bytes = sum(v[1] for v in prof.values())
+
+    # e2e: this rank's values from pinned host memory every step (+ b in, x out)
+    e2e = None
+    if not args.no_e2e:
+        r = case.hosted[0]
+        hv = torch.from_numpy(case.host_values(r)).pin_memory()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            P.set_values(r, hv.numpy())  # the basis stays (same batch size)
+            xs, it, conv, status, _ = case.solve()
+            ok &= bool(np.all(conv)) and bool(np.all(status == 0))
+        e1.record(stream)
+        barrier()
+        ems = D.max_over_ranks(e0.elapsed_time(e1), dev)
+        n_own = len(case.bvec[r])
+        e2e = {"value": args.steps / (ems / 1e3), "unit": UNIT, "pinned": True,
+               "h2d_bytes_per_step": int(hv.numel() * 8 + n_own * 8),
+               "d2h_bytes_per_step": int(n_own * 8 + 16),
+               "note": "per rank; values re-uploaded every step, basis kept (shared_ptr)"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        try:
+            cpu = c5_cpu_baseline(case, max(its), args.c5_cpu_iters)
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+    if rank == 0:
+        n, nnz = case.mesh.n, case.mesh.nnz
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded KL lognormal modulus; generator in include/pod2g_gen.h)",
+            "config": {"workload": workload_name(cfg), "n_dofs": n, "nnz": nnz,
+                       "pod_rank": int(case.k), "instances": 1, "tol": cfg.tol,
+                       "x0": "reduced_solve", "smoother": "multicolour symmetric GS (mesh "
+                       "parity node colouring, D1)",
+                       "l2": "inputs larger than L2 (values %.1f GB)" % (8.0 * nnz / 1e9),
+                       "parallelism": f"row-partitioned x{ws}" + (" (NCCL)" if ws > 1 else ""),
+                       "iterations": its[-1], "loop": {1: "conditional-WHILE graph",
+                                                       2: "captured 8-iteration chunks",
+                                                       0: "eager"}[loop_mode],
+                       "offline": f"{case.n_snapshots} snapshot solves, POD k={case.k}, "
+                                  f"{case.offline_s:.0f} s",
+                       "all_converged": ok, "input_generation_s": round(gen_s, 1)},
+            "roofline": {"bound": "hbm", "kernel": dom_name, "achieved":
+                         dom_bytes / (dom_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": dom_bytes / (dom_ms * 1e-3) / 1e9 / peak,
+                         "peak_source": peak_src, "traffic": ncu_traffic(cfg.name, dom_name),
+                         "algorithmic_bytes_per_iteration": iter_bytes,
+                         "iteration_ms": iter_ms,
+                         "iteration_frac": iter_bytes / (iter_ms * 1e-3) / 1e9 / peak,
+                         "classes": {k: {"ms": v[0], "bytes": v[1]} for k, v in prof.items()},
+                         "note": "rank 0's partition"},
+            "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(l1 - l0), "launches_per_iteration": int(per_iter),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    case.close()
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def c5_cpu_baseline(case, iters_gpu, n_prefix):
+    """The unmodified reference (oracle/_ref) on the c5 system, ONE core (the
+    reference has no intra-solve parallelism): Pod2gPreconditioner
+    construction (A_c = Phi^T K Phi, k SpMVs + k^2 dots, and DenseLu) plus the
+    first `n_prefix` PCG iterations (krylov.hpp:243-297, SolveReport
+    wall_time_s for the loop).  Extrapolated to a whole solve as 2 x setup
+    (reduced_solve builds A_c again) + iters_gpu x seconds per iteration."""
+    from oracle.bindings import Reference
+    R = Reference()
+    mesh = case.mesh
+    rp, ci = mesh.pattern()
+    v = mesh.assemble(case.E, 0)[0]
+    phi = case.phi_own[0]
+    f = mesh.rhs()
+    t = time.perf_counter()
+    res = R.pcg_pod2g(rp.view(np.int64), ci.view(np.int64), v, f, phi, np.zeros(mesh.n), 0.0,
+                      n_prefix)
+    call = time.perf_counter() - t
+    if res.status != 0:
+        raise RuntimeError(f"reference pcg_solve status {res.status}")
+    t_iter = res.wall_s / max(res.iters, 1)
+    setup = call - res.wall_s
+    total = 2.0 * setup + iters_gpu * t_iter
+    return {"value": 1.0 / total, "unit": UNIT, "cores": 1, "kind": "reference",
+            "extrapolated": True,
+            "sample": f"c5 query system, 1 core: Pod2gPreconditioner construction {setup:.1f} s "
+                      f"(A_c + LU, incl. CSR copy-in) and the first {res.iters} PCG iterations "
+                      f"({t_iter:.2f} s each, natural-order SGS); solve = 2 x setup + "
+                      f"{iters_gpu} iterations = {total:.0f} s (extrapolated)"}
 
 
 def reference_arm(args, cfg, PR, cores, ws):

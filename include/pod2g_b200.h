@@ -271,7 +271,7 @@ int p2g_analyze_node_blocking(int64_t n, const uint64_t* row_offsets, const uint
  * no solve ran since p2g_setup: a zero state has p'Kp = 0).  ms receives the
  * mean time per iteration of each class, bytes the algorithmic HBM bytes per
  * iteration of each class, names the class names (static). */
-#define P2G_NUM_KCLASS 10
+#define P2G_NUM_KCLASS 11
 int p2g_profile_iteration(p2g_handle* h, int32_t reps, double* ms, double* bytes,
                           const char** names);
 
@@ -328,6 +328,21 @@ int p2g_part_solve(p2g_part* p, const double* const* b, const double* const* x0,
                    double tol, int64_t max_iter, double* const* x, int64_t* iters,
                    int32_t* converged, int32_t* status, double* hist, int64_t hist_cap);
 int p2g_part_last_solve_ms(const p2g_part* p, double* ms);
+/* Kernel launches: per PCG iteration of the captured loop, and the running
+ * total over the hosted partitions (graph iterations included); loop_mode =
+ * how the last solve's loop ran: 1 conditional-WHILE graph (device-side
+ * stopping), 2 captured chunks of 8 iterations with a host poll between
+ * chunks, 0 eager (P2G_PART_EAGER=1). */
+int p2g_part_launch_counts(const p2g_part* p, int64_t* per_iteration, int64_t* total,
+                           int32_t* loop_mode);
+/* The stream every hosted partition launches on (cudaStream_t). */
+void* p2g_part_get_stream(const p2g_part* p);
+/* p2g_profile_iteration for a handle hosting ONE partition (N = 1, or one
+ * rank of an NCCL job): eager iterations with CUDA events between kernel
+ * classes on the handle's stream; class "halo_allreduce" is the exchange /
+ * all-reduce time.  After p2g_part_solve (P2G_ESTATE otherwise). */
+int p2g_part_profile_iteration(p2g_part* p, int32_t reps, double* ms, double* bytes,
+                               const char** names);
 /* Host-only (no device): the partition plan of one rank.  sizes = {n_own,
  * n_ghost, nnz, ncolors}; send_counts / recv_counts ([ncolors][world], zeroed
  * by the caller) accumulate the rows exchanged with each peer per colour. */

@@ -50,6 +50,11 @@ int p2g_mesh_element_stiffness(const p2g_mesh* m, double* Ke);
  * E[b][e] * Ke1[local]; nthreads worker threads (<= 0: hardware count). */
 int p2g_mesh_assemble(const p2g_mesh* m, int64_t B, const double* E, double* values,
                       int32_t nthreads);
+/* The same for the node-aligned free-row range [r0, r1) only (a partition's
+ * rows): values[b][nnz_range], nnz_range = row_offsets[r1] - row_offsets[r0]
+ * (the p2g_mesh_pattern_range layout).  Identical bits to the full assembly. */
+int p2g_mesh_assemble_range(const p2g_mesh* m, int64_t B, const double* E, int64_t r0,
+                            int64_t r1, double* values, int32_t nthreads);
 
 /* On-device generation: the B instances K(E_b) written
  * straight into a solver handle whose pattern is this mesh's (p2g_set_pattern

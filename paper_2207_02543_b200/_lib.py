@@ -73,6 +73,9 @@ SIGNATURES = [
     ("p2g_part_solve", C.c_int, [H, C.POINTER(D), C.POINTER(D), C.c_int32, C.c_double, C.c_int64,
                                  C.POINTER(D), I64, I32, I32, D, C.c_int64]),
     ("p2g_part_last_solve_ms", C.c_int, [H, D]),
+    ("p2g_part_launch_counts", C.c_int, [H, I64, I64, I32]),
+    ("p2g_part_get_stream", C.c_void_p, [H]),
+    ("p2g_part_profile_iteration", C.c_int, [H, C.c_int32, D, D, C.POINTER(C.c_char_p)]),
     ("p2g_plan_partition", C.c_int, [C.c_int, C.c_int, I64, C.c_int64, U64, U64, C.c_int32, I32,
                                      I64, I64, I64, I64, C.c_char_p, C.c_int32]),
     # pod2g_gen.h, device-side assembly (in libpod2g_b200.so)
@@ -92,6 +95,7 @@ GEN_SIGNATURES = [
     ("p2g_mesh_node_colors", C.c_int, [H, I32]),
     ("p2g_mesh_element_stiffness", C.c_int, [H, D]),
     ("p2g_mesh_assemble", C.c_int, [H, C.c_int64, D, D, C.c_int32]),
+    ("p2g_mesh_assemble_range", C.c_int, [H, C.c_int64, D, C.c_int64, C.c_int64, D, C.c_int32]),
     ("p2g_kl_field", C.c_int, [H, C.c_int32, C.c_double, C.c_double, C.c_int32, C.c_int64, U64,
                                D, D]),
     ("p2g_kl_eigenvalues", C.c_int, [H, C.c_int32, C.c_double, C.c_int32, D]),
@@ -158,4 +162,4 @@ RESIDUAL_FULL, RESIDUAL_UPPER = 0, 1
 KP_SPMV, KP_RECURRENCE = 0, 1
 X0_ZERO, X0_GIVEN, X0_REDUCED, X0_SURROGATE = 0, 1, 2, 3
 ACT_TANH, ACT_RELU = 0, 1
-NUM_KCLASS = 10
+NUM_KCLASS = 11

@@ -106,8 +106,58 @@ def _orthonormal(parts_own, parts_ghost, comm):
             {r: np.ascontiguousarray(v @ Ri) for r, v in parts_ghost.items()})
 
 
+class C5Case:
+    """The row-partitioned system after the offline stage: partition handle
+    `P` (pattern, device-generated query values, POD basis installed), the
+    right-hand sides of the hosted ranks, and the offline-stage record."""
+
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+    def query_values(self):
+        """The query instance's values on the device (p2g_part_assemble)."""
+        for r in self.hosted:
+            self.P.assemble(r, self.mesh, self.E)
+            self.P.set_basis(r, self.phi_own[r], self.phi_gh[r])
+
+    def host_values(self, r):
+        """Rank r's rows of the query instance's values, assembled on the host
+        ([1][local nnz], local rows, global columns) -- the e2e input."""
+        r0, r1 = int(self.bounds[r]), int(self.bounds[r + 1])
+        rp, ci = self.mesh.pattern_range(r0, r1)
+        return self.mesh.assemble_rows(self.E, r0, r1, int(rp[-1]))
+
+    def solve(self, max_iter=20000, tol=None):
+        self.P.setup()
+        return self.P.solve({r: self.bvec[r][None, :] for r in self.hosted},
+                            self.cfg.tol if tol is None else tol, max_iter, L.X0_REDUCED)
+
+    def close(self):
+        self.P.close()
+
+
 def run(cfg_name="c5", world=1, hosted=None, nccl_uid=None, n_snapshots=48, snap_batch=8,
         k=None, snap_tol=None, log=print, device=0):
+    """The offline stage (prepare) and one query solve; returns (record, x)."""
+    case = prepare(cfg_name, world, hosted, nccl_uid, n_snapshots, snap_batch, k, snap_tol, log,
+                   device)
+    t2 = time.perf_counter()
+    case.query_values()
+    xs, it, conv, status, hist = case.solve()
+    t_solve = time.perf_counter() - t2
+    P = case.P
+    log(f"[c5] query: iterations {int(it[0])} converged {bool(conv[0])} status {int(status[0])} "
+        f"setup+solve {t_solve * 1e3:.1f} ms (device solve {P.last_solve_ms():.1f} ms)")
+    res = dict(n=case.mesh.n, nnz=case.mesh.nnz, world=world, iterations=int(it[0]),
+               converged=bool(conv[0]), solve_ms=P.last_solve_ms(), setup_solve_s=t_solve,
+               offline_s=case.offline_s, snapshot_iterations_mean=case.snapshot_iterations_mean,
+               history=hist[0, :int(it[0]) + 1])
+    case.close()
+    return res, xs
+
+
+def prepare(cfg_name="c5", world=1, hosted=None, nccl_uid=None, n_snapshots=48, snap_batch=8,
+            k=None, snap_tol=None, log=print, device=0):
     cfg = PR.CONFIGS[cfg_name]
     k = cfg.k if k is None else k
     snap_tol = PR.SNAP_TOL if snap_tol is None else snap_tol
@@ -178,20 +228,9 @@ def run(cfg_name="c5", world=1, hosted=None, nccl_uid=None, n_snapshots=48, snap
     t_off = time.perf_counter() - t1
     log(f"[c5] offline: {n_snapshots} snapshots in {t_off:.1f}s (mean iterations "
         f"{np.mean(it_all):.0f}), POD rank {k}, defect {defect:.1e}")
-    # the measured query solve: one instance, x0 = reduced_solve, tol 1e-8
+    # the measured query: one instance (query seed 0), x0 = reduced_solve, tol 1e-8
     E, _ = mesh.kl_field(PR.query_seeds(cfg, 1), cfg.kl_terms)
-    for r in hosted:
-        P.assemble(r, mesh, E)
-        P.set_basis(r, phi_own[r], phi_gh[r])
-    t2 = time.perf_counter()
-    P.setup()
-    xs, it, conv, status, hist = P.solve({r: bvec[r][None, :] for r in hosted}, cfg.tol, 20000,
-                                         L.X0_REDUCED)
-    t_solve = time.perf_counter() - t2
-    log(f"[c5] query: iterations {int(it[0])} converged {bool(conv[0])} status {int(status[0])} "
-        f"setup+solve {t_solve * 1e3:.1f} ms (device solve {P.last_solve_ms():.1f} ms)")
-    res = dict(n=n, nnz=mesh.nnz, world=world, iterations=int(it[0]), converged=bool(conv[0]),
-               solve_ms=P.last_solve_ms(), setup_solve_s=t_solve, offline_s=t_off,
-               snapshot_iterations_mean=float(np.mean(it_all)), history=hist[0, :int(it[0]) + 1])
-    P.close()
-    return res, xs
+    return C5Case(cfg=cfg, P=P, mesh=mesh, bounds=bounds, hosted=hosted, world=world,
+                  ghosts=ghosts, bvec=bvec, phi_own=phi_own, phi_gh=phi_gh, E=E, k=k,
+                  offline_s=t_off, snapshot_iterations_mean=float(np.mean(it_all)),
+                  n_snapshots=n_snapshots)

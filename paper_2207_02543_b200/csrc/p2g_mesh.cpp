@@ -535,16 +535,19 @@ int p2g_mesh_element_stiffness(const p2g_mesh* m, double* Ke) {
     return P2G_GEN_OK;
 }
 
-int p2g_mesh_assemble(const p2g_mesh* m, int64_t B, const double* E, double* values,
-                      int32_t nthreads) {
-    if (!m || !E || !values || B < 1) return P2G_GEN_EINVAL;
+namespace {
+// values of free rows [row0, row1) (node aligned) into values[b][stride],
+// entry q of the range at values[b * stride + q - rp[row0]]
+int assemble_rows(const p2g_mesh* m, int64_t B, const double* E, int64_t row0, int64_t row1,
+                  double* values, int64_t stride, int32_t nthreads) {
     const Grid G = grid_of(m);
     const int dim = m->dim, ned = m->ned;
-    const int64_t nx = m->nx, ny = m->ny, nz = m->nz, nnz = m->nnz, nel = m->nelem;
-    parallel_rows(m->n / dim, nthreads, [&](int64_t r0, int64_t r1) {
+    const int64_t nx = m->nx, ny = m->ny, nz = m->nz, nnz = stride, nel = m->nelem;
+    const int64_t vbase = static_cast<int64_t>(m->rp[row0]);
+    parallel_rows((row1 - row0) / dim, nthreads, [&](int64_t a0, int64_t a1) {
         int64_t elist[8];
         int kidx[8][3][3];
-        for (int64_t rn = r0; rn < r1; ++rn) {
+        for (int64_t rn = row0 / dim + a0; rn < row0 / dim + a1; ++rn) {
             int64_t ix, iy, iz;
             G.coords(rn, ix, iy, iz);
             int64_t ax, bx, ay, by, az, bz;
@@ -579,7 +582,7 @@ int p2g_mesh_assemble(const p2g_mesh* m, int64_t B, const double* E, double* val
                                 }
                         for (int c = 0; c < dim; ++c) {
                             const int64_t row = rn * dim + c;
-                            const int64_t base = static_cast<int64_t>(m->rp[row]) + slot * dim;
+                            const int64_t base = static_cast<int64_t>(m->rp[row]) - vbase + slot * dim;
                             for (int d = 0; d < dim; ++d) {
                                 for (int64_t b = 0; b < B; ++b) {
                                     const double* Eb = E + b * nel;
@@ -593,6 +596,23 @@ int p2g_mesh_assemble(const p2g_mesh* m, int64_t B, const double* E, double* val
         }
     });
     return P2G_GEN_OK;
+}
+}  // namespace
+
+int p2g_mesh_assemble(const p2g_mesh* m, int64_t B, const double* E, double* values,
+                      int32_t nthreads) {
+    if (!m || !E || !values || B < 1) return P2G_GEN_EINVAL;
+    return assemble_rows(m, B, E, 0, m->n, values, m->nnz, nthreads);
+}
+
+int p2g_mesh_assemble_range(const p2g_mesh* m, int64_t B, const double* E, int64_t r0,
+                            int64_t r1, double* values, int32_t nthreads) {
+    if (!m || !E || !values || B < 1 || r0 < 0 || r1 > m->n || r0 > r1 || r0 % m->dim ||
+        r1 % m->dim)
+        return P2G_GEN_EINVAL;
+    const int64_t stride = static_cast<int64_t>(m->rp[r1] - m->rp[r0]);
+    if (r0 == r1) return P2G_GEN_OK;
+    return assemble_rows(m, B, E, r0, r1, values, stride, nthreads);
 }
 
 int p2g_normal_draws(uint64_t seed, int64_t count, double* out) {

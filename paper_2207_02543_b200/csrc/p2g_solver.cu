@@ -44,14 +44,15 @@ enum Kclass {
     KC_BWD,
     KC_REDUCE,
     KC_PUPDATE,
-    KC_RESID
+    KC_RESID,
+    KC_COMM
 };
 // one class per kernel family of the loop body (gs_forward / gs_backward: the
 // colour-phase launches of one sweep; scalar_reduce: k_alpha + k_finalize)
 const char* kKclassNames[P2G_NUM_KCLASS] = {"spmv_dot", "update_presmooth", "gs_forward",
                                             "restrict", "coarse_solve", "prolong",
                                             "gs_backward", "scalar_reduce", "p_update",
-                                            "residual"};
+                                            "residual", "halo_allreduce"};
 
 enum ShapeId { SH_B1A = 0, SH_B1B, SH_B8, SH_B32, SH_B64 };
 
@@ -259,14 +260,20 @@ Mat mat_of(p2g_handle* h) {
     return A;
 }
 
-void count_launch(p2g_handle* h, int kclass) {
-    ++h->launch_counter;
-    if (!h->capturing) ++h->launches_executed;
+// p2g_profile_iteration: close the current timing interval (everything
+// issued on the stream since the previous mark) and charge it to `kclass`
+void prof_mark(p2g_handle* h, int kclass) {
     if (h->profiling && h->kev_n < 63) {
         h->kev_class[h->kev_n] = kclass;
         cudaEventRecord(h->kev[h->kev_n + 1], h->stream);
         ++h->kev_n;
     }
+}
+
+void count_launch(p2g_handle* h, int kclass) {
+    ++h->launch_counter;
+    if (!h->capturing) ++h->launches_executed;
+    prof_mark(h, kclass);
 }
 
 // grid for a node-range kernel: one wave of resident blocks at most
@@ -2003,6 +2010,42 @@ int p2g_analyze_node_blocking(int64_t n, const uint64_t* row_offsets, const uint
     return P2G_OK;
 }
 
+// algorithmic HBM bytes per iteration of each kernel class (DESIGN.md,
+// SURVEY.md 8(d)) for the handle's current pattern / batch / basis / config
+static void class_bytes(const p2g_handle* h, double* by) {
+    for (int q = 0; q < P2G_NUM_KCLASS; ++q) by[q] = 0.0;
+    const double n = (double)h->pat.n, z = (double)h->pat.nnz, Bp = (double)h->B;
+    const double k = (double)std::max(h->k, 0);
+    const double Mv = 8.0 * z * Bp;                // values, one pass
+    const double C = h->pat.ncolors;
+    // lower/upper halves of the values (strict), diagonal
+    const double zl = 0.5 * (z - n);
+    // index bytes, shared by the batch: CSR column indices + row pointers, or
+    // -- node-blocked patterns, whose kernels read no column index -- the
+    // node table (16 B per node) and one 4 B neighbour id per bs x bs block
+    const double bs = std::max(h->pat.bs, 1), nodes = n / bs;
+    const double idx = h->node_blk ? 4.0 * z / (bs * bs) + 16.0 * nodes : 4.0 * z + 4.0 * (n + 1);
+    const double idx_half = h->node_blk ? 4.0 * (zl + n) / (bs * bs) + 16.0 * nodes
+                                        : 4.0 * zl + 4.0 * n;
+    const bool gs = h->cfg.smoother == P2G_SMOOTHER_GS_MULTICOLOR;
+    by[KC_SPMV] = kp_recurrence(h) ? 8.0 * zl * Bp + idx_half + 64.0 * n * Bp
+                                   : Mv + idx + 16.0 * n * Bp;  // L vals | vals, x once, y
+    by[KC_UPDATE] = 48.0 * n * Bp + (gs ? 0.0 : 24.0 * n * Bp);  // u,p,r,Kp r/w (+ s,d for Jacobi)
+    by[KC_FWD] = gs ? (8.0 * (zl + n) * Bp + idx_half + 24.0 * n * Bp * (C - 1) / C) : 0.0;
+    // residual: upper form t = -U s (U values, s read, t written); full form
+    // t = r - K s (all values, r and s read, t written)
+    by[KC_RESID] = gs && h->cfg.residual_form == P2G_RESIDUAL_UPPER && h->cfg.pre_sweeps == 1
+                       ? 8.0 * zl * Bp + idx_half + 16.0 * n * Bp
+                       : Mv + idx + 24.0 * n * Bp;
+    by[KC_RESTRICT] = 8.0 * n * Bp + 8.0 * n * k;  // t read, Phi read once
+    by[KC_COARSE] = 0.0;
+    by[KC_PROLONG] = 16.0 * n * Bp + 8.0 * n * k;
+    by[KC_BWD] = Mv + idx + 24.0 * n * Bp;
+    by[KC_REDUCE] = 0.0;
+    by[KC_PUPDATE] = kp_recurrence(h) ? 0.0 : 24.0 * n * Bp;
+    if (h->k == 0) by[KC_RESID] = by[KC_RESTRICT] = by[KC_PROLONG] = 0.0;
+}
+
 int p2g_profile_iteration(p2g_handle* h, int32_t reps, double* ms, double* bytes,
                           const char** names) {
     if (!h) return P2G_EINVAL;
@@ -2038,33 +2081,8 @@ int p2g_profile_iteration(p2g_handle* h, int32_t reps, double* ms, double* bytes
             acc[h->kev_class[q]] += t;
         }
     }
-    // algorithmic bytes per iteration per class:
-    const double n = (double)h->pat.n, z = (double)h->pat.nnz, Bp = (double)h->B;
-    const double k = (double)std::max(h->k, 0);
-    const double idx = 4.0 * z + 4.0 * (n + 1);    // shared pattern, once per batch
-    const double Mv = 8.0 * z * Bp;                // values, one pass
-    const double C = h->pat.ncolors;
     double by[P2G_NUM_KCLASS] = {0};
-    // lower/upper halves of the values (strict), diagonal
-    const double zl = 0.5 * (z - n);
-    const bool gs = h->cfg.smoother == P2G_SMOOTHER_GS_MULTICOLOR;
-    by[KC_SPMV] = kp_recurrence(h) ? 8.0 * zl * Bp + 4.0 * zl + 4.0 * n + 64.0 * n * Bp
-                                   : Mv + idx + 16.0 * n * Bp;  // L vals | vals, x once, y
-    by[KC_UPDATE] = 48.0 * n * Bp + (gs ? 0.0 : 24.0 * n * Bp);  // u,p,r,Kp r/w (+ s,d for Jacobi)
-    by[KC_FWD] = gs ? (8.0 * (zl + n) * Bp + 4.0 * (zl + n) + 4.0 * n + 24.0 * n * Bp * (C - 1) / C)
-                    : 0.0;
-    // residual: upper form t = -U s (U values, s read, t written); full form
-    // t = r - K s (all values, r and s read, t written)
-    by[KC_RESID] = gs && h->cfg.residual_form == P2G_RESIDUAL_UPPER && h->cfg.pre_sweeps == 1
-                       ? 8.0 * zl * Bp + 4.0 * zl + 4.0 * n + 16.0 * n * Bp
-                       : Mv + idx + 24.0 * n * Bp;
-    by[KC_RESTRICT] = 8.0 * n * Bp + 8.0 * n * k;  // t read, Phi read once
-    by[KC_COARSE] = 0.0;
-    by[KC_PROLONG] = 16.0 * n * Bp + 8.0 * n * k;
-    by[KC_BWD] = Mv + idx + 24.0 * n * Bp;
-    by[KC_REDUCE] = 0.0;
-    by[KC_PUPDATE] = kp_recurrence(h) ? 0.0 : 24.0 * n * Bp;
-    if (h->k == 0) by[KC_RESID] = by[KC_RESTRICT] = by[KC_PROLONG] = 0.0;
+    class_bytes(h, by);
     for (int q = 0; q < P2G_NUM_KCLASS; ++q) {
         if (ms) ms[q] = acc[q] / reps;
         if (bytes) bytes[q] = by[q];
@@ -2163,6 +2181,15 @@ struct p2g_part {
     bool setup_done = false;
     double last_ms = 0;
     int64_t iters_host = 0;
+    // the captured loop (build_part_graph): mode 1 = conditional WHILE node
+    // (device-side stopping, no host round trip), mode 2 = a chunk of
+    // kChunk iterations replayed until the host sees no active instance
+    cudaGraphExec_t loop_exec = nullptr;
+    int graph_mode = 0;
+    std::vector<uint64_t> graph_key;
+    cudaGraphConditionalHandle cond = 0;
+    bool capturing = false;
+    int64_t launches_per_iter = 0;
 };
 
 namespace {
@@ -2209,7 +2236,7 @@ int part_exchange(p2g_part* P, double* p2g_handle::*vec, int colour) {
         const int64_t total = cnt * h->Bp;
         const int grid = (int)std::min<int64_t>((total + 255) / 256, 4096);
         k_pack_rows<<<grid, 256, 0, P->stream>>>(h->*vec, h->Bp, L.d_rows + base, cnt, L.d_sendbuf);
-        ++h->launches_executed;
+        count_launch(h, KC_COMM);
         PCU(cudaGetLastError());
     }
     if (!P->use_nccl) {
@@ -2239,6 +2266,7 @@ int part_exchange(p2g_part* P, double* p2g_handle::*vec, int colour) {
                                     cudaMemcpyDeviceToDevice, P->stream));
             }
         }
+        prof_mark(P->parts[0].h, KC_COMM);
         return P2G_OK;
     }
     PartLocal& L = P->parts[0];
@@ -2254,6 +2282,7 @@ int part_exchange(p2g_part* P, double* p2g_handle::*vec, int colour) {
         PNC(g_nccl.Recv((L.h->*vec) + (size_t)rm.ghost_off * Bp, rm.count * Bp, ncclFloat64, rm.peer,
                         P->comm, P->stream));
     PNC(g_nccl.GroupEnd());
+    prof_mark(L.h, KC_COMM);
     return P2G_OK;
 }
 
@@ -2262,7 +2291,7 @@ int part_allreduce(p2g_part* P, double* p2g_handle::*buf, int nrows, int ncols) 
     for (auto& L : P->parts) {
         if (nrows > 1) {
             k_reduce_rows<<<(ncols + 255) / 256, 256, 0, P->stream>>>(L.h->*buf, nrows, ncols);
-            ++L.h->launches_executed;
+            count_launch(L.h, KC_COMM);
         }
     }
     if (P->world == 1) return P2G_OK;
@@ -2270,12 +2299,13 @@ int part_allreduce(p2g_part* P, double* p2g_handle::*buf, int nrows, int ncols) 
         PartPtrs pp{};
         for (size_t q = 0; q < P->parts.size(); ++q) pp.p[q] = P->parts[q].h->*buf;
         k_sum_parts<<<(ncols + 255) / 256, 256, 0, P->stream>>>(pp, (int)P->parts.size(), ncols);
-        ++P->parts[0].h->launches_executed;
+        count_launch(P->parts[0].h, KC_COMM);
         PCU(cudaGetLastError());
         return P2G_OK;
     }
     double* b = P->parts[0].h->*buf;
     PNC(g_nccl.AllReduce(b, b, ncols, ncclFloat64, ncclSum, P->comm, P->stream));
+    prof_mark(P->parts[0].h, KC_COMM);
     return P2G_OK;
 }
 
@@ -2365,10 +2395,13 @@ struct PartRun {
         PTRY(part_allreduce(P, &p2g_handle::d_part_rr, nb_rr, Bp));
         PTRY(part_allreduce(P, &p2g_handle::d_part_rs, rs_rows, Bp));
         PTRY(for_parts(P, [&](p2g_handle* h) {
+            // every partition holds the same (all-reduced) per-instance state;
+            // partition 0 drives the WHILE condition of the captured loop
+            const int set_cond = P->capturing && P->graph_mode == 1 && h == P->parts[0].h;
             k_finalize<<<(h->Bp + 7) / 8, 256, 0, h->stream>>>(
                 h->Bp, 1, h->d_part_rs, 1, h->d_part_rr, h->d_fnorm, h->d_rsold, h->d_beta,
                 h->d_rel, h->d_iters, h->d_active, h->d_status, h->d_hist, h->d_prm,
-                h->d_flag_ticket, h->cond, 0);
+                h->d_flag_ticket, set_cond ? P->cond : h->cond, set_cond);
             count_launch(h, KC_REDUCE);
             return P2G_OK;
         }));
@@ -2445,6 +2478,120 @@ int pdispatch(p2g_part* P, F&& f) {
         case SH_B32: return f(PartRun<ShB32>{});
         default: return f(PartRun<ShB64>{});
     }
+}
+
+constexpr int kPartChunk = 8;  // iterations per replay in graph mode 2 / the eager loop
+
+std::vector<uint64_t> part_graph_key(p2g_part* P) {
+    std::vector<uint64_t> key;
+    for (auto& L : P->parts) {
+        const auto k = graph_key_of(L.h);
+        key.insert(key.end(), k.begin(), k.end());
+        key.push_back((uint64_t)(uintptr_t)L.d_sendbuf);
+        key.push_back((uint64_t)(uintptr_t)L.d_rows);
+    }
+    return key;
+}
+
+void destroy_part_graph(p2g_part* P) {
+    if (P->loop_exec) cudaGraphExecDestroy(P->loop_exec);
+    P->loop_exec = nullptr;
+    P->graph_mode = 0;
+}
+
+// Capture one PCG iteration of every hosted partition (kernels, halo copies /
+// NCCL send-recv, all-reduces) as the body of a conditional WHILE node whose
+// condition partition 0's k_finalize sets (mode 1).  If the body cannot be
+// captured or instantiated that way (e.g. a transport whose operations are
+// not allowed inside a conditional body), capture kPartChunk iterations as a
+// plain graph instead (mode 2).  Returns P2G_OK with graph_mode 0 when neither
+// works: the eager loop then runs (P2G_PART_EAGER=1 forces it).
+int build_part_graph(p2g_part* P) {
+    destroy_part_graph(P);
+    const char* ev = std::getenv("P2G_PART_EAGER");
+    if (ev && ev[0] == '1') return P2G_OK;
+    p2g_handle* h0 = P->parts[0].h;
+    for (int mode = 1; mode <= 2; ++mode) {
+        cudaGraph_t outer = nullptr, body = nullptr;
+        if (cudaGraphCreate(&outer, 0) != cudaSuccess) break;
+        if (mode == 1) {
+            cudaGraphConditionalHandle cond;
+            if (cudaGraphConditionalHandleCreate(&cond, outer, 0, 0) != cudaSuccess) {
+                cudaGraphDestroy(outer);
+                continue;
+            }
+            P->cond = cond;
+            cudaKernelNodeParams kp = {};
+            int Bp = h0->Bp;
+            int* act = h0->d_active;
+            void* args[] = {&act, &Bp, &cond};
+            kp.func = (void*)k_set_cond;
+            kp.gridDim = dim3(1);
+            kp.blockDim = dim3(256);
+            kp.kernelParams = args;
+            cudaGraphNode_t setn, wnode;
+            cudaGraphNodeParams cp = {};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = cond;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            if (cudaGraphAddKernelNode(&setn, outer, nullptr, 0, &kp) != cudaSuccess ||
+                cudaGraphAddNode(&wnode, outer, &setn, 1, &cp) != cudaSuccess) {
+                cudaGraphDestroy(outer);
+                continue;
+            }
+            body = cp.conditional.phGraph_out[0];
+        } else {
+            body = outer;
+        }
+        if (cudaStreamBeginCaptureToGraph(P->stream, body, nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+            cudaGraphDestroy(outer);
+            cudaGetLastError();
+            continue;
+        }
+        P->capturing = true;
+        P->graph_mode = mode;
+        int64_t before = 0;
+        for (auto& L : P->parts) {
+            L.h->capturing = true;
+            before += L.h->launch_counter;
+        }
+        int st = P2G_OK;
+        const int reps = mode == 1 ? 1 : kPartChunk;
+        for (int q = 0; q < reps && st == P2G_OK; ++q)
+            st = pdispatch(P, [&](auto R) -> int { return decltype(R)::iteration(P); });
+        int64_t after = 0;
+        for (auto& L : P->parts) {
+            L.h->capturing = false;
+            after += L.h->launch_counter;
+        }
+        P->capturing = false;
+        cudaGraph_t captured = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(P->stream, &captured);
+        cudaGetLastError();
+        if (st != P2G_OK || ce != cudaSuccess) {
+            cudaGraphDestroy(outer);
+            P->graph_mode = 0;
+            P->err.clear();
+            if (st != P2G_OK && st != P2G_ECUDA && st != P2G_ENCCL) return st;
+            continue;
+        }
+        cudaGraphExec_t exec = nullptr;
+        const cudaError_t ie = cudaGraphInstantiate(&exec, outer, 0);
+        cudaGraphDestroy(outer);
+        if (ie != cudaSuccess) {
+            cudaGetLastError();
+            P->graph_mode = 0;
+            continue;
+        }
+        P->loop_exec = exec;
+        P->launches_per_iter = (after - before) / reps;
+        P->graph_key = part_graph_key(P);
+        return P2G_OK;
+    }
+    P->graph_mode = 0;
+    return P2G_OK;
 }
 
 int part_new(int device, int world, p2g_part** out) {
@@ -2530,6 +2677,7 @@ int p2g_part_destroy(p2g_part* P) {
     if (!P) return P2G_EINVAL;
     cudaSetDevice(P->device);
     cudaStreamSynchronize(P->stream);
+    destroy_part_graph(P);
     for (auto& L : P->parts) {
         if (L.d_rows) cudaFree(L.d_rows);
         if (L.d_sendbuf) cudaFree(L.d_sendbuf);
@@ -2548,6 +2696,7 @@ int p2g_part_set_pattern(p2g_part* P, int rank, int64_t n_global, const int64_t*
                          int32_t block_size, const int32_t* node_colors) {
     if (!P) return P2G_EINVAL;
     PCU(cudaSetDevice(P->device));
+    destroy_part_graph(P);
     PartLocal* L = local_of(P, rank);
     if (!L) {
         P->err = "p2g_part_set_pattern: rank not hosted by this handle";
@@ -2690,6 +2839,7 @@ int p2g_part_setup(p2g_part* P, const p2g_config* cfg, int32_t* status) {
     PCU(cudaSetDevice(P->device));
     p2g_config c;
     if (cfg) c = *cfg; else p2g_config_default(&c);
+    destroy_part_graph(P);
     if (c.smoother != P2G_SMOOTHER_GS_MULTICOLOR || c.pre_sweeps != 1 || c.post_sweeps != 1) {
         P->err = "p2g_part_setup: the partitioned path runs the multicolour GS smoother with r1 = r2 = 1";
         return P2G_EINVAL;
@@ -2772,23 +2922,36 @@ int p2g_part_solve(p2g_part* P, const double* const* b, const double* const* x0,
         PCU(cudaMemcpyAsync(h->d_active, h->d_all, sizeof(int) * h->Bp, cudaMemcpyDeviceToDevice,
                             P->stream));
     }
+    if (!P->loop_exec || P->graph_key != part_graph_key(P)) PTRY(build_part_graph(P));
     PTRY(pdispatch(P, [&](auto R) -> int { return decltype(R)::prologue(P, x0_mode); }));
-    // host-driven loop: instances deactivate on the device (exact stopping);
-    // the host polls "any active" every kChunk iterations
-    constexpr int kChunk = 8;
-    int64_t done = 0;
+    // instances deactivate on the device (exact stopping: iteration counts,
+    // history and solution equal those of independent solves)
     const int Bp = P->parts[0].h->Bp;
-    std::vector<int> act(Bp);
-    for (;;) {
-        PCU(cudaMemcpyAsync(act.data(), P->parts[0].h->d_active, sizeof(int) * Bp,
-                            cudaMemcpyDeviceToHost, P->stream));
-        PCU(cudaStreamSynchronize(P->stream));
-        bool any = false;
-        for (int v : act) any |= v != 0;
-        if (!any || done >= max_iter) break;
-        for (int q = 0; q < kChunk; ++q)
-            PTRY(pdispatch(P, [&](auto R) -> int { return decltype(R)::iteration(P); }));
-        done += kChunk;
+    int64_t replays = 0;
+    if (P->graph_mode == 1) {
+        // the whole loop on the device: conditional WHILE node
+        PCU(cudaGraphLaunch(P->loop_exec, P->stream));
+    } else {
+        // chunks of kPartChunk iterations (captured, or eager), the host
+        // polling "any active" between chunks
+        int64_t done = 0;
+        std::vector<int> act(Bp);
+        for (;;) {
+            PCU(cudaMemcpyAsync(act.data(), P->parts[0].h->d_active, sizeof(int) * Bp,
+                                cudaMemcpyDeviceToHost, P->stream));
+            PCU(cudaStreamSynchronize(P->stream));
+            bool any = false;
+            for (int v : act) any |= v != 0;
+            if (!any || done >= max_iter) break;
+            if (P->graph_mode == 2) {
+                PCU(cudaGraphLaunch(P->loop_exec, P->stream));
+                ++replays;
+            } else {
+                for (int q = 0; q < kPartChunk; ++q)
+                    PTRY(pdispatch(P, [&](auto R) -> int { return decltype(R)::iteration(P); }));
+            }
+            done += kPartChunk;
+        }
     }
     for (auto& L : P->parts) {
         p2g_handle* h = L.h;
@@ -2797,6 +2960,9 @@ int p2g_part_solve(p2g_part* P, const double* const* b, const double* const* x0,
                                                   h->d_status);
     }
     PTRY(part_allmax_int(P, &p2g_handle::d_status, Bp));
+    if (P->graph_mode == 2) {
+        P->parts[0].h->launches_executed += replays * kPartChunk * P->launches_per_iter;
+    }
     for (size_t q = 0; q < P->parts.size(); ++q)
         if (x && x[q] && download_interleaved(P->parts[q].h, P->parts[q].h->d_u, x[q], nullptr) != P2G_OK) {
             P->err = P->parts[q].h->err;
@@ -2813,6 +2979,11 @@ int p2g_part_solve(p2g_part* P, const double* const* b, const double* const* x0,
     PCU(cudaMemcpy(it.data(), h->d_iters, sizeof(int) * Bp, cudaMemcpyDeviceToHost));
     PCU(cudaMemcpy(stt.data(), h->d_status, sizeof(int) * Bp, cudaMemcpyDeviceToHost));
     PCU(cudaMemcpy(rel.data(), h->d_rel, sizeof(double) * Bp, cudaMemcpyDeviceToHost));
+    if (P->graph_mode == 1) {  // set_cond + one body per iteration of the slowest instance
+        int maxit = 0;
+        for (int bb = 0; bb < P->B; ++bb) maxit = std::max(maxit, it[bb]);
+        P->parts[0].h->launches_executed += 1 + (int64_t)maxit * P->launches_per_iter;
+    }
     int worst = P2G_OK;
     for (int bb = 0; bb < P->B; ++bb) {
         if (iters) iters[bb] = it[bb];
@@ -2832,6 +3003,64 @@ int p2g_part_solve(p2g_part* P, const double* const* b, const double* const* x0,
 int p2g_part_last_solve_ms(const p2g_part* P, double* ms) {
     if (!P || !ms) return P2G_EINVAL;
     *ms = P->last_ms;
+    return P2G_OK;
+}
+
+void* p2g_part_get_stream(const p2g_part* P) { return P ? (void*)P->stream : nullptr; }
+
+int p2g_part_launch_counts(const p2g_part* P, int64_t* per_iteration, int64_t* total,
+                           int32_t* loop_mode) {
+    if (!P) return P2G_EINVAL;
+    int64_t t = 0;
+    for (const auto& L : P->parts) t += L.h->launches_executed;
+    if (per_iteration) *per_iteration = P->launches_per_iter;
+    if (total) *total = t;
+    if (loop_mode) *loop_mode = P->graph_mode;
+    return P2G_OK;
+}
+
+int p2g_part_profile_iteration(p2g_part* P, int32_t reps, double* ms, double* bytes,
+                               const char** names) {
+    if (!P) return P2G_EINVAL;
+    PCU(cudaSetDevice(P->device));
+    if (P->parts.size() != 1 || !P->setup_done || reps < 1) {
+        P->err = "p2g_part_profile_iteration: one hosted partition, after p2g_part_solve, reps >= 1";
+        return P2G_ESTATE;
+    }
+    p2g_handle* h = P->parts[0].h;
+    std::vector<double> acc(P2G_NUM_KCLASS, 0.0);
+    SolveParams prm{0.0, (long long)1 << 62, 0};
+    PCU(cudaMemcpyAsync(h->d_prm, &prm, sizeof(prm), cudaMemcpyHostToDevice, P->stream));
+    for (int rep = 0; rep < reps; ++rep) {
+        PCU(cudaMemcpyAsync(h->d_active, h->d_all, sizeof(int) * h->Bp, cudaMemcpyDeviceToDevice,
+                            P->stream));
+        if (kp_recurrence(h)) {  // refresh Kp and the pKp partials (the body starts at alpha)
+            PTRY(part_exchange(P, &p2g_handle::d_p, -1));
+            PTRY(pdispatch(P, [&](auto R) -> int {
+                using Rn = typename decltype(R)::R;
+                return Rn::spmv(h, h->d_p, h->d_Kp, true, nullptr);
+            }));
+        }
+        h->profiling = true;
+        h->kev_n = 0;
+        PCU(cudaEventRecord(h->kev[0], P->stream));
+        const int st = pdispatch(P, [&](auto R) -> int { return decltype(R)::iteration(P); });
+        h->profiling = false;
+        PTRY(st);
+        PCU(cudaStreamSynchronize(P->stream));
+        for (int q = 0; q < h->kev_n; ++q) {
+            float t = 0;
+            cudaEventElapsedTime(&t, h->kev[q], h->kev[q + 1]);
+            acc[h->kev_class[q]] += t;
+        }
+    }
+    double by[P2G_NUM_KCLASS];
+    class_bytes(h, by);
+    for (int q = 0; q < P2G_NUM_KCLASS; ++q) {
+        if (ms) ms[q] = acc[q] / reps;
+        if (bytes) bytes[q] = by[q];
+        if (names) names[q] = kKclassNames[q];
+    }
     return P2G_OK;
 }
 

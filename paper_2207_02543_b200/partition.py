@@ -191,6 +191,27 @@ class PartitionedSolver:
         self._L.p2g_part_last_solve_ms(self._p, C.byref(ms))
         return ms.value
 
+    def stream(self) -> int:
+        """cudaStream_t of the hosted partitions (time with events on it)."""
+        return int(self._L.p2g_part_get_stream(self._p) or 0)
+
+    def launch_counts(self):
+        """(launches per iteration, running total, loop mode of the last solve)."""
+        per, tot, mode = C.c_int64(), C.c_int64(), C.c_int32()
+        self._check(self._L.p2g_part_launch_counts(self._p, C.byref(per), C.byref(tot),
+                                                   C.byref(mode)), "launch_counts")
+        return per.value, tot.value, mode.value
+
+    def profile_iteration(self, reps=3):
+        """{class: (ms per iteration, algorithmic bytes per iteration)} (one hosted partition)."""
+        ms = np.zeros(L.NUM_KCLASS)
+        by = np.zeros(L.NUM_KCLASS)
+        names = (C.c_char_p * L.NUM_KCLASS)()
+        self._check(self._L.p2g_part_profile_iteration(self._p, reps, ms.ctypes.data_as(L.D),
+                                                       by.ctypes.data_as(L.D), names),
+                    "profile_iteration")
+        return {names[i].decode(): (float(ms[i]), float(by[i])) for i in range(L.NUM_KCLASS)}
+
 
 def setup_partitioned(rp, ci, values, f, phi, world, block_size, device=0, colors=None,
                       **setup_kw):

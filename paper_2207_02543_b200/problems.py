@@ -192,6 +192,21 @@ class Mesh:
         return vals
 
 
+def _assemble_rows(self, E, r0, r1, nnz_range, nthreads=0):
+    """Values of free rows [r0, r1) (node aligned): [B][nnz_range], the
+    pattern_range(r0, r1) layout, bit-identical to assemble()'s entries."""
+    E = np.ascontiguousarray(np.atleast_2d(E), dtype=np.float64)
+    vals = np.empty((E.shape[0], nnz_range))
+    st = self._L.p2g_mesh_assemble_range(self._h, E.shape[0], E.ctypes.data_as(L.D), r0, r1,
+                                         vals.ctypes.data_as(L.D), nthreads)
+    if st != 0:
+        raise ValueError("p2g_mesh_assemble_range failed")
+    return vals
+
+
+Mesh.assemble_rows = _assemble_rows
+
+
 def normal_draws(seed: int, count: int):
     out = np.empty(count)
     L.gen().p2g_normal_draws(np.uint64(seed), count, out.ctypes.data_as(L.D))

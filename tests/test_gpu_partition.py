@@ -97,3 +97,40 @@ def test_c5_driver_end_to_end_small(gpu):
     u1 = x1[0][0]
     u2 = np.concatenate([x2[0][0], x2[1][0]])
     assert np.linalg.norm(u1 - u2) <= 1e-7 * np.linalg.norm(u1)
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_partitioned_graph_loop_equals_eager_loop(gpu, monkeypatch, world):
+    """The captured partitioned loop (conditional-WHILE graph, device-side
+    stopping) runs the same kernels in the same order as the eager host loop:
+    bit-identical solutions and equal iteration counts; launch accounting."""
+    m, rp, ci, f, V, phi = _problem(3, 2)
+    out = []
+    for eager in (False, True):
+        if eager:
+            monkeypatch.setenv("P2G_PART_EAGER", "1")
+        P, bounds, bs, st = setup_partitioned(rp, ci, V, f, phi, world, m.block_size)
+        xs, it, conv, status, hist = P.solve(bs, 1e-8, 3000, L.X0_REDUCED)
+        per, total, mode = P.launch_counts()
+        assert mode == (0 if eager else 1)
+        assert per > 0 or eager
+        out.append((np.concatenate([xs[r] for r in range(world)], axis=1), it, hist))
+        P.close()
+    (x1, it1, h1), (x0, it0, h0) = out
+    assert np.array_equal(it1, it0)
+    assert np.array_equal(x1, x0)
+    k = int(it1.max()) + 1
+    assert np.array_equal(h1[:, :k], h0[:, :k])
+
+
+def test_partitioned_profile_single_partition(gpu):
+    """p2g_part_profile_iteration: per-class times and algorithmic bytes of one
+    hosted partition's iteration (the c5 bench roofline)."""
+    m, rp, ci, f, V, phi = _problem(3, 1)
+    P, bounds, bs, st = setup_partitioned(rp, ci, V, f, phi, 1, m.block_size)
+    P.solve(bs, 1e-8, 3000, L.X0_REDUCED)
+    prof = P.profile_iteration(2)
+    P.close()
+    assert prof["gs_backward"][0] > 0 and prof["gs_backward"][1] > 0
+    assert prof["restrict"][1] > 0 and prof["prolong"][1] > 0
+    assert set(prof) >= {"halo_allreduce", "residual", "spmv_dot"}

@@ -289,3 +289,18 @@ def test_wavefront_colouring_knob_is_valid(monkeypatch):
     off = a != b
     assert np.all(colour[a[off]] != colour[b[off]])
     assert np.all(perm[1::bs] == perm[0::bs] + 1)
+
+
+@pytest.mark.parametrize("dims", [(3, 6, 4, 4, 1.5, 1.0, 1.0), (2, 14, 7, 1, 2.0, 1.0, 1.0)])
+def test_range_assembly_equals_full_assembly(dims):
+    """p2g_mesh_assemble_range (a partition's rows, the e2e input of the
+    partitioned c5 bench) gives the full assembly's entries bit for bit."""
+    m = PR.Mesh(*dims)
+    rp, ci = m.pattern()
+    E, _ = m.kl_field(np.arange(2, dtype=np.uint64), 20)
+    V = m.assemble(E)
+    d = m.block_size
+    for r0, r1 in ((0, m.n), (d * 7, d * 40), (d * 3, d * 3)):
+        prp, _ = m.pattern_range(r0, r1)
+        W = m.assemble_rows(E, r0, r1, int(prp[-1]))
+        assert np.array_equal(W, V[:, int(rp[r0]):int(rp[r1])])
