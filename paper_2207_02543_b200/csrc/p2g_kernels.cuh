@@ -1156,6 +1156,9 @@ __launch_bounds__(kBlock, Sh::W == 1 ? P2G_B1_MINB : (BS == 2 ? P2G_MINB : 2)) k
 #ifndef P2G_B1BLK_MINB
 #define P2G_B1BLK_MINB 4  // a whole node's loads in flight per lane need ~60 registers
 #endif
+#ifndef P2G_B1H_WIDE_MINB
+#define P2G_B1H_WIDE_MINB 4  // 128^3: 4 CTAs/SM (small spills) beat 3 (no spills): Kp 0.96 vs 1.03 ms, bwd 1.27 vs 1.33
+#endif
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -1378,25 +1381,46 @@ __device__ __forceinline__ double half_sum(double x) {
     return x;
 }
 
+// Each half-warp's next node-table entry (info + its two neighbour-id slots)
+// is fetched one iteration ahead, so an iteration costs one round of loads
+// (values, gathers, own block) instead of table -> ids -> gathers.
 #define P2G_B1H_NODE_LOOP(T, nb, ne, ...)                                                      \
     {                                                                                          \
         const int lane = threadIdx.x & 31, hl = lane & 15;                                     \
         const int stride_ = gridDim.x * kWarps * 2;                                            \
-        for (int base_ = (nb) + (blockIdx.x * kWarps + (threadIdx.x >> 5)) * 2; base_ < (ne);  \
-             base_ += stride_) {                                                               \
+        int base_ = (nb) + (blockIdx.x * kWarps + (threadIdx.x >> 5)) * 2;                     \
+        int4 inf_n_ = make_int4(0, 0, 0, 0);                                                   \
+        int nc0_n_ = 0, nc1_n_ = 0;                                                            \
+        auto fetch_ = [&](int b_) {                                                            \
+            const int nd_ = b_ + (lane >> 4);                                                  \
+            if (nd_ < (ne)) {                                                                  \
+                inf_n_ = __ldg(T.info + nd_);                                                  \
+                const int* nl_ = T.ncol + (size_t)nd_ * T.nmax;                                \
+                nc0_n_ = hl < T.nmax ? __ldg(nl_ + hl) : 0;                                    \
+                nc1_n_ = hl + 16 < T.nmax ? __ldg(nl_ + hl + 16) : 0;                          \
+            }                                                                                  \
+        };                                                                                     \
+        if (base_ < (ne)) fetch_(base_);                                                       \
+        for (; base_ < (ne); base_ += stride_) {                                               \
             const int node = base_ + (lane >> 4);                                              \
             const bool valid = node < (ne);                                                    \
-            int4 inf = make_int4(0, 0, 0, 0);                                                  \
-            int nc0 = 0, nc1 = 0;                                                              \
-            if (valid) {                                                                       \
-                inf = __ldg(T.info + node);                                                    \
-                const int* nl = T.ncol + (size_t)node * T.nmax;                                \
-                if (hl < T.nmax) nc0 = __ldg(nl + hl);                                         \
-                if (hl + 16 < T.nmax) nc1 = __ldg(nl + hl + 16);                               \
-            }                                                                                  \
+            const int4 inf = inf_n_;                                                           \
+            const int nc0 = nc0_n_, nc1 = nc1_n_;                                              \
+            if (base_ + stride_ < (ne)) fetch_(base_ + stride_);                               \
             __VA_ARGS__                                                                        \
         }                                                                                      \
     }
+
+// the value a lane of a node's half-warp stores: row hl's entry of v[BS]
+// (predicated selects -- no dynamic register indexing, which would spill the
+// array to local memory)
+template <int BS>
+__device__ __forceinline__ double pick_row(const double (&v)[BS], int hl) {
+    double o = v[0];
+#pragma unroll
+    for (int c = 1; c < BS; ++c) o = hl == c ? v[c] : o;
+    return o;
+}
 
 // forward sweep from zero, hex8, two nodes per warp (lower neighbours only)
 template <int BS>
@@ -1432,16 +1456,14 @@ __global__ void __launch_bounds__(kBlock, P2G_B1BLK_MINB)
                 for (int cc = 0; cc < c; ++cc) acc -= ob[c][cc] * sn[cc];
                 sn[c] = acc / ob[c][c];
             }
-#pragma unroll
-            for (int c = 0; c < BS; ++c)
-                if (hl == c) s[(size_t)nd * BS + c] = sn[c];
+            if (hl < BS) s[(size_t)nd * BS + hl] = pick_row<BS>(sn, hl);
         }
     })
 }
 
 // backward sweep, hex8, two nodes per warp (every neighbour: slots l, l + 16)
 template <int BS, bool LAST>
-__global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1BLK_MINB)
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1H_WIDE_MINB)
     k_gs_backward_b1h(Mat A, NodeTab T, const double* __restrict__ f, const double* xlo, double* s,
                       const int* active, int nb, int ne, double* part_rs, int accumulate) {
     double rs[1] = {0.0};
@@ -1479,10 +1501,10 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1BLK_MINB)
                     }
                     sn[c] = acc / ob[c][c];
                 }
+                if (hl < BS) s[(size_t)node * BS + hl] = pick_row<BS>(sn, hl);
+                if (LAST && hl == 0) {
 #pragma unroll
-                for (int c = 0; c < BS; ++c) {
-                    if (hl == c) s[(size_t)node * BS + c] = sn[c];
-                    if (LAST && hl == 0) rs[0] += fo[c] * sn[c];
+                    for (int c = 0; c < BS; ++c) rs[0] += fo[c] * sn[c];
                 }
             }
         })
@@ -1491,7 +1513,7 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1BLK_MINB)
 }
 
 template <int BS>
-__global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1BLK_MINB)
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1H_WIDE_MINB)
     k_kp_update_b1h(Mat A, NodeTab T, const double* __restrict__ r, const double* __restrict__ s,
                     const double* __restrict__ sp, double* __restrict__ Kp, double* __restrict__ p,
                     const double* beta, const int* active, double* part) {
@@ -1534,13 +1556,16 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1BLK_MINB)
 #pragma unroll
             for (int c = 0; c < BS; ++c) q[c] = half_sum(q[c]);
             if (valid) {
+                double lo[BS];  // every row's L(s - s') term; lane hl < BS keeps row hl's
 #pragma unroll
                 for (int c = 0; c < BS; ++c) {
-                    if (hl != c) continue;
                     double acc = q[c];
 #pragma unroll
                     for (int cc = 0; cc < c; ++cc) acc += ob[c][cc] * xd[cc];
-                    const double kpi = (ri + acc) + bt * kpo;
+                    lo[c] = acc;
+                }
+                if (hl < BS) {
+                    const double kpi = (ri + pick_row<BS>(lo, hl)) + bt * kpo;
                     const double pi = si + bt * po;
                     Kp[o] = kpi;
                     p[o] = pi;
@@ -1577,17 +1602,19 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1BLK_MINB)
 #pragma unroll
         for (int c = 0; c < BS; ++c) q[c] = half_sum(q[c]);
         if (valid) {
+            double tv[BS];
 #pragma unroll
             for (int c = 0; c < BS; ++c) {
-                if (hl != c) continue;
                 double acc = 0.0;
 #pragma unroll
                 for (int cc = c + 1; cc < BS; ++cc) acc += ob[c][cc] * uo[cc];
-                t[(size_t)node * BS + c] = -(acc + q[c]);
+                tv[c] = -(acc + q[c]);
             }
+            if (hl < BS) t[(size_t)node * BS + hl] = pick_row<BS>(tv, hl);
         }
     })
 }
+
 
 // Restriction c = Phi^T t (PodBasis::project, pod.hpp:27-35) of a vector
 // t[n][Bp] (the residual, or f itself for reduced_solve, pod.hpp:171).

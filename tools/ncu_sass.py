@@ -17,7 +17,13 @@ def main():
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[1]
-    data = [r for r in rows[2:] if len(r) == len(hdr)]
+    # the source page can list a kernel's SASS more than once (one block per
+    # source view); keep each instruction address once
+    data, seen = [], set()
+    for r in rows[2:]:
+        if len(r) == len(hdr) and r[0] not in seen:
+            seen.add(r[0])
+            data.append(r)
 
     def num(r, c):
         try:
