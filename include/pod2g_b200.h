@@ -265,12 +265,14 @@ int p2g_analyze_pattern(int64_t n, const uint64_t* row_offsets, const uint64_t* 
 int p2g_analyze_node_blocking(int64_t n, const uint64_t* row_offsets, const uint64_t* col_indices,
                               int32_t block_size, int32_t* blocked, int32_t* nmax);
 
-/* Per-kernel-class timing of the iteration loop: runs `reps` eager
- * iterations (no graph) with CUDA events between kernel classes on the
- * handle's stream, on the current state of the last solve (P2G_ESTATE when
- * no solve ran since p2g_setup: a zero state has p'Kp = 0).  ms receives the
- * mean time per iteration of each class, bytes the algorithmic HBM bytes per
- * iteration of each class, names the class names (static). */
+/* Per-kernel-class timing of the iteration loop: the loop body with a CUDA
+ * event after every kernel class, captured once as a plain graph and replayed
+ * `reps` times on the handle's stream (kernels back to back as in the solve;
+ * P2G_PROFILE_EAGER=1: eager launches), on the current state of the last
+ * solve (P2G_ESTATE when no solve ran since p2g_setup: a zero state has
+ * p'Kp = 0).  ms receives the mean time per iteration of each class, bytes
+ * the algorithmic HBM bytes per iteration of each class, names
+ * the class names (static). */
 #define P2G_NUM_KCLASS 11
 int p2g_profile_iteration(p2g_handle* h, int32_t reps, double* ms, double* bytes,
                           const char** names);

@@ -1696,9 +1696,9 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_restrict_vec(int n, int 
     }
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();
-    if (cl.block_rank() == 0) {
+    {  // every CTA of the cluster sums its share of the entries (same rank order)
         double* prow = part + (size_t)(blockIdx.x / kCluster) * k * Bp + blockIdx.y * Sh::T;
-        for (int e = threadIdx.x; e < k * Sh::T; e += kBlock) {
+        for (int e = threadIdx.x + (int)cl.block_rank() * kBlock; e < k * Sh::T; e += kBlock * kCluster) {
             const int a = e / Sh::T, bt = e % Sh::T;
             double tt = 0.0;
 #pragma unroll
@@ -1985,9 +1985,9 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock) k_restrict_mma(int n, int 
     }
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();
-    if (cl.block_rank() == 0) {
+    {  // every CTA of the cluster sums its share of the entries (same rank order)
         double* prow = part + (size_t)(blockIdx.x / kCluster) * k * Bp + bt0;
-        for (int q = threadIdx.x; q < k * TB; q += kBlock) {
+        for (int q = threadIdx.x + (int)cl.block_rank() * kBlock; q < k * TB; q += kBlock * kCluster) {
             double tt = 0.0;
 #pragma unroll
             for (int r = 0; r < kCluster; ++r) tt += cl.map_shared_rank(tot, r)[q];
@@ -2139,9 +2139,9 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock, KMAX > 40 ? 2 : P2G_RESTRI
     }
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();
-    if (cl.block_rank() == 0) {
+    {  // every CTA of the cluster sums its share of the entries (same rank order)
         double* prow = part + (size_t)(blockIdx.x / kCluster) * k * Bp + bt0;
-        for (int q = threadIdx.x; q < k * TB; q += kBlock) {
+        for (int q = threadIdx.x + (int)cl.block_rank() * kBlock; q < k * TB; q += kBlock * kCluster) {
             double tt = 0.0;
 #pragma unroll
             for (int r = 0; r < kCluster; ++r) tt += cl.map_shared_rank(&tot[0][0], r)[q];
@@ -2151,15 +2151,114 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock, KMAX > 40 ? 2 : P2G_RESTRI
     cl.sync();
 }
 
+// Restriction, wide form: a warp owns a PAIR of 8-instance n-blocks (16
+// instances, one 16-byte load per lane per k-step: .x feeds the "even" DMMA
+// stream, .y the "odd" one, so both B fragments come from one load) and every
+// m-block, with U k-steps of loads in flight -- fewer, fatter loop iterations
+// than k_restrict_reg (whose per-iteration latency, not bandwidth, set its
+// time: c4 343 k-steps per worker in 172 serial rounds).  Warps of a CTA
+// split the k-steps KSPLIT ways; the k-split partials are summed in smem in
+// fixed order, then the clusters' partial rows as before (deterministic).
+#ifndef P2G_RESTRICT2_MINB
+#define P2G_RESTRICT2_MINB 2
+#endif
+template <int KMAX>
+struct Restrict2Cfg {
+    static constexpr int MBX = (KMAX + 7) / 8;
+    static constexpr int U = KMAX <= 24 ? 8 : (KMAX <= 32 ? 6 : (KMAX <= 40 ? 4 : 2));
+};
+template <int TB, int KMAX>
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_RESTRICT2_MINB)
+    k_restrict_reg2(int n, int Bp, const double* __restrict__ t, const double* __restrict__ phit,
+                    int k, int ks, double* part) {
+    constexpr int NP = TB / 16, KSPLIT = kWarps / NP;
+    constexpr int MBX = Restrict2Cfg<KMAX>::MBX, U = Restrict2Cfg<KMAX>::U;
+    static_assert(TB % 16 == 0 && kWarps % NP == 0, "n-block pairs per CTA");
+    extern __shared__ __align__(16) double tot2[];  // [KMAX][TB]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, tg = lane & 3;
+    const int np = warp % NP, kpart = warp / NP;
+    const int bt0 = blockIdx.y * TB;
+    const int mb = (k + 7) / 8;
+    const int nq = (n + 3) / 4;
+    const int wk = blockIdx.x * KSPLIT + kpart, nwk = gridDim.x * KSPLIT;
+    const double* tcol = t + bt0 + 16 * np + 2 * g;
+    double ce[MBX][2], co[MBX][2];
+#pragma unroll
+    for (int m = 0; m < MBX; ++m) ce[m][0] = ce[m][1] = co[m][0] = co[m][1] = 0.0;
+    for (int q0 = wk; q0 < nq; q0 += U * nwk) {
+        double2 b[U];
+        double a[U][MBX];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int row = 4 * (q0 + u * nwk) + tg;
+            const bool ok = row < n;
+            b[u] = ok ? __ldg(reinterpret_cast<const double2*>(tcol + (size_t)row * Bp))
+                      : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int m = 0; m < MBX; ++m)
+                a[u][m] = (ok && m < mb) ? __ldg(phit + (size_t)row * ks + 8 * m + g) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int m = 0; m < MBX; ++m)
+                if (m < mb) {
+                    dmma(ce[m][0], ce[m][1], a[u][m], b[u].x);
+                    dmma(co[m][0], co[m][1], a[u][m], b[u].y);
+                }
+    }
+    // lane holds C[8m + g][instances 16 np + 4 tg + {0 (even .0), 1 (odd .0), 2 (even .1), 3 (odd .1)}]
+    for (int kp = KSPLIT - 1; kp >= 0; --kp) {  // fixed-order k-split sum
+        if (kpart == kp) {
+#pragma unroll
+            for (int m = 0; m < MBX; ++m)
+                if (8 * m + g < k) {
+                    double* d = tot2 + (size_t)(8 * m + g) * TB + 16 * np + 4 * tg;
+                    const double v0 = ce[m][0], v1 = co[m][0], v2 = ce[m][1], v3 = co[m][1];
+                    if (kp == KSPLIT - 1) {
+                        d[0] = v0; d[1] = v1; d[2] = v2; d[3] = v3;
+                    } else {
+                        d[0] = d[0] + v0; d[1] = d[1] + v1; d[2] = d[2] + v2; d[3] = d[3] + v3;
+                    }
+                }
+        }
+        __syncthreads();
+    }
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    {  // every CTA of the cluster sums its share of the entries (same rank order)
+        double* prow = part + (size_t)(blockIdx.x / kCluster) * k * Bp + bt0;
+        for (int q = threadIdx.x + (int)cl.block_rank() * kBlock; q < k * TB; q += kBlock * kCluster) {
+            double tt = 0.0;
+#pragma unroll
+            for (int r = 0; r < kCluster; ++r) tt += cl.map_shared_rank(tot2, r)[q];
+            prow[(size_t)(q / TB) * Bp + q % TB] = tt;
+        }
+    }
+    cl.sync();
+}
+
 // the CTA's warps share 8-row m-blocks (NB n-blocks each; with TB = 32 two
 // m-blocks per step); U steps of S / Phi loads issued before their MMAs
+#ifndef P2G_PROLONG_U_WIDE
+#define P2G_PROLONG_U_WIDE 2  // m-blocks in flight for 24 < KMAX <= 40 (c4: 201 vs 241 us at 1)
+#endif
+#ifndef P2G_PROLONG_MINB_WIDE
+#define P2G_PROLONG_MINB_WIDE 3
+#endif
+#ifndef P2G_PROLONG_U_NARROW
+#define P2G_PROLONG_U_NARROW 2  // m-blocks in flight for KMAX <= 24
+#endif
+#ifndef P2G_PROLONG_MINB_NARROW
+#define P2G_PROLONG_MINB_NARROW 4
+#endif
 template <int TB, int KMAX, bool ASSIGN>
-__global__ void __launch_bounds__(kBlock, KMAX > 40 ? 2 : 4) k_prolong_reg(int n, int Bp, double* s,
-                                                           const double* __restrict__ phit, int k,
-                                                           int ks, const double* __restrict__ e,
-                                                           const int* active) {
+__global__ void __launch_bounds__(kBlock, KMAX > 40 ? 2 : (KMAX > 24 ? P2G_PROLONG_MINB_WIDE : P2G_PROLONG_MINB_NARROW))
+    k_prolong_reg(int n, int Bp, double* s, const double* __restrict__ phit, int k, int ks,
+                  const double* __restrict__ e, const int* active) {
     constexpr int NB = TB / 8, MSPLIT = kWarps / NB, KQ = (KMAX + 3) / 4;
-    constexpr int U = KMAX <= 24 ? 2 : 1;  // m-blocks of loads ahead
+    constexpr int U = KMAX <= 24 ? P2G_PROLONG_U_NARROW : (KMAX <= 40 ? P2G_PROLONG_U_WIDE : 1);  // m-blocks of loads ahead
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, tg = lane & 3;
     const int nb = warp % NB, mpart = warp / NB;

@@ -211,6 +211,18 @@ int ensure(p2g_handle* h, T*& p, size_t count) {
     return P2G_OK;
 }
 
+constexpr int kProlongTmaRows = 1 << 18;  // rows from which the prolongation is TMA-staged
+
+// the wide tensor-core restriction (k_restrict_reg2); P2G_RESTRICT_WIDE=0
+// selects k_restrict_reg (A/B)
+bool restrict_wide() {
+    static const bool w = [] {
+        const char* v = std::getenv("P2G_RESTRICT_WIDE");
+        return !(v && v[0] == '0');
+    }();
+    return w;
+}
+
 int kbucket(int k) {
     if (k <= 8) return 8;
     if (k <= 16) return 16;
@@ -262,10 +274,16 @@ Mat mat_of(p2g_handle* h) {
 
 // p2g_profile_iteration: close the current timing interval (everything
 // issued on the stream since the previous mark) and charge it to `kclass`
+// (inside a stream capture the record becomes an external event-record node)
+cudaError_t prof_record(p2g_handle* h, cudaEvent_t e, cudaStream_t st) {
+    return h->capturing ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal)
+                        : cudaEventRecord(e, st);
+}
+
 void prof_mark(p2g_handle* h, int kclass) {
     if (h->profiling && h->kev_n < 63) {
         h->kev_class[h->kev_n] = kclass;
-        cudaEventRecord(h->kev[h->kev_n + 1], h->stream);
+        prof_record(h, h->kev[h->kev_n + 1], h->stream);
         ++h->kev_n;
     }
 }
@@ -689,13 +707,23 @@ struct Run {
         }
         const int k = h->k;
         const int n = static_cast<int>(h->pat.n);
-        if constexpr (Sh::S == 1) {  // batched tiles: bulk-copy pipelined restriction
+        if constexpr (Sh::S == 1) {  // batched tiles: tensor-core restriction
             constexpr int TB = Sh::T;
             KSWITCH(k, {
-                auto fn = (std::getenv("P2G_TMA") ? k_restrict_mma<TB, KM> : k_restrict_reg<TB, KM>);
-                const size_t smem = std::getenv("P2G_TMA") ? MmaTile<TB, KM>::SMEM : 0;
+                const bool tma = std::getenv("P2G_TMA") != nullptr;
+                const bool wide = TB % 16 == 0 && !tma && restrict_wide();
+                auto fn = tma ? k_restrict_mma<TB, KM>
+                              : (wide ? k_restrict_reg2<(TB % 16 == 0 ? TB : 16), KM>
+                                      : k_restrict_reg<TB, KM>);
+                const size_t smem = tma ? MmaTile<TB, KM>::SMEM
+                                        : (wide ? sizeof(double) * KM * TB : 0);
                 const int64_t need = (n + 127) / 128;
-                int64_t gx = std::min<int64_t>(need, resident_ctas(h, (const void*)fn, true, smem));
+                // every instance tile (grid.y) co-resident in ONE wave, marching over
+                // the same rows together: a Phi row read from DRAM serves every tile
+                // from L2 (one wave per tile re-streamed Phi once per tile)
+                const int64_t tiles = h->Bp / TB;
+                int64_t gx = std::min<int64_t>(
+                    need, std::max<int64_t>(resident_ctas(h, (const void*)fn, true, smem) / tiles, kCluster));
                 gx = std::min<int64_t>(std::max<int64_t>(gx, 1), h->nb_cap);
                 gx = (gx + kCluster - 1) / kCluster * kCluster;
                 dim3 g((unsigned)gx, (unsigned)(h->Bp / TB));
@@ -736,12 +764,16 @@ struct Run {
         if constexpr (Sh::S == 1) {  // batched tiles: bulk-copy pipelined prolongation
             constexpr int TB = Sh::T;
             KSWITCH(k, {
-                const bool tma = std::getenv("P2G_TMA") != nullptr;
+                // the TMA-staged (bulk copy + mbarrier) form pays on large systems
+                // (c3 975 vs 1100 us, c4 190 vs 201), not on c2 (21 vs 18.5 us)
+                const bool tma = std::getenv("P2G_TMA") != nullptr || n >= kProlongTmaRows;
                 auto fn = tma ? (assign ? k_prolong_mma<TB, KM, true> : k_prolong_mma<TB, KM, false>)
                               : (assign ? k_prolong_reg<TB, KM, true> : k_prolong_reg<TB, KM, false>);
                 const size_t smem = tma ? MmaTile<TB, KM>::SMEM : 0;
                 const int64_t need = (n + 31) / 32;
-                int64_t gx = std::min<int64_t>(need, resident_ctas(h, (const void*)fn, false, smem));
+                const int64_t tiles = h->Bp / TB;  // all tiles in one wave (Phi rows shared via L2)
+                int64_t gx = std::min<int64_t>(
+                    need, std::max<int64_t>(resident_ctas(h, (const void*)fn, false, smem) / tiles, 1));
                 dim3 g((unsigned)std::max<int64_t>(gx, 1), (unsigned)(h->Bp / TB));
                 fn<<<g, kBlock, smem, h->stream>>>(n, h->Bp, s, h->d_phit, k, h->phi_ks, h->d_e,
                                                    h->d_active);
@@ -2061,6 +2093,38 @@ int p2g_profile_iteration(p2g_handle* h, int32_t reps, double* ms, double* bytes
         SolveParams prm{0.0, (long long)1 << 62, 0};
         CU(cudaMemcpyAsync(h->d_prm, &prm, sizeof(prm), cudaMemcpyHostToDevice, h->stream));
     }
+    // The loop body with a CUDA event after every kernel class, captured as a
+    // plain graph and replayed: kernels follow each other as in the solve's
+    // graph (no host launch gap between them), and the event-record nodes time
+    // each class on the device.  P2G_PROFILE_EAGER=1: eager launches instead.
+    const char* pe = std::getenv("P2G_PROFILE_EAGER");
+    const bool eager = pe && pe[0] == '1';
+    auto body = [&]() -> int {
+        h->profiling = true;
+        h->kev_n = 0;
+        CU(prof_record(h, h->kev[0], h->stream));
+        const int st = dispatch(h, [&](auto R) -> int { return decltype(R)::iteration(h, false); });
+        h->profiling = false;
+        return st;
+    };
+    cudaGraphExec_t ge = nullptr;
+    if (!eager) {
+        CU(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
+        h->capturing = true;
+        const int st = body();
+        h->capturing = false;
+        cudaGraph_t g = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(h->stream, &g);
+        TRY(st);
+        CU(ce);
+        const cudaError_t ie = cudaGraphInstantiate(&ge, g, 0);
+        cudaGraphDestroy(g);
+        CU(ie);
+    }
+    struct ExecGuard {
+        cudaGraphExec_t e;
+        ~ExecGuard() { if (e) cudaGraphExecDestroy(e); }
+    } guard{ge};
     for (int rep = 0; rep < reps; ++rep) {
         CU(cudaMemcpyAsync(h->d_active, h->d_all, sizeof(int) * h->Bp, cudaMemcpyDeviceToDevice,
                            h->stream));
@@ -2068,12 +2132,11 @@ int p2g_profile_iteration(p2g_handle* h, int32_t reps, double* ms, double* bytes
             // the body starts at alpha: refresh Kp and the pKp partials first
             TRY(dispatch(h, [&](auto R) -> int { return decltype(R)::spmv(h, h->d_p, h->d_Kp, true, nullptr); }));
         }
-        h->profiling = true;
-        h->kev_n = 0;
-        CU(cudaEventRecord(h->kev[0], h->stream));
-        int st = dispatch(h, [&](auto R) -> int { return decltype(R)::iteration(h, false); });
-        h->profiling = false;
-        TRY(st);
+        if (ge) {
+            CU(cudaGraphLaunch(ge, h->stream));
+        } else {
+            TRY(body());
+        }
         CU(cudaStreamSynchronize(h->stream));
         for (int q = 0; q < h->kev_n; ++q) {
             float t = 0;
@@ -3041,12 +3104,38 @@ int p2g_part_profile_iteration(p2g_part* P, int32_t reps, double* ms, double* by
                 return Rn::spmv(h, h->d_p, h->d_Kp, true, nullptr);
             }));
         }
-        h->profiling = true;
-        h->kev_n = 0;
-        PCU(cudaEventRecord(h->kev[0], P->stream));
-        const int st = pdispatch(P, [&](auto R) -> int { return decltype(R)::iteration(P); });
-        h->profiling = false;
-        PTRY(st);
+        // as p2g_profile_iteration: the body captured with its event nodes and
+        // replayed as a graph (P2G_PROFILE_EAGER=1: eager)
+        const char* pe = std::getenv("P2G_PROFILE_EAGER");
+        const bool eager = pe && pe[0] == '1';
+        auto body = [&]() -> int {
+            h->profiling = true;
+            h->kev_n = 0;
+            PCU(prof_record(h, h->kev[0], P->stream));
+            const int st = pdispatch(P, [&](auto R) -> int { return decltype(R)::iteration(P); });
+            h->profiling = false;
+            return st;
+        };
+        if (eager) {
+            PTRY(body());
+        } else {
+            PCU(cudaStreamBeginCapture(P->stream, cudaStreamCaptureModeRelaxed));
+            h->capturing = true;
+            const int st = body();
+            h->capturing = false;
+            cudaGraph_t g = nullptr;
+            const cudaError_t ce = cudaStreamEndCapture(P->stream, &g);
+            PTRY(st);
+            PCU(ce);
+            cudaGraphExec_t ge = nullptr;
+            const cudaError_t ie = cudaGraphInstantiate(&ge, g, 0);
+            cudaGraphDestroy(g);
+            PCU(ie);
+            const cudaError_t le = cudaGraphLaunch(ge, P->stream);
+            cudaStreamSynchronize(P->stream);
+            cudaGraphExecDestroy(ge);
+            PCU(le);
+        }
         PCU(cudaStreamSynchronize(P->stream));
         for (int q = 0; q < h->kev_n; ++q) {
             float t = 0;
