@@ -25,7 +25,15 @@ s.assemble(m, E)
 s.set_basis(phi)
 s.setup()
 s.solve(f[None, :], None, 1e-8, 5, x0_mode=L.X0_REDUCED, hist_cap=0)
+try:  # NVTX range "profile" around the profiled iterations (ncu --nvtx-include profile/)
+    import torch
+    torch.cuda.nvtx.range_push("profile")
+except Exception:
+    torch = None
 prof = s.profile_iteration(reps)
+if torch is not None:
+    torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
 tot = sum(v[0] for v in prof.values())
 pk = 6451.8
 for kname, (ms_, by) in prof.items():

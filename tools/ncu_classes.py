@@ -81,8 +81,9 @@ def full(path, out):
         print("%-18s %9d %9.1f %7.1f%% %9.1f %7.0f" % (
             c, a["launches"], a["us"], 100 * a["us"] / tot, a["dram_bytes"] / 1e6,
             a["dram_bytes"] / (a["us"] * 1e-6) / 1e9 if a["us"] else 0))
-    res = {"source": path, "capture": "ncu --set full --clock-control none, one PCG iteration "
-                                      "(last k_alpha .. end) of tools/ncu_iter.py",
+    res = {"source": path, "capture": "ncu --set full --clock-control none --cache-control all, "
+                                      "one PCG iteration (last k_alpha .. end) of the eager profile "
+                                      "(tools/ncu_iter.py / ncu_b1.py, NVTX range 'profile')",
            "per_iteration_dram_bytes": {c: a["dram_bytes"] for c, a in agg.items()},
            "per_iteration_us": {c: a["us"] for c, a in agg.items()},
            "launches_per_iteration": {c: a["launches"] for c, a in agg.items()},
@@ -90,6 +91,20 @@ def full(path, out):
     if out:
         with open(out, "w") as fh:
             json.dump(res, fh, indent=1)
+    if "--traffic" in sys.argv:  # merge into profiles/ncu_traffic.json under this config
+        cfg = sys.argv[sys.argv.index("--traffic") + 1]
+        tp = "profiles/ncu_traffic.json"
+        try:
+            with open(tp) as fh:
+                allt = json.load(fh)
+        except Exception:
+            allt = {}
+        allt[cfg] = {"source": path, "capture": res["capture"],
+                     "per_iteration_dram_bytes": res["per_iteration_dram_bytes"],
+                     "per_iteration_us": res["per_iteration_us"],
+                     "launches_per_iteration": res["launches_per_iteration"]}
+        with open(tp, "w") as fh:
+            json.dump(allt, fh, indent=1, sort_keys=True)
 
 
 def launches(path, out):

@@ -25,7 +25,15 @@ F = np.broadcast_to(f, (cfg.batch, m.n)).copy()
 import os
 if not os.environ.get('NO_SOLVE'):
     s.solve(F, None, 1e-8, 3, x0_mode=L.X0_REDUCED)
+try:  # NVTX range "profile" around the profiled iterations (ncu --nvtx-include profile/)
+    import torch
+    torch.cuda.nvtx.range_push("profile")
+except Exception:
+    torch = None
 prof = s.profile_iteration(reps)
+if torch is not None:
+    torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
 tot = sum(v[0] for v in prof.values())
 for kname, (ms_, by) in prof.items():
     gbs = by / (ms_ * 1e-3) / 1e9 if ms_ > 0 else 0
