@@ -184,6 +184,34 @@ def cpu_reference_run(prob, values, F, instances, jobs):
     return dt, it
 
 
+# Large configs: one reference solve takes minutes per core (c3 ~160 s, c4 ~100 s), so
+# a step times a bounded PREFIX of every solve instead -- per instance the setup
+# (reduced_solve x0 + Pod2gPreconditioner: A_c, LU; max_iter = 0) and the first
+# REF_PREFIX PCG iterations, all instances in parallel -- and extrapolates with
+# the reference's own natural-order mean iteration count on that config, measured
+# with full solves on the GPU box in round 1 (profiles/r01_configs/bench_cN.json).
+REF_PREFIX = 10
+REF_ITERS = {"c3": 668.8, "c4": 139.3}
+
+
+def cpu_reference_prefix(prob, values, F, instances, jobs, nref):
+    """(extrapolated seconds for `instances` full solves in parallel, setup s, s/iteration)."""
+    from oracle.bindings import Reference
+    R = Reference()
+    args = (prob.rp.astype(np.int64), prob.ci.astype(np.int64), values[:instances],
+            F[:instances], prob.phi, 1, prob.cfg.tol)
+    t = time.perf_counter()
+    R.pcg_pod2g_batch(*args, 0, jobs)
+    t0 = time.perf_counter() - t
+    t = time.perf_counter()
+    _, it, _, failed = R.pcg_pod2g_batch(*args, REF_PREFIX, jobs)
+    tp = time.perf_counter() - t
+    if np.any(failed):
+        raise RuntimeError("reference CPU arm: an instance failed")
+    t_iter = max(tp - t0, 0.0) / REF_PREFIX
+    return t0 + nref * t_iter, t0, t_iter
+
+
 def pin_limit():
     """largest value batch to pin (the pinned copy doubles its host footprint)"""
     try:
@@ -367,11 +395,22 @@ def main():
     if rank == 0 and ws == 1 and not args.no_cpu:
         ninst = args.cpu_instances or min(B, cores)
         try:
-            dt, cit = cpu_reference_run(prob, values, F, ninst, cores)
-            cpu = {"value": ninst / dt, "unit": UNIT, "cores": cores, "kind": "reference",
-                   "sample": f"{ninst} of the {B} {cfg.name} instances, natural-order SGS "
-                             f"(reference default), x0=reduced_solve, tol {cfg.tol:g}; "
-                             f"mean iterations {float(np.mean(cit)):.1f}; {dt:.2f} s wall"}
+            if cfg.name in REF_ITERS:
+                est, t0s, t_it = cpu_reference_prefix(prob, values, F, ninst, cores,
+                                                      REF_ITERS[cfg.name])
+                cpu = {"value": ninst / est, "unit": UNIT, "cores": cores, "kind": "reference",
+                       "extrapolated": True,
+                       "sample": f"{ninst} of the {B} {cfg.name} instances in parallel, "
+                                 f"natural-order SGS, x0=reduced_solve: setup {t0s:.2f} s + "
+                                 f"first {REF_PREFIX} PCG iterations ({t_it:.3f} s each) timed, "
+                                 f"extrapolated to the reference's {REF_ITERS[cfg.name]} mean "
+                                 f"iterations (round-1 full solves on this box type)"}
+            else:
+                dt, cit = cpu_reference_run(prob, values, F, ninst, cores)
+                cpu = {"value": ninst / dt, "unit": UNIT, "cores": cores, "kind": "reference",
+                       "sample": f"{ninst} of the {B} {cfg.name} instances, natural-order SGS "
+                                 f"(reference default), x0=reduced_solve, tol {cfg.tol:g}; "
+                                 f"mean iterations {float(np.mean(cit)):.1f}; {dt:.2f} s wall"}
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": cores, "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -585,9 +624,12 @@ def reference_arm(args, cfg, PR, cores, ws):
     seeds = PR.query_seeds(cfg, ninst)
     values = mesh.assemble(mesh.kl_field(seeds, cfg.kl_terms)[0])
     F = np.ascontiguousarray(np.broadcast_to(f, (ninst, mesh.n)))
-    times = []
+    times, prefix = [], cfg.name in REF_ITERS
     for i in range(args.warmup + args.steps):
-        dt, it = cpu_reference_run(prob, values, F, ninst, cores)
+        if prefix:  # bounded sample, extrapolated (see REF_ITERS)
+            dt, t0s, t_it = cpu_reference_prefix(prob, values, F, ninst, cores, REF_ITERS[cfg.name])
+        else:
+            dt, it = cpu_reference_run(prob, values, F, ninst, cores)
         if i >= args.warmup:
             times.append(dt)
     tot = sum(times)
@@ -602,8 +644,12 @@ def reference_arm(args, cfg, PR, cores, ws):
                    "tol": cfg.tol, "x0": "reduced_solve",
                    "smoother": "natural-order symmetric GS (reference default)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "extrapolated": prefix,
                          "sample": f"{ninst} {cfg.name} instances per step, one per host core "
-                                   f"(parallel_for), natural-order SGS, x0=reduced_solve"},
+                                   f"(parallel_for), natural-order SGS, x0=reduced_solve"
+                                   + (f"; per step setup + first {REF_PREFIX} PCG iterations "
+                                      f"timed, extrapolated to {REF_ITERS.get(cfg.name)} "
+                                      f"iterations" if prefix else "")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -617,6 +663,19 @@ def _basis_for_reference(cfg, PR, mesh, rp, ci, f, jobs):
     input generator (mesh, KL field) is ours."""
     from oracle.bindings import Reference
     R = Reference()
+    if cfg.name in REF_ITERS:
+        # 10^6-dof systems: Jacobi-PCG snapshots would take ~hours on the host;
+        # the reference's pcg_solve + Pod2gPreconditioner over the smooth
+        # degree <= 3 displacement modes instead, 2 snapshots per core (>= k + 2)
+        from paper_2207_02543_b200 import c5 as C5
+        nsnap = max(cfg.k + 2, min(cfg.n_snapshots, 2 * jobs))
+        S = C5.smooth_space(mesh, np.arange(mesh.n, dtype=np.int64))
+        boot = np.ascontiguousarray(S @ np.linalg.inv(np.linalg.cholesky(S.T @ S).T))
+        vals = mesh.assemble(mesh.kl_field(PR.snapshot_seeds(cfg, nsnap), cfg.kl_terms)[0])
+        F = np.ascontiguousarray(np.broadcast_to(f, (len(vals), mesh.n)))
+        phi = R.offline_basis_pod2g(rp.view(np.int64), ci.view(np.int64), vals, F, cfg.k, boot,
+                                    PR.SNAP_TOL, jobs)
+        return PR.Problem(cfg, mesh, rp, ci, f, phi, np.zeros(0), np.zeros(0))
     vals = mesh.assemble(mesh.kl_field(PR.snapshot_seeds(cfg), cfg.kl_terms)[0])
     F = np.ascontiguousarray(np.broadcast_to(f, (len(vals), mesh.n)))
     phi = R.offline_basis(rp.astype(np.int64), ci.astype(np.int64), vals, F, cfg.k,

@@ -302,6 +302,9 @@ class Reference:
                                           _I64, _I32, _I32, C.c_int]
         L.ref_offline_basis.argtypes = [C.c_int64, _I64, _I64, C.c_int64, _D, C.c_int64, _D,
                                          C.c_double, C.c_int64, C.c_int, _D, _I64]
+        L.ref_offline_basis_pod2g.argtypes = [C.c_int64, _I64, _I64, C.c_int64, _D, C.c_int64, _D,
+                                              C.c_double, C.c_int64, C.c_int, C.c_int64, _D, _D,
+                                              _I64]
         L.ref_compute_pod.argtypes = [C.c_int64, C.c_int64, _D, C.c_double, C.c_int64, _D,
                                       _I64, _D, _D]
         L.ref_its_case.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
@@ -503,6 +506,19 @@ class Reference:
                                              _d(eig), C.byref(en)))
         return np.ascontiguousarray(phi.reshape(-1)[: d * r.value].reshape(d, r.value)), eig, \
             en.value
+
+    def offline_basis_pod2g(self, rp, ci, values, F, rank, phi0, tol=1e-10, jobs=1):
+        """Snapshots (pcg_solve + Pod2gPreconditioner over bootstrap basis phi0,
+        generate_snapshots' tolerance ladder) + compute_pod(RankTarget{rank})."""
+        rp, ci, values, F, phi0 = _ix(rp), _ix(ci), _f64(values), _f64(F), _f64(phi0)
+        N, nnz = values.shape
+        n = len(rp) - 1
+        phi = np.empty((n, rank))
+        r = C.c_int64()
+        self._check(self.lib.ref_offline_basis_pod2g(n, _i64(rp), _i64(ci), nnz, _d(values), N,
+                                                     _d(F), tol, rank, jobs, phi0.shape[1],
+                                                     _d(phi0), _d(phi), C.byref(r)))
+        return np.ascontiguousarray(phi[:, : r.value])
 
     def its_case(self, res=32, n_snapshots=100, offline_seed=42, bench_seed=7, inst=0, jobs=8):
         n, nnz, rank = C.c_int64(), C.c_int64(), C.c_int64()

@@ -338,6 +338,45 @@ int ref_compute_pod(int64_t N, int64_t d, const double* U, double target, int64_
     });
 }
 
+// Snapshots for the large configs' reference arm (c3, c4), where the Jacobi-PCG
+// ladder of generate_snapshots needs thousands of iterations per 10^6-dof
+// snapshot: the same ladder (delta, delta/10, delta/100, true-residual check,
+// parallel_for over samples) with the reference's own pcg_solve and
+// Pod2gPreconditioner over a caller-given bootstrap basis (phi0, n x k0, the
+// smooth displacement modes), then compute_pod(RankTarget{rank}).
+int ref_offline_basis_pod2g(int64_t n, const int64_t* rp, const int64_t* ci, int64_t nnz,
+                            const double* values, int64_t N, const double* f, double tolerance,
+                            int64_t rank, int jobs, int64_t k0, const double* phi0, double* phi,
+                            int64_t* rank_out) {
+    return guarded([&] {
+        auto boot = std::make_shared<const PodBasis>(make_basis(n, k0, phi0));
+        std::vector<Vector> sols(static_cast<size_t>(N));
+        parallel_for(static_cast<index_t>(N), static_cast<index_t>(jobs), [&](index_t i) {
+            auto K = std::make_shared<const CsrMatrix>(make_csr(n, rp, ci, values + i * nnz));
+            const Vector ff(f + i * n, f + (i + 1) * n);
+            const Pod2gPreconditioner T(K, boot, 1, 1);
+            const index_t max_iter = 10 * K->nrows;
+            Vector u(K->nrows, 0.0);
+            const double fnorm = norm2(ff);
+            double true_rel = std::numeric_limits<double>::infinity();
+            for (double delta : {tolerance, tolerance / 10.0, tolerance / 100.0}) {
+                auto [sol, rep] = pcg_solve(*K, ff, T, u, delta, max_iter);
+                u = std::move(sol);
+                Vector r;
+                residual(*K, ff, u, r);
+                true_rel = fnorm > 0.0 ? norm2(r) / fnorm : norm2(r);
+                if (true_rel <= tolerance) break;
+            }
+            if (true_rel > tolerance)
+                throw std::runtime_error("snapshot " + std::to_string(i) + " failed");
+            sols[i] = std::move(u);
+        });
+        const PodBasis b = compute_pod(sols, RankTarget{static_cast<index_t>(rank)});
+        *rank_out = static_cast<int64_t>(b.rank);
+        std::memcpy(phi, b.phi_r.data.data(), sizeof(double) * b.phi_r.data.size());
+    });
+}
+
 // Known-answer case from the reference's own acceptance run: the `its`
 // problem (problems.hpp:99-177, make_its_problem :399-407) at resolution `res`,
 // offline basis exactly as run_offline builds it (bench.hpp:58-64: LHS seed,
