@@ -195,21 +195,17 @@ REF_ITERS = {"c3": 668.8, "c4": 139.3}
 
 
 def cpu_reference_prefix(prob, values, F, instances, jobs, nref):
-    """(extrapolated seconds for `instances` full solves in parallel, setup s, s/iteration)."""
+    """(extrapolated seconds for `instances` full solves in parallel, setup s, s/iteration):
+    per instance, its measured setup (x0 + A_c + LU) plus nref x its measured seconds per
+    PCG iteration over the first REF_PREFIX iterations; the batch takes the slowest."""
     from oracle.bindings import Reference
     R = Reference()
-    args = (prob.rp.astype(np.int64), prob.ci.astype(np.int64), values[:instances],
-            F[:instances], prob.phi, 1, prob.cfg.tol)
-    t = time.perf_counter()
-    R.pcg_pod2g_batch(*args, 0, jobs)
-    t0 = time.perf_counter() - t
-    t = time.perf_counter()
-    _, it, _, failed = R.pcg_pod2g_batch(*args, REF_PREFIX, jobs)
-    tp = time.perf_counter() - t
-    if np.any(failed):
-        raise RuntimeError("reference CPU arm: an instance failed")
-    t_iter = max(tp - t0, 0.0) / REF_PREFIX
-    return t0 + nref * t_iter, t0, t_iter
+    it, su, lo = R.pcg_pod2g_batch_timed(prob.rp.astype(np.int64), prob.ci.astype(np.int64),
+                                         values[:instances], F[:instances], prob.phi,
+                                         prob.cfg.tol, REF_PREFIX, jobs)
+    t_it = lo / np.maximum(it, 1)
+    est = float(np.max(su + nref * t_it))
+    return est, float(np.mean(su)), float(np.mean(t_it))
 
 
 def pin_limit():

@@ -305,6 +305,9 @@ class Reference:
         L.ref_offline_basis_pod2g.argtypes = [C.c_int64, _I64, _I64, C.c_int64, _D, C.c_int64, _D,
                                               C.c_double, C.c_int64, C.c_int, C.c_int64, _D, _D,
                                               _I64]
+        L.ref_pcg_pod2g_batch_timed.argtypes = [C.c_int64, _I64, _I64, C.c_int64, _D, C.c_int64,
+                                                _D, C.c_int64, _D, C.c_double, C.c_int64, _I64,
+                                                _I32, _D, _D, C.c_int]
         L.ref_compute_pod.argtypes = [C.c_int64, C.c_int64, _D, C.c_double, C.c_int64, _D,
                                       _I64, _D, _D]
         L.ref_its_case.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
@@ -481,6 +484,22 @@ class Reference:
             delta, max_iter, _d(u), _i64(it), conv.ctypes.data_as(_I32),
             failed.ctypes.data_as(_I32), jobs))
         return u, it, conv, failed
+
+    def pcg_pod2g_batch_timed(self, rp, ci, values, f, phi, delta, max_iter, jobs=1):
+        """Per instance: (iterations, setup seconds, PCG loop seconds), x0 = reduced_solve."""
+        rp, ci = _ix(rp), _ix(ci)
+        values, f, phi = _f64(values), _f64(f), _f64(phi)
+        B, nnz = values.shape
+        n = len(rp) - 1
+        it = np.empty(B, dtype=np.int64)
+        failed = np.empty(B, dtype=np.int32)
+        su, lo = np.empty(B), np.empty(B)
+        self._check(self.lib.ref_pcg_pod2g_batch_timed(
+            n, _i64(rp), _i64(ci), nnz, _d(values), B, _d(f), phi.shape[1], _d(phi), delta,
+            max_iter, _i64(it), failed.ctypes.data_as(_I32), _d(su), _d(lo), jobs))
+        if np.any(failed):
+            raise RuntimeError("reference pcg_solve failed on an instance")
+        return it, su, lo
 
     def offline_basis(self, rp, ci, values, F, rank, tol=1e-10, jobs=1):
         """Snapshots (Jacobi-PCG ladder) + compute_pod(RankTarget{rank})."""

@@ -281,6 +281,35 @@ int ref_pcg_pod2g_batch(int64_t n, const int64_t* rp, const int64_t* ci, int64_t
     });
 }
 
+// ref_pcg_pod2g_batch with per-instance timings (steady_clock): setup_s =
+// reduced_solve x0 + Pod2gPreconditioner construction, loop_s = pcg_solve's
+// SolveReport::wall_time_s -- the bounded CPU samples of the large configs.
+int ref_pcg_pod2g_batch_timed(int64_t n, const int64_t* rp, const int64_t* ci, int64_t nnz,
+                              const double* values, int64_t B, const double* f, int64_t k,
+                              const double* phi, double delta, int64_t max_iter, int64_t* iters,
+                              int* failed, double* setup_s, double* loop_s, int jobs) {
+    return guarded([&] {
+        auto basis = std::make_shared<const PodBasis>(make_basis(n, k, phi));
+        parallel_for(static_cast<index_t>(B), static_cast<index_t>(jobs), [&](index_t b) {
+            auto K = std::make_shared<const CsrMatrix>(make_csr(n, rp, ci, values + b * nnz));
+            const Vector ff(f + b * n, f + (b + 1) * n);
+            try {
+                const auto t0 = std::chrono::steady_clock::now();
+                Vector u0 = reduced_solve(*K, ff, *basis).first;
+                Pod2gPreconditioner T(K, basis, 1, 1);
+                setup_s[b] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                auto res = pcg_solve(*K, ff, T, u0, delta, static_cast<index_t>(max_iter));
+                loop_s[b] = res.second.wall_time_s;
+                iters[b] = static_cast<int64_t>(res.second.cycles);
+                failed[b] = 0;
+            } catch (const std::runtime_error&) {
+                failed[b] = 1;
+                iters[b] = 0;
+            }
+        });
+    });
+}
+
 // Offline stage with the reference's own solvers, for the reference CPU arm:
 // snapshots as generate_snapshots solves them (problems.hpp:489-519: Jacobi-PCG,
 // tolerance ladder delta, delta/10, delta/100, true-residual check,

@@ -15,9 +15,9 @@ if [ -z "$NO_B1" ]; then
     --cache-control all --nvtx --nvtx-include "profile/" -o /tmp/iter_b1 \
     python tools/ncu_b1.py 160 40 1 > gpurun_out/prof/ncu_b1.log 2>&1; echo "b1 ncu=$?"
   ncu -i /tmp/iter_b1.ncu-rep --page raw --csv | gzip > gpurun_out/prof/iter_b1_raw.csv.gz
-  cp /tmp/iter_b1.ncu-rep gpurun_out/prof/ 2>/dev/null
+
 fi
-cp /tmp/iter_c2.ncu-rep gpurun_out/prof/ 2>/dev/null
+
 # launch list of the default bench command (eager loop: every kernel visible)
 P2G_EAGER_LOOP=1 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/prof/launches_c2.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu \
