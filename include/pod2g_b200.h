@@ -281,6 +281,13 @@ int p2g_profile_iteration(p2g_handle* h, int32_t reps, double* ms, double* bytes
  * launched on it; callers time with CUDA events recorded on this stream. */
 void* p2g_get_stream(const p2g_handle* h);
 
+/* Test hook.  With P2G_GUARD=1 in the environment (read once, at the first
+ * allocation) every handle buffer carries a guard band of a fixed byte
+ * pattern on each side; this returns the number of guard bands that changed
+ * (out-of-bounds device writes) over all live handles, -1 when guard mode is
+ * off, -2 on a CUDA error. */
+int p2g_debug_guard_check(void);
+
 /* Kernel launches of one loop iteration, and the running total of every
  * kernel this handle has executed (setup, prologue and graph iterations). */
 int p2g_launch_counts(const p2g_handle* h, int64_t* per_iteration, int64_t* total_executed);

@@ -60,6 +60,7 @@ SIGNATURES = [
     ("p2g_profile_iteration", C.c_int, [H, C.c_int32, D, D, C.POINTER(C.c_char_p)]),
     ("p2g_launch_counts", C.c_int, [H, I64, I64]),
     ("p2g_get_stream", C.c_void_p, [H]),
+    ("p2g_debug_guard_check", C.c_int, []),
     ("p2g_nccl_unique_id", C.c_int, [C.c_void_p]),
     ("p2g_part_create_local", C.c_int, [C.c_int, C.c_int, C.POINTER(H)]),
     ("p2g_part_create_nccl", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(H)]),

@@ -28,6 +28,8 @@
 #include "../../include/pod2g_gen.h"
 
 #include <dlfcn.h>
+#include <mutex>
+#include <unordered_map>
 #include <nccl.h>
 
 using namespace p2g;
@@ -180,9 +182,42 @@ namespace {
         if (st_ != P2G_OK) return st_;  \
     } while (0)
 
+// ---- guard bands (P2G_GUARD=1, debugging / tests): every handle buffer gets
+// kGuardBytes of a fixed byte pattern on each side; p2g_debug_guard_check()
+// reports buffers whose bands changed, i.e. out-of-bounds device writes.
+// (compute-sanitizer is not available on the GPU pool this was built on.)
+constexpr size_t kGuardBytes = 256;
+constexpr unsigned char kGuardByte = 0xA5;
+struct GuardRegistry {
+    std::mutex mu;
+    std::unordered_map<void*, size_t> bytes;  // user pointer -> user bytes
+};
+GuardRegistry& guards() {
+    static GuardRegistry g;
+    return g;
+}
+bool guard_mode() {
+    static const bool on = [] {
+        const char* v = std::getenv("P2G_GUARD");
+        return v && v[0] == '1';
+    }();
+    return on;
+}
+
 template <class T>
 void dfree(T*& p) {
-    if (p) cudaFree(p);
+    if (p) {
+        void* raw = p;
+        if (guard_mode()) {
+            std::lock_guard<std::mutex> lk(guards().mu);
+            auto it = guards().bytes.find((void*)p);
+            if (it != guards().bytes.end()) {
+                raw = (unsigned char*)(void*)p - kGuardBytes;
+                guards().bytes.erase(it);
+            }
+        }
+        cudaFree(raw);
+    }
     p = nullptr;
 }
 
@@ -190,7 +225,18 @@ template <class T>
 int dalloc(p2g_handle* h, T*& p, size_t count) {
     dfree(p);
     if (count == 0) count = 1;
-    CU(cudaMalloc(&p, count * sizeof(T)));
+    if (!guard_mode()) {
+        CU(cudaMalloc(&p, count * sizeof(T)));
+        return P2G_OK;
+    }
+    const size_t bytes = count * sizeof(T);
+    unsigned char* raw = nullptr;
+    CU(cudaMalloc(&raw, bytes + 2 * kGuardBytes));
+    CU(cudaMemset(raw, kGuardByte, kGuardBytes));
+    CU(cudaMemset(raw + kGuardBytes + bytes, kGuardByte, kGuardBytes));
+    p = reinterpret_cast<T*>(raw + kGuardBytes);
+    std::lock_guard<std::mutex> lk(guards().mu);
+    guards().bytes[(void*)p] = bytes;
     return P2G_OK;
 }
 
@@ -2155,6 +2201,27 @@ int p2g_profile_iteration(p2g_handle* h, int32_t reps, double* ms, double* bytes
 }
 
 void* p2g_get_stream(const p2g_handle* h) { return h ? (void*)h->stream : nullptr; }
+
+int p2g_debug_guard_check(void) {
+    if (!guard_mode()) return -1;
+    if (cudaDeviceSynchronize() != cudaSuccess) return -2;
+    std::lock_guard<std::mutex> lk(guards().mu);
+    int bad = 0;
+    std::vector<unsigned char> band(kGuardBytes);
+    for (const auto& [p, bytes] : guards().bytes) {
+        const unsigned char* u = static_cast<const unsigned char*>(p);
+        for (const unsigned char* b : {u - kGuardBytes, u + bytes}) {
+            if (cudaMemcpy(band.data(), b, kGuardBytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+                return -2;
+            for (unsigned char c : band)
+                if (c != kGuardByte) {
+                    ++bad;
+                    break;
+                }
+        }
+    }
+    return bad;
+}
 
 int p2g_launch_counts(const p2g_handle* h, int64_t* per_iteration, int64_t* last_solve_total) {
     if (!h) return P2G_EINVAL;
