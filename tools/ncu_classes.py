@@ -22,7 +22,7 @@ CLASSES = [
     ("update_presmooth", r"^(void )?(p2g::)?k_(update_pre|update_rows|jacobi)\b"),
     ("gs_forward", r"^(void )?(p2g::)?k_gs_forward\w*\b"),
     ("residual", r"^(void )?(p2g::)?k_residual\w*\b"),
-    ("restrict", r"^(void )?(p2g::)?k_(restrict_vec|restrict_tiled|restrict_reg|restrict_mma)\b"),
+    ("restrict", r"^(void )?(p2g::)?k_restrict_(vec|tiled|reg2?|mma)\b"),
     ("coarse_solve", r"^(void )?(p2g::)?k_coarse\b"),
     ("prolong", r"^(void )?(p2g::)?k_prolong(_tiled|_reg|_mma)?\b"),
     ("gs_backward", r"^(void )?(p2g::)?k_gs_backward\w*\b"),
