@@ -388,6 +388,7 @@ def main():
 
     # ---- CPU baseline: the reference itself on host cores, bounded sample
     cpu = None
+    natural_iters = REF_ITERS.get(cfg.name)  # the reference's natural-order SGS count
     if rank == 0 and ws == 1 and not args.no_cpu:
         ninst = args.cpu_instances or min(B, cores)
         try:
@@ -403,6 +404,7 @@ def main():
                                  f"iterations (round-1 full solves on this box type)"}
             else:
                 dt, cit = cpu_reference_run(prob, values, F, ninst, cores)
+                natural_iters = float(np.mean(cit))
                 cpu = {"value": ninst / dt, "unit": UNIT, "cores": cores, "kind": "reference",
                        "sample": f"{ninst} of the {B} {cfg.name} instances, natural-order SGS "
                                  f"(reference default), x0=reduced_solve, tol {cfg.tol:g}; "
@@ -425,6 +427,7 @@ def main():
                        "l2": "inputs larger than L2 (values %.0f MB per GPU)" % (values.nbytes / 1e6),
                        "parallelism": f"instance-sharded x{ws}",
                        "iterations_mean": float(np.mean(iters)),
+                       "iterations_natural_order_reference": natural_iters,
                        "iterations_max": int(np.max(iters)),
                        "all_converged": ok, "input_generation_s": round(gen_s, 2)},
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak,
