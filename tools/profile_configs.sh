@@ -19,7 +19,7 @@ if [ -z "$NO_B1" ]; then
 fi
 
 # launch list of the default bench command (eager loop: every kernel visible)
-P2G_EAGER_LOOP=1 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+[ -z "$NO_LAUNCHES" ] && P2G_EAGER_LOOP=1 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/prof/launches_c2.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu \
   > gpurun_out/prof/ncu_launch.log 2>&1; echo launches=$?
-gzip -f gpurun_out/prof/launches_c2.csv
+[ -z "$NO_LAUNCHES" ] && gzip -f gpurun_out/prof/launches_c2.csv
