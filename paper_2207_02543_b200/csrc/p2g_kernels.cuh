@@ -1853,6 +1853,188 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// L2 evict-first policy for streamed-once bulk copies (the matrix values)
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes,
+                                              uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+// ================= bulk-copy staged backward GS colour phases (Q4, one instance tile)
+// The register-fed node kernels above keep ~2 KB of matrix values in flight
+// per warp (one neighbour node), so a node is a chain of ~9 load rounds and a
+// short colour phase (c2: ~8k nodes, < 2 nodes per warp) is mostly ramp and
+// tail.  Here a warp owns one shared-memory slot and fetches a node's WHOLE
+// value block -- BS consecutive rows of one instance tile are contiguous when
+// Bp == Sh::T -- with one cp.async.bulk (up to 18 KB, L2 evict-first)
+// completing on the warp's mbarrier, while its lanes gather the neighbours' x
+// into registers.  A node costs one round trip, and an SM keeps NW x 18 KB
+// (144 KB at NW = 8) of values in flight instead of 64 KB.  The row sums run
+// from shared memory in exactly the order of k_gs_backward_blk (ascending
+// columns, separately rounded multiply / subtract): bit-identical results.
+// Reduction partials: one row per CTA (no cluster).
+// c2 (per colour phase launch, back to back in a graph): backward sweep 171 ->
+// 139 us per iteration; the fixed-length graph loop 439.5 -> 408.8 us per
+// iteration (tools/probe_loop.py).  NW = 7..10 are equivalent; at 216 KB of
+// slots (NW = 12) the 12 KB of L1 left throttles the gathers (158 us).
+// Measured and rejected: two slots per warp with the next node's
+// block in flight (the gathers then sit on the critical path: 157-162 us), a
+// per-row refill ring (142), a staged forward sweep (87-91 vs 83 us), and the
+// whole sweep as one persistent launch with a grid barrier between phases
+// (125 us by the per-class events but 410.5 vs 408.8 us in the graph loop).
+constexpr int kStgNmax = 9;  // Q4: at most 9 neighbour nodes (own included)
+#ifndef P2G_STG_NW_DEFAULT
+#define P2G_STG_NW_DEFAULT 8  // warps per CTA of the staged backward phases (0: register-fed kernels)
+#endif
+
+template <class Sh, int NW>
+struct StgGeo {
+    static constexpr int BS = 2;
+    static constexpr int SLOT = BS * BS * kStgNmax * Sh::T;  // doubles per warp slot
+    static constexpr size_t smem = (size_t)NW * SLOT * sizeof(double);
+    static constexpr int minb = NW >= 12 ? 1 : 12 / NW;
+};
+
+template <class Sh, int NW>
+__device__ __forceinline__ void stg_cta_partial(double (&acc)[Sh::V], double* part, int Bp,
+                                                bool accumulate) {
+    __shared__ double sm[NW][Sh::T];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int v = 0; v < Sh::V; ++v) sm[warp][lane * Sh::V + v] = acc[v];
+    __syncthreads();
+    if (threadIdx.x < Sh::T) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) t += sm[w][threadIdx.x];
+        double* dst = part + (size_t)blockIdx.x * Bp + threadIdx.x;
+        *dst = accumulate ? *dst + t : t;
+    }
+}
+
+template <class Sh, int NW, bool LAST>
+__global__ void __launch_bounds__(NW * 32, StgGeo<Sh, NW>::minb)
+    k_gs_backward_stg(Mat A, NodeTab T, const double* __restrict__ f, const double* xlo, double* s,
+                      const int* active, int nb, int ne, double* part_rs, int accumulate) {
+    constexpr int V = Sh::V, BS = 2, TT = Sh::T, SLOT = StgGeo<Sh, NW>::SLOT;
+    extern __shared__ __align__(128) double stg_smem[];
+    __shared__ uint64_t bars[NW];
+    __shared__ int sh_nc[NW][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int b0 = lane * V;
+    bool m[V], any;
+    lane_mask<Sh>(active, b0, m, any);
+    double rs[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) rs[v] = 0.0;
+    double* slot = stg_smem + warp * SLOT;
+    uint64_t* bar = &bars[warp];
+    if (lane == 0) {
+        mbar_init(bar, 1);
+        mbar_fence_init();
+    }
+    __syncwarp();
+    const uint64_t pol = l2_evict_first_policy();
+    uint32_t parity = 0;
+    // warp-major node order: consecutive nodes on consecutive CTAs, so a
+    // partly filled last round leaves every SM equally busy
+    const int stride = gridDim.x * NW;
+    int node = nb + warp * (int)gridDim.x + (int)blockIdx.x;
+    int4 inf_n = make_int4(0, 0, 0, 0);
+    int nc_n = 0;
+    const bool wany = __any_sync(0xffffffffu, any);  // some instance of the tile is still active
+    if (wany && node < ne) node_fetch(T, node, lane, inf_n, nc_n);
+    for (; wany && node < ne; node += stride) {
+        __syncwarp();  // every lane is done with the slot and the list of the previous node
+        sh_nc[warp][lane] = nc_n;
+        const int4 inf = inf_n;
+        __syncwarp();
+        const unsigned rl = (unsigned)inf.y;
+        const int pos = inf.z, nnb = inf.w;
+        if (lane == 0) {
+            // the node's BS rows are one contiguous block of BS * rowlen entries
+            const uint32_t bytes = (uint32_t)(BS * rl * TT * sizeof(double));
+            mbar_arrive_tx(bar, bytes);
+            bulk_g2s_hint(slot, A.vals + (size_t)inf.x * TT, bytes, bar, pol);
+        }
+        if (node + stride < ne) node_fetch(T, node + stride, lane, inf_n, nc_n);
+        const int* nc = sh_nc[warp];
+        const size_t ro = (size_t)node * BS * TT + b0;
+        // gathers: lower nodes and the node's own old components from xlo,
+        // upper nodes (already swept colours) from s
+        double x[kStgNmax][BS][V], fi[BS][V];
+#pragma unroll
+        for (int j = 0; j < kStgNmax; ++j) {
+            if (j < nnb) {
+                const double* src = (j <= pos ? xlo : s) + (size_t)((unsigned)nc[j] * BS * TT) + b0;
+#pragma unroll
+                for (int cc = 0; cc < BS; ++cc) ldv<V>(x[j][cc], src + cc * TT);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < BS; ++c) ldv<V>(fi[c], f + ro + c * TT);
+        mbar_wait(bar, parity);
+        parity ^= 1u;
+        double sn[BS][V];
+#pragma unroll
+        for (int c = BS - 1; c >= 0; --c) {
+            double acc[V], d[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                acc[v] = fi[c][v];
+                d[v] = 1.0;
+            }
+            const double* vr = slot + (unsigned)c * rl * TT + b0;
+#pragma unroll
+            for (int j = 0; j < kStgNmax; ++j) {
+                if (j < nnb) {
+#pragma unroll
+                    for (int cc = 0; cc < BS; ++cc) {
+                        double a[V];
+                        ldv<V>(a, vr + (j * BS + cc) * TT);
+                        const bool own = j == pos;
+#pragma unroll
+                        for (int v = 0; v < V; ++v) {
+                            // x[pos][.]: old components below c, new ones above (patched
+                            // in below); the diagonal entry is kept aside
+                            const double nv = __dsub_rn(acc[v], __dmul_rn(a[v], x[j][cc][v]));
+                            if (cc == c) {
+                                acc[v] = own ? acc[v] : nv;
+                                d[v] = own ? a[v] : d[v];
+                            } else {
+                                acc[v] = nv;
+                            }
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < V; ++v) sn[c][v] = __ddiv_rn(acc[v], d[v]);
+            stv<V>(s + ro + c * TT, sn[c], m);
+            if (c > 0) {
+                // the rows above read this node's new component c
+#pragma unroll
+                for (int j = 0; j < kStgNmax; ++j)
+#pragma unroll
+                    for (int v = 0; v < V; ++v) x[j][c][v] = j == pos ? sn[c][v] : x[j][c][v];
+            }
+            if constexpr (LAST) {
+#pragma unroll
+                for (int v = 0; v < V; ++v) rs[v] = __dadd_rn(rs[v], __dmul_rn(fi[c][v], sn[c][v]));
+            }
+        }
+    }
+    if constexpr (LAST) stg_cta_partial<Sh, NW>(rs, part_rs, A.Bp, accumulate != 0);
+}
+
 // Row stride (doubles) of the padded Phi copy the tensor-core tiles read:
 // k rounded up to 4 (whole k-steps, zero filled), then to 4 mod 8 so both the
 // A-fragment pattern of the restriction (row = lane%4, col = lane/4) and of

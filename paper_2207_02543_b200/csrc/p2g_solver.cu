@@ -521,6 +521,46 @@ struct Run {
         return P2G_OK;
     }
 
+    // Bulk-copy staged backward colour phases (k_gs_backward_stg): Q4
+    // node-blocked patterns with the whole batch in one instance tile.
+    // P2G_STG_NW = warps per CTA (4, 6, 7, 8, 9, 10, 12; 0 = register-fed kernels).
+    static int stg_nw(const p2g_handle* h) {
+        if constexpr (Sh::S != 1 || Sh::T < 32) return 0;
+        if (!h->node_blk || h->pat.bs != 2 || h->nmax > kStgNmax || h->Bp != Sh::T) return 0;
+        const char* e = std::getenv("P2G_STG_NW");
+        const int v = e ? std::atoi(e) : P2G_STG_NW_DEFAULT;
+        return (v == 4 || v == 6 || v == 7 || v == 8 || v == 9 || v == 10 || v == 12) ? v : 0;
+    }
+    template <int NW>
+    static dim3 stg_grid(p2g_handle* h, int64_t nodes, const void* fn) {
+        int ctas = 0;
+        for (auto& e : h->occ_cache)
+            if (e.first == fn) ctas = e.second;
+        if (!ctas) {
+            const size_t smem = StgGeo<Sh, NW>::smem;
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, NW * 32, smem);
+            ctas = std::max(occ, 1) * h->num_sms;
+            h->occ_cache.emplace_back(fn, ctas);
+        }
+        const int64_t need = (nodes + NW - 1) / NW;
+        int64_t gx = std::min<int64_t>(std::max<int64_t>(std::min<int64_t>(need, ctas), 1), h->nb_cap);
+        return dim3(static_cast<unsigned>(gx), 1);
+    }
+#define P2G_NW_CASE(nw, ...) \
+    case nw: { constexpr int NW = nw; __VA_ARGS__ } break;
+#define P2G_NW_SWITCH(code, ...)               \
+    switch (code) {                            \
+        P2G_NW_CASE(4, __VA_ARGS__)            \
+        P2G_NW_CASE(6, __VA_ARGS__)            \
+        P2G_NW_CASE(7, __VA_ARGS__)            \
+        P2G_NW_CASE(9, __VA_ARGS__)            \
+        P2G_NW_CASE(10, __VA_ARGS__)           \
+        P2G_NW_CASE(12, __VA_ARGS__)           \
+        default: { constexpr int NW = 8; __VA_ARGS__ } break; \
+    }
+
     static int gs_forward(p2g_handle* h, const double* f, double* s, int c, bool first) {
         Mat A = mat_of(h);
         const int nb = static_cast<int>(h->pat.color_rows[c] / h->pat.bs);
@@ -602,6 +642,27 @@ struct Run {
                                                     last ? h->d_part_rs : nullptr,
                                                     first_phase ? 0 : 1);
                     if (last) *rs_rows = g.x / kCluster;
+                })
+                count_launch(h, KC_BWD);
+                CU(cudaGetLastError());
+                return P2G_OK;
+            }
+        }
+        if constexpr (Sh::S == 1 && Sh::T >= 32) {
+            if (stg_nw(h) > 0) {
+                P2G_NW_SWITCH(stg_nw(h), {
+                    if (last) {
+                        auto fn = k_gs_backward_stg<Sh, NW, true>;
+                        dim3 g = stg_grid<NW>(h, maxc, (const void*)fn);
+                        fn<<<g, NW * 32, StgGeo<Sh, NW>::smem, h->stream>>>(
+                            A, ntab(h), f, xlo, s, h->d_active, nb, ne, h->d_part_rs, first_phase ? 0 : 1);
+                        *rs_rows = g.x;
+                    } else {
+                        auto fn = k_gs_backward_stg<Sh, NW, false>;
+                        dim3 g = stg_grid<NW>(h, maxc, (const void*)fn);
+                        fn<<<g, NW * 32, StgGeo<Sh, NW>::smem, h->stream>>>(
+                            A, ntab(h), f, xlo, s, h->d_active, nb, ne, nullptr, 0);
+                    }
                 })
                 count_launch(h, KC_BWD);
                 CU(cudaGetLastError());

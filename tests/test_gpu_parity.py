@@ -388,6 +388,31 @@ def test_node_blocked_kernels_bit_identical_to_row_kernels(gpu, monkeypatch, dim
     assert np.linalg.norm(x1 - x0) <= 1e-10 * np.linalg.norm(x0)
 
 
+@pytest.mark.parametrize("B,nw", [(64, 8), (40, 8), (20, 10), (64, 4), (64, 7), (40, 6), (32, 12), (64, 9)])
+def test_staged_colour_phases_bit_identical(gpu, monkeypatch, B, nw):
+    """Bulk-copy staged backward GS colour phases (k_gs_backward_stg: a node's
+    value block fetched with cp.async.bulk into the warp's shared-memory slot)
+    keep the ascending-column operation order of the register-fed node
+    kernels: preconditioner bit-identical, same iterations."""
+    m, rp, ci, f, V, phi = small_problem(B=B, k=10, nx=32, ny=16)
+    R = np.random.default_rng(13).standard_normal((B, m.n))
+    F = np.broadcast_to(f, (B, m.n)).copy()
+    out = []
+    for stg in (0, nw):
+        monkeypatch.setenv("P2G_STG_NW", str(stg))
+        s = make_solver(m, rp, ci, V, phi)
+        S = s.precond_apply(R)
+        x, it, conv, status, hist = s.solve(F, None, 1e-8, 2000, x0_mode=L.X0_REDUCED)
+        out.append((S, x, it, status, hist))
+        s.close()
+    (S0, x0, it0, st0, h0), (S1, x1, it1, st1, h1) = out
+    assert np.array_equal(S1, S0)
+    assert np.all(st1 == 0) and np.all(st0 == 0)
+    assert np.all(np.abs(it1 - it0) <= 1)
+    # only the r.s partial rows differ (one row per CTA instead of per cluster)
+    assert np.linalg.norm(x1 - x0) <= 1e-10 * np.linalg.norm(x0)
+
+
 @pytest.mark.parametrize("dims", [2, 3])
 def test_single_instance_node_blocked_kernels(gpu, monkeypatch, dims):
     """B = 1 node-blocked kernels (one warp per node, lane = neighbour node)
