@@ -2851,6 +2851,437 @@ __global__ void k_set_cond(const int* active, int Bp, cudaGraphConditionalHandle
     if (threadIdx.x == 0) cudaGraphSetConditional(cond, any ? 1u : 0u);
 }
 
+// ================ single-cluster persistent PCG loop (small single systems)
+// c1-sized problems (a few thousand dofs, one instance) are latency bound:
+// the captured loop runs 15 launches per iteration at ~3.3 us each, and every
+// kernel is a chain of 2-3 dependent L2 round trips (~0.5 us each).  Here the
+// WHOLE loop (krylov.hpp:267-289 with the Kp recurrence D9 and the POD-2G
+// preconditioner, pod.hpp:264-267) runs inside ONE kernel on one thread-block
+// cluster of kClSize CTAs:
+//   * the phases of an iteration are separated by the hardware cluster
+//     barrier (~0.2 us) instead of kernel boundaries, the dot products are
+//     combined over distributed shared memory (fixed rank order), and the
+//     convergence test never leaves the kernel;
+//   * the matrix is SHARED-MEMORY RESIDENT: node q belongs to CTA q % kClSize,
+//     which keeps the node's BS x rowlen values and column indices in
+//     [entry][slot] layout (conflict free) for the whole solve, so a node's
+//     only L2 round trip per phase is ONE round of x gathers, all issued
+//     together (the vectors stay in L2: ~0.2 MB);
+//   * one THREAD owns a node and walks its rows and their entries in
+//     ascending column order with separately rounded multiply / subtract --
+//     the reference's own operation order (smoothers.hpp:31-44, 56-70) on the
+//     colour-permuted system, without the xor-tree reassociation of the
+//     warp-per-node B = 1 kernels.  Reductions are fixed-order (D4).
+// Q4-shaped patterns (2 dofs per node, <= 9 neighbour nodes) whose matrix
+// fits the cluster's shared memory (<= ~3700 nodes).
+constexpr int kClSize = 8;       // CTAs per cluster (portable maximum)
+constexpr int kClThreads = 320;  // threads per CTA (204 registers each: a node's 36 gathers stay in flight)
+constexpr int kClKmax = 40;      // POD rank limit (coarse vectors and factor in shared memory)
+constexpr int kClBS = 2, kClRL = 18;  // dofs per node, entries per row at most
+
+struct ClusterLoop {
+    int n, k, ncolors, nrows_pkp, nl;  // nl = node slots per CTA = ceil(nodes / kClSize)
+    int color_rows[17];
+    const int *rp, *ci, *dpos;
+    const double *vals, *phi, *Lfac;  // phi [n][k], Lfac [k][k] (LDL^T, row-major)
+    double *u, *r, *p, *Kp, *s, *s2;  // s: forward sweep / prolongated s', s2: backward sweep
+    const double* part_pkp;           // pKp partial rows of the prologue's SpMV
+    double *rs_old, *rel, *hist, *beta, *alpha;
+    const double* fnorm;
+    int *iters, *active, *status;
+    const SolveParams* prm;
+    long long* trace;  // P2G_CLUSTER_TRACE=1: clock64 at the phase boundaries of iteration 2
+};
+// matrix values + column indices + per-node {row length, own position} + the nodes' Phi rows
+inline size_t cluster_loop_smem(int nl, int k) {
+    return (size_t)nl * (kClBS * kClRL * (sizeof(double) + sizeof(int)) + 2 * sizeof(int) +
+                         kClBS * (size_t)k * sizeof(double)) + 16;
+}
+
+struct ClusterShared {
+    double warp[kClThreads / 32][2];      // per-warp partials of a block reduction
+    double slot[4][2];                    // this CTA's published partials, one slot per reduction point
+    double total[2];                      // cluster totals, broadcast inside the CTA
+    double prod[8][kClThreads];           // restriction: per-thread products of 8 coefficients
+    double cpart[kClKmax];                // this CTA's restriction partial (read over DSMEM)
+    double cvec[kClKmax];                 // coarse right-hand side, then the coarse solution e
+};
+
+// block-reduce a value (fixed xor tree per warp, warps in order) into this
+// CTA's slot; the caller's cluster barrier publishes it
+__device__ __forceinline__ void cl_block_reduce(ClusterShared& S, int slot, double a) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    a = warp_sum(a);
+    if (lane == 0) S.warp[warp][0] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double ta = 0.0;
+        for (int w = 0; w < kClThreads / 32; ++w) ta += S.warp[w][0];
+        S.slot[slot][0] = ta;
+    }
+}
+
+// after the cluster barrier: sum the CTAs' slots in rank order (same value on every CTA)
+__device__ __forceinline__ double cl_gather(cg::cluster_group& cl, ClusterShared& S, int slot) {
+    if (threadIdx.x == 0) {
+        double ta = 0.0;
+        for (int rk = 0; rk < kClSize; ++rk) ta += cl.map_shared_rank(&S.slot[slot][0], rk)[0];
+        S.total[0] = ta;
+    }
+    __syncthreads();
+    const double a = S.total[0];
+    __syncthreads();
+    return a;
+}
+
+// Vector loads: plain (weak) loads.  Every vector element read here was
+// written before the last cluster barrier (release / acquire at cluster
+// scope, which also invalidates L1) or by the reading thread itself.
+// (ld.global.cg compiles to LDG.STRONG.GPU here, which the hardware does not
+// overlap: a node's 36 gathers then cost 36 serial L2 round trips.)
+__device__ __forceinline__ double cl_ld(const double* p) { return *p; }
+
+// one node's view of the shared-memory resident matrix
+struct ClNode {
+    const double* mv;  // values of entry (c, e) at mv[(c * kClRL + e) * nl]
+    const int* mc;     // column indices, same layout
+    int nl, rl, dp0;   // slot stride, entries per row, in-row position of the node's own block
+};
+
+// x[e] = X[col(c, e)] for the entries e in [e0, e1) of row c (one round of L2 loads)
+__device__ __forceinline__ void cl_gather_row(const ClNode& N, int c, int e0, int e1, const double* X,
+                                              double (&x)[kClRL]) {
+#pragma unroll
+    for (int e = 0; e < kClRL; ++e) {
+        const bool in = e >= e0 && e < e1;
+        const int col = in ? N.mc[(c * kClRL + e) * N.nl] : 0;
+        const double v = cl_ld(X + col);  // out-of-range entries read X[0], never used
+        x[e] = in ? v : x[e];
+    }
+}
+// sum (-= | +=) a(c, e) * x[e] over e in [e0, e1), ascending, separately rounded
+template <bool SUB>
+__device__ __forceinline__ double cl_row_sum(const ClNode& N, int c, int e0, int e1,
+                                             const double (&x)[kClRL], double sum) {
+#pragma unroll
+    for (int e = 0; e < kClRL; ++e) {
+        if (e >= e0 && e < e1) {
+            const double pr = __dmul_rn(N.mv[(c * kClRL + e) * N.nl], x[e]);
+            sum = SUB ? __dsub_rn(sum, pr) : __dadd_rn(sum, pr);
+        }
+    }
+    return sum;
+}
+
+__global__ void __cluster_dims__(kClSize, 1, 1) __launch_bounds__(kClThreads, 1)
+    k_pcg_cluster(ClusterLoop A) {
+    constexpr int BS = kClBS, RL = kClRL;
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ ClusterShared S;
+    __shared__ double Ls[kClKmax * kClKmax];
+    extern __shared__ __align__(16) unsigned char cl_dyn[];
+    const int nl = A.nl;
+    double* mv = reinterpret_cast<double*>(cl_dyn);
+    int* mc = reinterpret_cast<int*>(mv + (size_t)BS * RL * nl);
+    int* meta = mc + (size_t)BS * RL * nl;  // [nl][2] = {row length, own block position}
+    // the nodes' Phi rows, [c][a][slot] (8-byte aligned: 2 * nl ints precede it and BS * RL * nl is even)
+    double* mphi = reinterpret_cast<double*>(meta + 2 * nl);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int crank = (int)cl.block_rank();
+    const int n = A.n, k = A.k, C = A.ncolors;
+    const int nn = n / BS;
+    const int mine = (nn - crank + kClSize - 1) / kClSize;  // this CTA's nodes: slot * kClSize + crank
+    if (!A.active[0]) return;  // uniform over the cluster
+    // ---- the CTA's share of the matrix into shared memory, once
+    for (int sl = threadIdx.x; sl < mine; sl += kClThreads) {
+        const int i0 = (sl * kClSize + crank) * BS;
+        const int kb = __ldg(A.rp + i0), rl = __ldg(A.rp + i0 + 1) - kb;
+        meta[2 * sl] = rl;
+        meta[2 * sl + 1] = __ldg(A.dpos + i0) - kb;
+        for (int c = 0; c < BS; ++c)
+            for (int e = 0; e < rl; ++e) {
+                mv[(c * RL + e) * nl + sl] = __ldg(A.vals + kb + c * rl + e);
+                mc[(c * RL + e) * nl + sl] = __ldg(A.ci + kb + c * rl + e);
+            }
+    }
+    for (int sl = threadIdx.x; sl < mine; sl += kClThreads) {
+        const int i0 = (sl * kClSize + crank) * BS;
+        for (int c = 0; c < BS; ++c)
+            for (int a = 0; a < k; ++a) mphi[(c * k + a) * nl + sl] = __ldg(A.phi + (size_t)(i0 + c) * k + a);
+    }
+    for (int e2 = threadIdx.x; e2 < k * k; e2 += kClThreads) Ls[e2] = A.Lfac[e2];
+#define P2G_CL_TRACE(j) \
+    if (A.trace && crank == 0 && threadIdx.x == 0 && it == A.iters[0] + 1) A.trace[j] = clock64();
+    // pKp of the prologue's SpMV: fixed-order sum of its partial rows
+    double pKp = 0.0;
+    for (int q = 0; q < A.nrows_pkp; ++q) pKp += A.part_pkp[q];
+    double rs_old = A.rs_old[0];
+    const double fn = A.fnorm[0];
+    const double tol = A.prm->tol;
+    const long long max_iter = A.prm->max_iter, hist_cap = A.prm->hist_cap;
+    long long it = A.iters[0];
+    int status = ST_OK;
+    double rl_ = A.rel[0], beta = 0.0, alpha = 0.0;
+    __syncthreads();
+    // local slot range of the nodes [nb, ne) (node = slot * kClSize + crank)
+    auto first_slot = [&](int nb) { return nb > crank ? (nb - crank + kClSize - 1) / kClSize : 0; };
+    auto node_of = [&](int sl, ClNode& N) {
+        N.mv = mv + sl;
+        N.mc = mc + sl;
+        N.nl = nl;
+        N.rl = meta[2 * sl];
+        N.dp0 = meta[2 * sl + 1];
+        return (sl * kClSize + crank) * BS;
+    };
+    for (;;) {
+        // ---- alpha (krylov.hpp:273-276)
+        if (pKp <= 0.0) {
+            status = ST_EBREAKDOWN;
+            break;
+        }
+        alpha = rs_old / pKp;
+        P2G_CL_TRACE(44)
+        // ---- u += alpha p ; r -= alpha Kp ; r.r ; colour-0 forward rows (own lower components only)
+        double rr = 0.0;
+        const int c0s = first_slot(A.color_rows[1] / BS);
+        for (int sl = threadIdx.x; sl < mine; sl += kClThreads) {
+            ClNode N;
+            const int i0 = node_of(sl, N);
+            double sn[BS];
+#pragma unroll
+            for (int c = 0; c < BS; ++c) {
+                const int i = i0 + c;
+                const double ui = __dadd_rn(cl_ld(A.u + i), __dmul_rn(alpha, cl_ld(A.p + i)));
+                const double ri = __dadd_rn(cl_ld(A.r + i), __dmul_rn(-alpha, cl_ld(A.Kp + i)));
+                rr = __dadd_rn(rr, __dmul_rn(ri, ri));
+                A.u[i] = ui;
+                A.r[i] = ri;
+                if (sl < c0s) {
+                    double sum = ri;
+#pragma unroll
+                    for (int cc = 0; cc < c; ++cc)
+                        sum = __dsub_rn(sum, __dmul_rn(N.mv[(c * RL + N.dp0 + cc) * nl], sn[cc]));
+                    sn[c] = __ddiv_rn(sum, N.mv[(c * RL + N.dp0 + c) * nl]);
+                    A.s[i] = sn[c];
+                }
+            }
+        }
+        P2G_CL_TRACE(0)
+        cl_block_reduce(S, 0, rr);
+        cl.sync();
+        P2G_CL_TRACE(1)
+        // ---- forward colours 1 .. C-1 (first sweep from zero: L part only)
+        for (int col = 1; col < C; ++col) {
+            const int sb = first_slot(A.color_rows[col] / BS), se = first_slot(A.color_rows[col + 1] / BS);
+            for (int sl = sb + threadIdx.x; sl < se; sl += kClThreads) {
+                ClNode N;
+                const int i0 = node_of(sl, N);
+                double x[BS][RL] = {}, ri[BS], sn[BS];
+#pragma unroll
+                for (int c = 0; c < BS; ++c) {
+                    cl_gather_row(N, c, 0, N.dp0, A.s, x[c]);
+                    ri[c] = cl_ld(A.r + i0 + c);
+                }
+#pragma unroll
+                for (int c = 0; c < BS; ++c) {
+                    double sum = cl_row_sum<true>(N, c, 0, N.dp0, x[c], ri[c]);
+#pragma unroll
+                    for (int cc = 0; cc < c; ++cc)
+                        sum = __dsub_rn(sum, __dmul_rn(N.mv[(c * RL + N.dp0 + cc) * nl], sn[cc]));
+                    sn[c] = __ddiv_rn(sum, N.mv[(c * RL + N.dp0 + c) * nl]);
+                    A.s[i0 + c] = sn[c];
+                }
+            }
+            cl.sync();
+        }
+        P2G_CL_TRACE(2)
+        if (k > 0) {
+            // ---- t = -U s (D6) and c = Phi^T t: every thread's products of 8
+            // coefficients at a time into shared memory, one warp sums each
+            // coefficient over the threads (lane-strided, then a fixed xor tree)
+            for (int a = threadIdx.x; a < k; a += kClThreads) S.cpart[a] = 0.0;
+            for (int base = 0; base < mine; base += kClThreads) {
+                const int sl = base + threadIdx.x;
+                const bool ok = sl < mine;
+                double t[BS];
+#pragma unroll
+                for (int c = 0; c < BS; ++c) t[c] = 0.0;
+                if (ok) {
+                    ClNode N;
+                    node_of(sl, N);
+                    double x[BS][RL] = {};
+#pragma unroll
+                    for (int c = 0; c < BS; ++c) cl_gather_row(N, c, N.dp0 + c + 1, N.rl, A.s, x[c]);
+#pragma unroll
+                    for (int c = 0; c < BS; ++c)
+                        t[c] = -cl_row_sum<false>(N, c, N.dp0 + c + 1, N.rl, x[c], 0.0);
+                }
+                for (int a0 = 0; a0 < k; a0 += 8) {
+                    __syncthreads();  // S.prod is free again
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        double v = 0.0;
+                        if (ok && a0 + q < k) {
+#pragma unroll
+                            for (int c = 0; c < BS; ++c)
+                                v = __dadd_rn(v, __dmul_rn(mphi[(c * k + a0 + q) * nl + sl], t[c]));
+                        }
+                        S.prod[q][threadIdx.x] = v;
+                    }
+                    __syncthreads();
+                    if (warp < 8 && a0 + warp < k) {
+                        double v = 0.0;
+                        for (int q = lane; q < kClThreads; q += 32) v += S.prod[warp][q];
+                        v = warp_sum(v);
+                        if (lane == 0) S.cpart[a0 + warp] += v;
+                    }
+                }
+            }
+            P2G_CL_TRACE(3)
+            cl.sync();
+            P2G_CL_TRACE(4)
+            if (threadIdx.x < k) {
+                double tt = 0.0;
+                for (int rk = 0; rk < kClSize; ++rk)
+                    tt += cl.map_shared_rank(&S.cpart[0], rk)[threadIdx.x];
+                S.cvec[threadIdx.x] = tt;
+            }
+            __syncthreads();
+            // e = A_c^{-1} c with the LDL^T factor (k_coarse's substitution order)
+            if (warp == 0) {
+                double y0 = lane < k ? S.cvec[lane] : 0.0, y1 = lane + 32 < k ? S.cvec[lane + 32] : 0.0;
+                for (int j = 0; j < k; ++j) {
+                    const double yj = __shfl_sync(0xffffffffu, j < 32 ? y0 : y1, j & 31);
+                    if (lane > j && lane < k) y0 -= Ls[lane * k + j] * yj;
+                    if (lane + 32 > j && lane + 32 < k) y1 -= Ls[(lane + 32) * k + j] * yj;
+                }
+                if (lane < k) y0 /= Ls[lane * k + lane];
+                if (lane + 32 < k) y1 /= Ls[(lane + 32) * k + lane + 32];
+                for (int j = k - 1; j >= 0; --j) {
+                    const double xj = __shfl_sync(0xffffffffu, j < 32 ? y0 : y1, j & 31);
+                    if (lane < j) y0 -= Ls[j * k + lane] * xj;
+                    if (lane + 32 < j) y1 -= Ls[j * k + lane + 32] * xj;
+                }
+                __syncwarp();
+                if (lane < k) S.cvec[lane] = y0;
+                if (lane + 32 < k) S.cvec[lane + 32] = y1;
+            }
+            __syncthreads();
+            P2G_CL_TRACE(5)
+            // ---- s' = s + Phi e (ascending coefficients, fused multiply-adds: k_prolong)
+            for (int sl = threadIdx.x; sl < mine; sl += kClThreads) {
+                const int i0 = (sl * kClSize + crank) * BS;
+                double si[BS];
+#pragma unroll
+                for (int c = 0; c < BS; ++c) si[c] = cl_ld(A.s + i0 + c);
+#pragma unroll
+                for (int c = 0; c < BS; ++c) {
+                    double corr = 0.0;
+                    for (int a = 0; a < k; ++a) corr = fma(mphi[(c * k + a) * nl + sl], S.cvec[a], corr);
+                    A.s[i0 + c] = __dadd_rn(si[c], corr);
+                }
+            }
+            P2G_CL_TRACE(6)
+            cl.sync();  // also protects S.cpart / S.cvec against the next iteration
+            P2G_CL_TRACE(7)
+        }
+        // ---- backward sweep, out of place (D9): L part from s', U part from the new s2
+        double rs = 0.0;
+        for (int col = C - 1; col >= 0; --col) {
+            const int sb = first_slot(A.color_rows[col] / BS), se = first_slot(A.color_rows[col + 1] / BS);
+            for (int sl = sb + threadIdx.x; sl < se; sl += kClThreads) {
+                ClNode N;
+                const int i0 = node_of(sl, N);
+                double x[BS][RL] = {}, ri[BS];
+#pragma unroll
+                for (int c = 0; c < BS; ++c) {
+                    // lower nodes and own components below c: s' ; upper nodes: s2 ; own
+                    // components above c are this thread's new values (patched in below)
+                    cl_gather_row(N, c, 0, N.dp0 + c, A.s, x[c]);
+                    cl_gather_row(N, c, N.dp0 + BS, N.rl, A.s2, x[c]);
+                    ri[c] = cl_ld(A.r + i0 + c);
+                }
+#pragma unroll
+                for (int c = BS - 1; c >= 0; --c) {
+                    double sum = cl_row_sum<true>(N, c, 0, N.dp0 + c, x[c], ri[c]);
+                    sum = cl_row_sum<true>(N, c, N.dp0 + c + 1, N.rl, x[c], sum);
+                    const double si = __ddiv_rn(sum, N.mv[(c * RL + N.dp0 + c) * nl]);
+                    A.s2[i0 + c] = si;
+                    rs = __dadd_rn(rs, __dmul_rn(ri[c], si));
+#pragma unroll
+                    for (int cr = 0; cr < BS; ++cr) {
+                        if (cr < c) {
+#pragma unroll
+                            for (int e = 0; e < RL; ++e) x[cr][e] = e == N.dp0 + c ? si : x[cr][e];
+                        }
+                    }
+                }
+            }
+            if (col == 0) cl_block_reduce(S, 1, rs);
+            P2G_CL_TRACE(8 + 2 * (C - 1 - col))
+            cl.sync();
+            P2G_CL_TRACE(9 + 2 * (C - 1 - col))
+        }
+        // ---- end of the iteration (krylov.hpp:280-288), identical on every thread
+        const double rr_t = cl_gather(cl, S, 0);
+        const double rs_new = cl_gather(cl, S, 1);
+        beta = rs_new / rs_old;
+        rs_old = rs_new;
+        ++it;
+        const double rn = sqrt(rr_t);
+        rl_ = fn > 0.0 ? rn / fn : rn;
+        if (crank == 0 && threadIdx.x == 0 && it < hist_cap) A.hist[it] = rl_;
+        bool done = false;
+        if (rs_new <= 0.0 && rl_ > tol) {
+            status = ST_EBREAKDOWN;
+            done = true;
+        } else if (!(rl_ > tol) || it >= max_iter) {
+            done = true;
+        }
+        P2G_CL_TRACE(40)
+        if (done) break;
+        // ---- Kp = r + L (s2 - s') + beta Kp ; p = s2 + beta p ; p.Kp (D9)
+        double dot = 0.0;
+        for (int sl = threadIdx.x; sl < mine; sl += kClThreads) {
+            ClNode N;
+            const int i0 = node_of(sl, N);
+#pragma unroll
+            for (int c = 0; c < BS; ++c) {
+                const int i = i0 + c;
+                double x1[RL] = {}, x0[RL] = {};
+                cl_gather_row(N, c, 0, N.dp0 + c, A.s2, x1);
+                cl_gather_row(N, c, 0, N.dp0 + c, A.s, x0);
+                const double ri = cl_ld(A.r + i), kp0 = cl_ld(A.Kp + i), s2i = cl_ld(A.s2 + i),
+                             p0 = cl_ld(A.p + i);
+#pragma unroll
+                for (int e = 0; e < RL; ++e) x1[e] = __dsub_rn(x1[e], x0[e]);
+                const double acc = cl_row_sum<false>(N, c, 0, N.dp0 + c, x1, 0.0);
+                const double kpi = __dadd_rn(__dadd_rn(ri, acc), __dmul_rn(beta, kp0));
+                const double pi = __dadd_rn(s2i, __dmul_rn(beta, p0));
+                dot = __dadd_rn(dot, __dmul_rn(pi, kpi));
+                A.Kp[i] = kpi;
+                A.p[i] = pi;
+            }
+        }
+        P2G_CL_TRACE(41)
+        cl_block_reduce(S, 2, dot);
+        cl.sync();
+        P2G_CL_TRACE(42)
+        pKp = cl_gather(cl, S, 2);
+        P2G_CL_TRACE(43)
+    }
+    if (crank == 0 && threadIdx.x == 0) {
+        A.rs_old[0] = rs_old;
+        A.iters[0] = (int)it;
+        A.rel[0] = rl_;
+        A.beta[0] = beta;
+        A.alpha[0] = alpha;
+        A.active[0] = 0;
+        if (status != ST_OK) A.status[0] = status;
+    }
+    cl.sync();  // no CTA exits while its shared memory may still be read
+}
+
 // ---------------------------------------------------------------- layout kernels
 // dst[new][Bp] (b < B) <- src[b][old] with old = map[new] ; padded columns = pad
 __global__ void k_gather_interleave(const double* __restrict__ src, int64_t src_stride, int B,

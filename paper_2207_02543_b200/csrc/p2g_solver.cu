@@ -1399,6 +1399,25 @@ bool eager_loop() {
     return e;
 }
 
+// Single-cluster persistent loop (k_pcg_cluster): one instance, default
+// configuration (multicolour GS, one pre / post sweep, upper residual, Kp
+// recurrence), Q4-shaped pattern whose matrix fits the cluster's shared memory.
+// P2G_CLUSTER_NNZ = largest nnz taken.  OFF by default (0): measured on c1 at
+// 55 us per iteration against 51 us for the captured loop -- a phase costs one
+// global round trip (~1 us under the cluster barrier's release) plus the
+// barrier (~0.9 us), no less than a kernel boundary inside a graph
+// (P2G_CLUSTER_TRACE=1 prints the phase clock, c1).
+bool cluster_loop_ok(const p2g_handle* h) {
+    const char* e = std::getenv("P2G_CLUSTER_NNZ");
+    const long long lim = e ? std::atoll(e) : 0;
+    const int nl = static_cast<int>((h->pat.n / 2 + kClSize - 1) / kClSize);
+    return h->B == 1 && h->Bp == 1 && lim > 0 && (long long)h->pat.nnz <= lim && kp_recurrence(h) &&
+           h->cfg.pre_sweeps == 1 && h->cfg.post_sweeps == 1 &&
+           h->cfg.residual_form == P2G_RESIDUAL_UPPER && h->k <= kClKmax && h->pat.ncolors <= 16 &&
+           h->pat.ncolors >= 1 && h->node_blk && h->pat.bs == kClBS && h->nmax * kClBS <= kClRL &&
+           cluster_loop_smem(nl, h->k) <= 200 * 1024;
+}
+
 // cycle == false: pcg_solve (krylov.hpp:243-297) with the POD-2G preconditioner;
 // cycle == true: pod2g_solve (pod.hpp:224-256), iters = cycles
 // start a requested prefetch copy (p2g_prefetch_values) on the copy stream
@@ -1481,6 +1500,7 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
     if (st != P2G_OK) return st;
     CU(cudaEventRecord(h->ev[1], h->stream));
     int64_t eager_iters = -1;
+    bool cluster_loop = false;
     if (eager_loop()) {
         // profiling aid (P2G_EAGER_LOOP=1): the same loop body launched eagerly so
         // ncu lists every kernel (it does not descend into the conditional-WHILE
@@ -1498,6 +1518,61 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
                 return cycle ? decltype(R)::cycle(h, false) : decltype(R)::iteration(h, false);
             }));
         }
+    } else if (!cycle && cluster_loop_ok(h)) {
+        // small single system: the whole loop in one kernel on one cluster
+        ClusterLoop A;
+        A.n = static_cast<int>(h->pat.n);
+        A.nl = static_cast<int>((h->pat.n / kClBS + kClSize - 1) / kClSize);
+        A.k = h->k;
+        A.ncolors = h->pat.ncolors;
+        A.nrows_pkp = dispatch(h, [&](auto R) -> int { return decltype(R)::kp_rows(h); });
+        for (int c = 0; c <= h->pat.ncolors; ++c) A.color_rows[c] = static_cast<int>(h->pat.color_rows[c]);
+        A.rp = h->d_rp;
+        A.ci = h->d_ci;
+        A.dpos = h->d_dpos;
+        A.vals = h->d_vals;
+        A.phi = h->d_phi;
+        A.Lfac = h->d_L;
+        A.u = h->d_u;
+        A.r = h->d_r;
+        A.p = h->d_p;
+        A.Kp = h->d_Kp;
+        A.s = h->d_s;
+        A.s2 = h->d_s2;
+        A.part_pkp = h->d_part_dot;
+        A.rs_old = h->d_rsold;
+        A.rel = h->d_rel;
+        A.hist = h->d_hist;
+        A.beta = h->d_beta;
+        A.alpha = h->d_alpha;
+        A.fnorm = h->d_fnorm;
+        A.iters = h->d_iters;
+        A.active = h->d_active;
+        A.status = h->d_status;
+        A.prm = h->d_prm;
+        const size_t smem = cluster_loop_smem(A.nl, A.k);
+        CU(cudaFuncSetAttribute(k_pcg_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        A.trace = nullptr;
+        const bool trace = std::getenv("P2G_CLUSTER_TRACE") != nullptr;
+        if (trace) {
+            CU(cudaMalloc(&A.trace, 64 * sizeof(long long)));
+            CU(cudaMemset(A.trace, 0, 64 * sizeof(long long)));
+        }
+        k_pcg_cluster<<<kClSize, kClThreads, smem, h->stream>>>(A);
+        if (trace) {
+            long long tr[64];
+            CU(cudaStreamSynchronize(h->stream));
+            CU(cudaMemcpy(tr, A.trace, sizeof(tr), cudaMemcpyDeviceToHost));
+            cudaFree(A.trace);
+            std::fprintf(stderr, "k_pcg_cluster trace (cycles since the iteration's alpha):");
+            for (int j = 0; j < 44; ++j)
+                if (tr[j]) std::fprintf(stderr, " [%d]%lld", j, tr[j] - tr[44]);
+            std::fprintf(stderr, "\n");
+        }
+        CU(cudaGetLastError());
+        h->s_prol = h->d_s;
+        h->s_final = h->d_s2;
+        cluster_loop = true;
     } else {
         CU(cudaGraphLaunch(cycle ? h->cyc_exec : h->loop_exec, h->stream));
     }
@@ -1538,7 +1613,9 @@ int solve_impl(p2g_handle* h, const double* b_host, const double* b_dev, const d
     h->last_ms[1] = ms_loop;
     int64_t maxit = 0;
     for (int b = 0; b < h->B; ++b) maxit = std::max<int64_t>(maxit, it[b]);
-    if (eager_iters < 0)
+    if (cluster_loop)
+        h->launches_executed += 1;
+    else if (eager_iters < 0)
         h->launches_executed +=
             1 /*set_cond*/ + maxit * (cycle ? h->launches_per_cycle : h->launches_per_iter);
     h->launches_last_solve = h->launches_executed - lc0;
