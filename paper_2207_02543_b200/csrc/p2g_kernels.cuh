@@ -2035,6 +2035,322 @@ __global__ void __launch_bounds__(NW * 32, StgGeo<Sh, NW>::minb)
     if constexpr (LAST) stg_cta_partial<Sh, NW>(rs, part_rs, A.Bp, accumulate != 0);
 }
 
+// ============ bulk-copy staged single-instance hex8 kernels (c5's kernels)
+// The two-nodes-per-warp kernels above are bound by L1 wavefronts, not DRAM:
+// a lane reads its neighbour slot's 3 x 3 value block with nine 8-byte loads
+// at a 24-byte lane stride (every 32-byte sector is requested ~3.5 times:
+// ~430 sector requests per node pair) next to ~190 for the x gathers.  The
+// staged forms fetch each node's whole value block (BS rows x rowlen, up to
+// 1944 contiguous bytes) with ONE cp.async.bulk into the half-warp's
+// shared-memory slot -- the copy engine, not the load pipe, moves the matrix --
+// and the lanes read their blocks from shared memory (stride of 3 doubles:
+// conflict free).  The x gathers and the node's own vector entries are issued
+// before the warp waits on its mbarrier.  Lane mapping, fma order and xor tree
+// are those of the register-fed kernels: results are bit-identical.
+// A node's block starts at an 8-byte aligned value index; the copy starts at
+// the 16-byte aligned address at or below it (the values array carries two
+// doubles of slack at its end).
+constexpr int kB1SlotDoubles = 256;  // per node: 3 * 81 values + alignment slack
+#ifndef P2G_B1S_DEFAULT
+#define P2G_B1S_DEFAULT 6  // backward sweep and Kp recurrence (128^3: 1265 -> 1153 us, 960 -> 917 us); forward 715 -> 878, residual unchanged
+#endif
+
+// terms of neighbour slot j from the staged block vs (row length rl)
+template <int BS>
+__device__ __forceinline__ void b1s_terms(const double* vs, int rl, int j, const double (&x)[BS],
+                                          double (&p)[BS]) {
+#pragma unroll
+    for (int c = 0; c < BS; ++c)
+#pragma unroll
+        for (int cc = 0; cc < BS; ++cc) p[c] = fma(vs[c * rl + j * BS + cc], x[cc], p[c]);
+}
+template <int BS>
+__device__ __forceinline__ void b1s_own(const double* vs, int rl, int pos, double (&ob)[BS][BS]) {
+#pragma unroll
+    for (int c = 0; c < BS; ++c)
+#pragma unroll
+        for (int cc = 0; cc < BS; ++cc) ob[c][cc] = vs[c * rl + pos * BS + cc];
+}
+
+// Node loop of the staged kernels: as P2G_B1H_NODE_LOOP, plus per iteration
+// the two bulk copies of the warp's node pair (issued by lane 0 of each half)
+// on the warp's mbarrier.  The body gathers first, then calls B1S_WAIT() and
+// reads the values through `vs`.
+#define P2G_B1S_NODE_LOOP(MODE, BS, A, T, nb, ne, ...)                                              \
+    {                                                                                          \
+        extern __shared__ __align__(128) double b1s_smem[];                                    \
+        __shared__ uint64_t b1s_bars[kWarps];                                                  \
+        const int lane = threadIdx.x & 31, hl = lane & 15, warp_ = threadIdx.x >> 5;           \
+        double* slot_ = b1s_smem + (warp_ * 2 + (lane >> 4)) * kB1SlotDoubles;                 \
+        uint64_t* bar_ = &b1s_bars[warp_];                                                     \
+        if (lane == 0) {                                                                       \
+            mbar_init(bar_, 1);                                                                \
+            mbar_fence_init();                                                                 \
+        }                                                                                      \
+        __syncwarp();                                                                          \
+        const uint64_t pol_ = l2_evict_first_policy();                                         \
+        uint32_t par_ = 0;                                                                     \
+        const int stride_ = gridDim.x * kWarps * 2;                                            \
+        int base_ = (nb) + (blockIdx.x * kWarps + warp_) * 2;                                  \
+        int4 inf_n_ = make_int4(0, 0, 0, 0);                                                   \
+        int nc0_n_ = 0, nc1_n_ = 0;                                                            \
+        auto fetch_ = [&](int b_) {                                                            \
+            const int nd_ = b_ + (lane >> 4);                                                  \
+            if (nd_ < (ne)) {                                                                  \
+                inf_n_ = __ldg(T.info + nd_);                                                  \
+                const int* nl_ = T.ncol + (size_t)nd_ * T.nmax;                                \
+                nc0_n_ = hl < T.nmax ? __ldg(nl_ + hl) : 0;                                    \
+                nc1_n_ = hl + 16 < T.nmax ? __ldg(nl_ + hl + 16) : 0;                          \
+            }                                                                                  \
+        };                                                                                     \
+        if (base_ < (ne)) fetch_(base_);                                                       \
+        for (; base_ < (ne); base_ += stride_) {                                               \
+            const int node = base_ + (lane >> 4);                                              \
+            const bool valid = node < (ne);                                                    \
+            const int4 inf = inf_n_;                                                           \
+            const int nc0 = nc0_n_, nc1 = nc1_n_;                                              \
+            __syncwarp(); /* the previous pair's slot reads are done */                        \
+            {                                                                                  \
+                /* lane hl < BS copies the part of row hl the kernel reads (MODE 0: lane 0  */ \
+                /* copies the whole block; 1: [0, own block]; 2: [own block, row end)),     */ \
+                /* widened to 16-byte aligned value indices; same offsets in the slot       */ \
+                int e0_ = 0, e1_ = 0;                                                          \
+                if (valid && hl < ((MODE) == 0 ? 1 : BS)) {                                    \
+                    e0_ = (MODE) == 0 ? 0 : hl * inf.y + ((MODE) == 2 ? inf.z * BS : 0);       \
+                    e1_ = (MODE) == 0 ? BS * inf.y                                             \
+                                      : hl * inf.y + ((MODE) == 1 ? (inf.z + 1) * BS : inf.y); \
+                }                                                                              \
+                const int a0_ = (inf.x + e0_) & ~1, a1_ = (inf.x + e1_ + 1) & ~1;              \
+                const uint32_t by_ = e1_ > e0_ ? (uint32_t)((a1_ - a0_) * sizeof(double)) : 0u; \
+                const uint32_t tot_ = __reduce_add_sync(0xffffffffu, by_);                     \
+                if (lane == 0) mbar_arrive_tx(bar_, tot_);                                     \
+                __syncwarp();                                                                  \
+                if (by_) bulk_g2s_hint(slot_ + (a0_ - (inf.x & ~1)), A.vals + a0_, by_, bar_, pol_); \
+            }                                                                                  \
+            const double* vs = slot_ + (inf.x & 1);                                            \
+            if (base_ + stride_ < (ne)) fetch_(base_ + stride_);                               \
+            __VA_ARGS__                                                                        \
+        }                                                                                      \
+    }
+#define B1S_WAIT()              \
+    mbar_wait(bar_, par_ & 1u); \
+    par_ ^= 1u;
+
+template <int BS>
+__global__ void __launch_bounds__(kBlock, P2G_B1BLK_MINB)
+    k_gs_forward_b1s(Mat A, NodeTab T, const double* __restrict__ f, double* s, const int* active,
+                     int nb, int ne) {
+    if (!active[0]) return;
+    P2G_B1S_NODE_LOOP(1, BS, A, T, nb, ne, {
+        const int nd = node;
+        double ob[BS][BS], fo[BS], q[BS], x[2][BS];
+#pragma unroll
+        for (int c = 0; c < BS; ++c) q[c] = 0.0;
+        const int rl = inf.y, pos = inf.z;
+        if (valid) {
+#pragma unroll
+            for (int c = 0; c < BS; ++c) fo[c] = __ldg(f + (size_t)nd * BS + c);
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                if (hl + 16 * h < pos) {
+#pragma unroll
+                    for (int cc = 0; cc < BS; ++cc) x[h][cc] = __ldg(s + (size_t)(h ? nc1 : nc0) * BS + cc);
+                }
+        }
+        B1S_WAIT()
+        if (valid) {
+            b1s_own<BS>(vs, rl, pos, ob);
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                if (hl + 16 * h < pos) b1s_terms<BS>(vs, rl, hl + 16 * h, x[h], q);
+        }
+#pragma unroll
+        for (int c = 0; c < BS; ++c) q[c] = half_sum(q[c]);
+        if (valid) {
+            double sn[BS];
+#pragma unroll
+            for (int c = 0; c < BS; ++c) {
+                double acc = fo[c] - q[c];
+#pragma unroll
+                for (int cc = 0; cc < c; ++cc) acc -= ob[c][cc] * sn[cc];
+                sn[c] = acc / ob[c][c];
+            }
+            if (hl < BS) s[(size_t)nd * BS + hl] = pick_row<BS>(sn, hl);
+        }
+    })
+}
+
+template <int BS, bool LAST>
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1H_WIDE_MINB)
+    k_gs_backward_b1s(Mat A, NodeTab T, const double* __restrict__ f, const double* xlo, double* s,
+                      const int* active, int nb, int ne, double* part_rs, int accumulate) {
+    double rs[1] = {0.0};
+    if (active[0]) {
+        P2G_B1S_NODE_LOOP(0, BS, A, T, nb, ne, {
+            const int rl = inf.y, pos = inf.z, nnb = inf.w;
+            double ob[BS][BS], fo[BS], xo[BS], q[BS], x[2][BS];
+#pragma unroll
+            for (int c = 0; c < BS; ++c) q[c] = 0.0;
+            if (valid) {
+#pragma unroll
+                for (int c = 0; c < BS; ++c) {
+                    fo[c] = __ldg(f + (size_t)node * BS + c);
+                    xo[c] = __ldg(xlo + (size_t)node * BS + c);
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int j = hl + 16 * h;
+                    if (j < nnb && j != pos) {
+                        const double* X = j < pos ? xlo : s;
+#pragma unroll
+                        for (int cc = 0; cc < BS; ++cc) x[h][cc] = __ldg(X + (size_t)(h ? nc1 : nc0) * BS + cc);
+                    }
+                }
+            }
+            B1S_WAIT()
+            if (valid) {
+                b1s_own<BS>(vs, rl, pos, ob);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int j = hl + 16 * h;
+                    if (j < nnb && j != pos) b1s_terms<BS>(vs, rl, j, x[h], q);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < BS; ++c) q[c] = half_sum(q[c]);
+            if (valid) {
+                double sn[BS];
+#pragma unroll
+                for (int c = BS - 1; c >= 0; --c) {
+                    double acc = fo[c] - q[c];
+#pragma unroll
+                    for (int cc = 0; cc < BS; ++cc) {
+                        if (cc == c) continue;
+                        acc -= ob[c][cc] * (cc < c ? xo[cc] : sn[cc]);
+                    }
+                    sn[c] = acc / ob[c][c];
+                }
+                if (hl < BS) s[(size_t)node * BS + hl] = pick_row<BS>(sn, hl);
+                if (LAST && hl == 0) {
+#pragma unroll
+                    for (int c = 0; c < BS; ++c) rs[0] += fo[c] * sn[c];
+                }
+            }
+        })
+    }
+    if constexpr (LAST) cluster_partial<ShB1a>(rs, part_rs, A.Bp, accumulate != 0);
+}
+
+template <int BS>
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1H_WIDE_MINB)
+    k_kp_update_b1s(Mat A, NodeTab T, const double* __restrict__ r, const double* __restrict__ s,
+                    const double* __restrict__ sp, double* __restrict__ Kp, double* __restrict__ p,
+                    const double* beta, const int* active, double* part) {
+    double dacc[1] = {0.0};
+    if (active[0]) {
+        const double bt = beta[0];
+        const int nn = A.n / BS;
+        P2G_B1S_NODE_LOOP(1, BS, A, T, 0, nn, {
+            const int rl = inf.y, pos = inf.z;
+            double ob[BS][BS], xd[BS], q[BS], x[2][BS];
+            const int c_own = hl < BS ? hl : 0;
+            const size_t o = (size_t)node * BS + c_own;
+            double ri = 0, si = 0, kpo = 0, po = 0;
+#pragma unroll
+            for (int c = 0; c < BS; ++c) q[c] = 0.0;
+            if (valid) {
+#pragma unroll
+                for (int c = 0; c < BS; ++c)
+                    xd[c] = __ldg(s + (size_t)node * BS + c) - __ldg(sp + (size_t)node * BS + c);
+                ri = __ldg(r + o), si = __ldg(s + o), kpo = __ldg(Kp + o), po = __ldg(p + o);
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    if (hl + 16 * h < pos) {
+                        const int col = h ? nc1 : nc0;
+#pragma unroll
+                        for (int cc = 0; cc < BS; ++cc)
+                            x[h][cc] = __ldg(s + (size_t)col * BS + cc) - __ldg(sp + (size_t)col * BS + cc);
+                    }
+            }
+            B1S_WAIT()
+            if (valid) {
+                b1s_own<BS>(vs, rl, pos, ob);
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    if (hl + 16 * h < pos) b1s_terms<BS>(vs, rl, hl + 16 * h, x[h], q);
+            }
+#pragma unroll
+            for (int c = 0; c < BS; ++c) q[c] = half_sum(q[c]);
+            if (valid) {
+                double lo[BS];
+#pragma unroll
+                for (int c = 0; c < BS; ++c) {
+                    double acc = q[c];
+#pragma unroll
+                    for (int cc = 0; cc < c; ++cc) acc += ob[c][cc] * xd[cc];
+                    lo[c] = acc;
+                }
+                if (hl < BS) {
+                    const double kpi = (ri + pick_row<BS>(lo, hl)) + bt * kpo;
+                    const double pi = si + bt * po;
+                    Kp[o] = kpi;
+                    p[o] = pi;
+                    dacc[0] += pi * kpi;
+                }
+            }
+        })
+    }
+    cluster_partial<ShB1a>(dacc, part, A.Bp, false);
+}
+
+template <int BS>
+__global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1BLK_MINB)
+    k_residual_upper_b1s(Mat A, NodeTab T, const double* __restrict__ u, double* __restrict__ t,
+                         const int* active) {
+    if (!active[0]) return;
+    const int nn = A.n / BS;
+    P2G_B1S_NODE_LOOP(2, BS, A, T, 0, nn, {
+        const int rl = inf.y, pos = inf.z, nnb = inf.w;
+        double ob[BS][BS], uo[BS], q[BS], x[2][BS];
+#pragma unroll
+        for (int c = 0; c < BS; ++c) q[c] = 0.0;
+        if (valid) {
+#pragma unroll
+            for (int c = 0; c < BS; ++c) uo[c] = __ldg(u + (size_t)node * BS + c);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = hl + 16 * h;
+                if (j > pos && j < nnb) {
+#pragma unroll
+                    for (int cc = 0; cc < BS; ++cc) x[h][cc] = __ldg(u + (size_t)(h ? nc1 : nc0) * BS + cc);
+                }
+            }
+        }
+        B1S_WAIT()
+        if (valid) {
+            b1s_own<BS>(vs, rl, pos, ob);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = hl + 16 * h;
+                if (j > pos && j < nnb) b1s_terms<BS>(vs, rl, j, x[h], q);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < BS; ++c) q[c] = half_sum(q[c]);
+        if (valid) {
+            double tv[BS];
+#pragma unroll
+            for (int c = 0; c < BS; ++c) {
+                double acc = 0.0;
+#pragma unroll
+                for (int cc = c + 1; cc < BS; ++cc) acc += ob[c][cc] * uo[cc];
+                tv[c] = -(acc + q[c]);
+            }
+            if (hl < BS) t[(size_t)node * BS + hl] = pick_row<BS>(tv, hl);
+        }
+    })
+}
+
 // Row stride (doubles) of the padded Phi copy the tensor-core tiles read:
 // k rounded up to 4 (whole k-steps, zero filled), then to 4 mod 8 so both the
 // A-fragment pattern of the restriction (row = lane%4, col = lane/4) and of

@@ -405,9 +405,18 @@ struct Run {
     static bool blk1_hw(const p2g_handle* h) {
         return blk1(h) && h->pat.bs == 3 && !std::getenv("P2G_NO_B1H");
     }
-    static dim3 blk1_grid(p2g_handle* h, int64_t nodes, const void* fn, bool cluster) {
+    // bulk-copy staged two-nodes-per-warp kernels (k_*_b1s): P2G_B1S = bit mask
+    // {1 forward, 2 backward, 4 Kp recurrence, 8 upper residual}
+    static constexpr size_t kB1sSmem = (size_t)kWarps * 2 * kB1SlotDoubles * sizeof(double);
+    static bool blk1_stg(const p2g_handle* h, int bit) {
+        if (!blk1_hw(h) || h->nmax * h->pat.bs * h->pat.bs + 2 > kB1SlotDoubles) return false;
+        const char* e = std::getenv("P2G_B1S");
+        const int mask = e ? std::atoi(e) : P2G_B1S_DEFAULT;
+        return (mask & bit) != 0;
+    }
+    static dim3 blk1_grid(p2g_handle* h, int64_t nodes, const void* fn, bool cluster, size_t smem = 0) {
         const int64_t need = (nodes + kWarps - 1) / kWarps;
-        int64_t gx = std::min<int64_t>(need, resident_ctas(h, fn, cluster));
+        int64_t gx = std::min<int64_t>(need, resident_ctas(h, fn, cluster, smem));
         gx = std::min<int64_t>(std::max<int64_t>(gx, 1), h->nb_cap);
         if (cluster) gx = (gx + kCluster - 1) / kCluster * kCluster;
         return dim3(static_cast<unsigned>(gx), 1);
@@ -432,8 +441,9 @@ struct Run {
         }
         if constexpr (Sh::W == 1) {
             if (blk1_hw(h)) {
-                kp = (const void*)k_kp_update_b1h<3>;
-                const dim3 b1 = blk1_grid(h, (nnodes(h) + 1) / 2, kp, true);
+                const bool stg = blk1_stg(h, 4);
+                kp = stg ? (const void*)k_kp_update_b1s<3> : (const void*)k_kp_update_b1h<3>;
+                const dim3 b1 = blk1_grid(h, (nnodes(h) + 1) / 2, kp, true, stg ? kB1sSmem : 0);
                 return a.x <= b1.x ? a : b1;
             }
             if (blk1_half(h)) {
@@ -568,9 +578,11 @@ struct Run {
         if (ne <= nb) return P2G_OK;
         if constexpr (Sh::W == 1) {
             if (first && blk1_hw(h)) {
-                auto fn = k_gs_forward_b1h<3>;
-                dim3 g = blk1_grid(h, (ne - nb + 1) / 2, (const void*)fn, false);
-                fn<<<g, kBlock, 0, h->stream>>>(A, ntab(h), f, s, h->d_active, nb, ne);
+                const bool stg = blk1_stg(h, 1);
+                auto fn = stg ? k_gs_forward_b1s<3> : k_gs_forward_b1h<3>;
+                const size_t smem = stg ? kB1sSmem : 0;
+                dim3 g = blk1_grid(h, (ne - nb + 1) / 2, (const void*)fn, false, smem);
+                fn<<<g, kBlock, smem, h->stream>>>(A, ntab(h), f, s, h->d_active, nb, ne);
                 count_launch(h, KC_FWD);
                 CU(cudaGetLastError());
                 return P2G_OK;
@@ -625,9 +637,12 @@ struct Run {
             maxc = std::max<int64_t>(maxc, (h->pat.color_rows[q + 1] - h->pat.color_rows[q]) / h->pat.bs);
         if constexpr (Sh::W == 1) {
             if (blk1_hw(h) && !std::getenv("P2G_NO_B1H_BWD")) {
-                auto fn = last ? k_gs_backward_b1h<3, true> : k_gs_backward_b1h<3, false>;
-                dim3 g = blk1_grid(h, (maxc + 1) / 2, (const void*)fn, true);
-                fn<<<g, kBlock, 0, h->stream>>>(A, ntab(h), f, xlo, s, h->d_active, nb, ne,
+                const bool stg = blk1_stg(h, 2);
+                auto fn = stg ? (last ? k_gs_backward_b1s<3, true> : k_gs_backward_b1s<3, false>)
+                              : (last ? k_gs_backward_b1h<3, true> : k_gs_backward_b1h<3, false>);
+                const size_t smem = stg ? kB1sSmem : 0;
+                dim3 g = blk1_grid(h, (maxc + 1) / 2, (const void*)fn, true, smem);
+                fn<<<g, kBlock, smem, h->stream>>>(A, ntab(h), f, xlo, s, h->d_active, nb, ne,
                                                 last ? h->d_part_rs : nullptr, first_phase ? 0 : 1);
                 if (last) *rs_rows = g.x / kCluster;
                 count_launch(h, KC_BWD);
@@ -713,9 +728,14 @@ struct Run {
         bool done = false;
         if constexpr (Sh::W == 1) {
             if (blk1_hw(h)) {
-                k_kp_update_b1h<3><<<g, kBlock, 0, h->stream>>>(A, ntab(h), h->d_r, s_new, s_prol,
-                                                                 h->d_Kp, h->d_p, h->d_beta,
-                                                                 h->d_active, h->d_part_dot);
+                if (blk1_stg(h, 4))
+                    k_kp_update_b1s<3><<<g, kBlock, kB1sSmem, h->stream>>>(
+                        A, ntab(h), h->d_r, s_new, s_prol, h->d_Kp, h->d_p, h->d_beta, h->d_active,
+                        h->d_part_dot);
+                else
+                    k_kp_update_b1h<3><<<g, kBlock, 0, h->stream>>>(A, ntab(h), h->d_r, s_new, s_prol,
+                                                                     h->d_Kp, h->d_p, h->d_beta,
+                                                                     h->d_active, h->d_part_dot);
                 done = true;
             } else if (blk1_half(h)) {
                 P2G_BS_SWITCH(h->pat.bs, {
@@ -776,9 +796,11 @@ struct Run {
             bool done = false;
             if constexpr (Sh::W == 1) {
                 if (form == RES_UPPER && blk1_hw(h)) {
-                    auto fn = k_residual_upper_b1h<3>;
-                    dim3 g = blk1_grid(h, (nnodes(h) + 1) / 2, (const void*)fn, true);
-                    fn<<<g, kBlock, 0, h->stream>>>(A, ntab(h), s, tb, h->d_active);
+                    const bool stg = blk1_stg(h, 8);
+                    auto fn = stg ? k_residual_upper_b1s<3> : k_residual_upper_b1h<3>;
+                    const size_t smem = stg ? kB1sSmem : 0;
+                    dim3 g = blk1_grid(h, (nnodes(h) + 1) / 2, (const void*)fn, true, smem);
+                    fn<<<g, kBlock, smem, h->stream>>>(A, ntab(h), s, tb, h->d_active);
                     done = true;
                 } else if (form == RES_UPPER && blk1_half(h)) {
                     P2G_BS_SWITCH(h->pat.bs, {
@@ -1180,7 +1202,8 @@ void destroy_graph(p2g_handle* h) {
 
 int alloc_batch(p2g_handle* h) {
     const size_t nv = (size_t)(h->pat.n + h->n_ghost) * h->Bp;
-    TRY(dalloc(h, h->d_vals, (size_t)h->pat.nnz * h->Bp));
+    // two doubles of slack: the staged B = 1 kernels copy whole 16-byte pairs
+    TRY(dalloc(h, h->d_vals, (size_t)h->pat.nnz * h->Bp + 2));
     CU(cudaMemsetAsync(h->d_vals, 0, (size_t)h->pat.nnz * h->Bp * sizeof(double), h->stream));
     for (double** p : {&h->d_u, &h->d_r, &h->d_s, &h->d_s2, &h->d_p, &h->d_Kp, &h->d_b, &h->d_t}) {
         TRY(dalloc(h, *p, nv));

@@ -467,6 +467,35 @@ def test_cluster_resident_loop(gpu, monkeypatch, dims, k):
     assert np.linalg.norm(x1[0][perm] - ref_m.u) <= X_RTOL * np.linalg.norm(ref_m.u)
 
 
+@pytest.mark.parametrize("nx,ny,nz", [(6, 6, 6), (9, 7, 5)])
+def test_staged_single_instance_hex8_kernels_bit_identical(gpu, monkeypatch, nx, ny, nz):
+    """Bulk-copy staged B = 1 hex8 kernels (k_*_b1s: each node's value block
+    by cp.async.bulk into the half-warp's shared-memory slot) keep the lane
+    mapping, fma order and xor tree of the register-fed two-nodes-per-warp
+    kernels: preconditioner and solve bit-identical, each kernel on its own
+    (P2G_B1S bit mask) and all together."""
+    m, rp, ci, f, V, phi = small_problem(dim=3, nx=nx, ny=ny, nz=nz, Lx=1, Ly=1, Lz=1, B=1, k=8)
+    R = np.random.default_rng(21).standard_normal((1, m.n))
+    F = f[None, :].copy()
+    monkeypatch.setenv("P2G_CLUSTER_NNZ", "0")
+    out = {}
+    for mask in (0, 1, 2, 4, 8, 15):
+        monkeypatch.setenv("P2G_B1S", str(mask))
+        s = make_solver(m, rp, ci, V, phi)
+        S = s.precond_apply(R)
+        x, it, conv, status, hist = s.solve(F, None, 1e-8, 2000, x0_mode=L.X0_REDUCED)
+        out[mask] = (S, x, it, status, hist)
+        s.close()
+    S0, x0, it0, st0, h0 = out[0]
+    assert st0[0] == 0 and it0[0] > 5
+    for mask in (1, 2, 4, 8, 15):
+        S1, x1, it1, st1, h1 = out[mask]
+        assert np.array_equal(S1, S0), mask
+        assert np.array_equal(it1, it0) and st1[0] == 0, mask
+        assert np.array_equal(x1, x0), mask
+        assert np.array_equal(h1, h0, equal_nan=True), mask
+
+
 @pytest.mark.parametrize("dims", [2, 3])
 def test_single_instance_node_blocked_kernels(gpu, monkeypatch, dims):
     """B = 1 node-blocked kernels (one warp per node, lane = neighbour node)
