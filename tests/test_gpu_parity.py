@@ -467,14 +467,15 @@ def test_cluster_resident_loop(gpu, monkeypatch, dims, k):
     assert np.linalg.norm(x1[0][perm] - ref_m.u) <= X_RTOL * np.linalg.norm(ref_m.u)
 
 
-@pytest.mark.parametrize("nx,ny,nz", [(6, 6, 6), (9, 7, 5)])
+@pytest.mark.parametrize("nx,ny,nz", [(6, 6, 6), (8, 6, 4)])
 def test_staged_single_instance_hex8_kernels_bit_identical(gpu, monkeypatch, nx, ny, nz):
     """Bulk-copy staged B = 1 hex8 kernels (k_*_b1s: each node's value block
     by cp.async.bulk into the half-warp's shared-memory slot) keep the lane
     mapping, fma order and xor tree of the register-fed two-nodes-per-warp
     kernels: preconditioner and solve bit-identical, each kernel on its own
     (P2G_B1S bit mask) and all together."""
-    m, rp, ci, f, V, phi = small_problem(dim=3, nx=nx, ny=ny, nz=nz, Lx=1, Ly=1, Lz=1, B=1, k=8)
+    m, rp, ci, f, V, phi = small_problem(dim=3, nx=nx, ny=ny, nz=nz, Lx=nx / 4.0, Ly=ny / 4.0,
+                                         Lz=nz / 4.0, B=1, k=8)
     R = np.random.default_rng(21).standard_normal((1, m.n))
     F = f[None, :].copy()
     monkeypatch.setenv("P2G_CLUSTER_NNZ", "0")
