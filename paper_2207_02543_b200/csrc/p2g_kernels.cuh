@@ -1465,7 +1465,8 @@ __global__ void __launch_bounds__(kBlock, P2G_B1BLK_MINB)
 template <int BS, bool LAST>
 __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1H_WIDE_MINB)
     k_gs_backward_b1h(Mat A, NodeTab T, const double* __restrict__ f, const double* xlo, double* s,
-                      const int* active, int nb, int ne, double* part_rs, int accumulate) {
+                      const int* active, int nb, int ne, double* part_rs, int accumulate,
+                      double* dlt) {
     double rs[1] = {0.0};
     if (active[0]) {
         P2G_B1H_NODE_LOOP(T, nb, ne, {
@@ -1501,7 +1502,12 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1H_WIDE_MINB)
                     }
                     sn[c] = acc / ob[c][c];
                 }
-                if (hl < BS) s[(size_t)node * BS + hl] = pick_row<BS>(sn, hl);
+                if (hl < BS) {
+                    const double sv = pick_row<BS>(sn, hl);
+                    s[(size_t)node * BS + hl] = sv;
+                    // s - s' of the out-of-place last sweep, for the Kp recurrence's gathers
+                    if (dlt) dlt[(size_t)node * BS + hl] = sv - pick_row<BS>(xo, hl);
+                }
                 if (LAST && hl == 0) {
 #pragma unroll
                     for (int c = 0; c < BS; ++c) rs[0] += fo[c] * sn[c];
@@ -1516,7 +1522,8 @@ template <int BS>
 __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1H_WIDE_MINB)
     k_kp_update_b1h(Mat A, NodeTab T, const double* __restrict__ r, const double* __restrict__ s,
                     const double* __restrict__ sp, double* __restrict__ Kp, double* __restrict__ p,
-                    const double* beta, const int* active, double* part) {
+                    const double* beta, const int* active, double* part,
+                    const double* __restrict__ dlt) {
     double dacc[1] = {0.0};
     if (active[0]) {
         const double bt = beta[0];
@@ -1534,7 +1541,8 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1H_WIDE_MINB)
                 b1_own<BS>(vb, rl, pos, ob);
 #pragma unroll
                 for (int c = 0; c < BS; ++c)
-                    xd[c] = __ldg(s + (size_t)node * BS + c) - __ldg(sp + (size_t)node * BS + c);
+                    xd[c] = dlt ? __ldg(dlt + (size_t)node * BS + c)
+                                : __ldg(s + (size_t)node * BS + c) - __ldg(sp + (size_t)node * BS + c);
                 ri = __ldg(r + o), si = __ldg(s + o), kpo = __ldg(Kp + o), po = __ldg(p + o);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -1542,9 +1550,12 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1H_WIDE_MINB)
                     if (j < pos) {
                         const int col = h ? nc1 : nc0;
                         double x[BS];
+                        // s - s' was stored by the last backward sweep for the owned rows
+                        const bool pre = dlt && col * BS < A.n;
 #pragma unroll
                         for (int cc = 0; cc < BS; ++cc)
-                            x[cc] = __ldg(s + (size_t)col * BS + cc) - __ldg(sp + (size_t)col * BS + cc);
+                            x[cc] = pre ? __ldg(dlt + (size_t)col * BS + cc)
+                                        : __ldg(s + (size_t)col * BS + cc) - __ldg(sp + (size_t)col * BS + cc);
 #pragma unroll
                         for (int c = 0; c < BS; ++c)
 #pragma unroll
@@ -2183,7 +2194,8 @@ __global__ void __launch_bounds__(kBlock, P2G_B1BLK_MINB)
 template <int BS, bool LAST>
 __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1H_WIDE_MINB)
     k_gs_backward_b1s(Mat A, NodeTab T, const double* __restrict__ f, const double* xlo, double* s,
-                      const int* active, int nb, int ne, double* part_rs, int accumulate) {
+                      const int* active, int nb, int ne, double* part_rs, int accumulate,
+                      double* dlt) {
     double rs[1] = {0.0};
     if (active[0]) {
         P2G_B1S_NODE_LOOP(0, BS, A, T, nb, ne, {
@@ -2230,7 +2242,12 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1H_WIDE_MINB)
                     }
                     sn[c] = acc / ob[c][c];
                 }
-                if (hl < BS) s[(size_t)node * BS + hl] = pick_row<BS>(sn, hl);
+                if (hl < BS) {
+                    const double sv = pick_row<BS>(sn, hl);
+                    s[(size_t)node * BS + hl] = sv;
+                    // s - s' of the out-of-place last sweep, for the Kp recurrence's gathers
+                    if (dlt) dlt[(size_t)node * BS + hl] = sv - pick_row<BS>(xo, hl);
+                }
                 if (LAST && hl == 0) {
 #pragma unroll
                     for (int c = 0; c < BS; ++c) rs[0] += fo[c] * sn[c];
@@ -2245,7 +2262,8 @@ template <int BS>
 __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1H_WIDE_MINB)
     k_kp_update_b1s(Mat A, NodeTab T, const double* __restrict__ r, const double* __restrict__ s,
                     const double* __restrict__ sp, double* __restrict__ Kp, double* __restrict__ p,
-                    const double* beta, const int* active, double* part) {
+                    const double* beta, const int* active, double* part,
+                    const double* __restrict__ dlt) {
     double dacc[1] = {0.0};
     if (active[0]) {
         const double bt = beta[0];
@@ -2261,15 +2279,18 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_B1H_WIDE_MINB)
             if (valid) {
 #pragma unroll
                 for (int c = 0; c < BS; ++c)
-                    xd[c] = __ldg(s + (size_t)node * BS + c) - __ldg(sp + (size_t)node * BS + c);
+                    xd[c] = dlt ? __ldg(dlt + (size_t)node * BS + c)
+                                : __ldg(s + (size_t)node * BS + c) - __ldg(sp + (size_t)node * BS + c);
                 ri = __ldg(r + o), si = __ldg(s + o), kpo = __ldg(Kp + o), po = __ldg(p + o);
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
                     if (hl + 16 * h < pos) {
                         const int col = h ? nc1 : nc0;
+                        const bool pre = dlt && col * BS < A.n;
 #pragma unroll
                         for (int cc = 0; cc < BS; ++cc)
-                            x[h][cc] = __ldg(s + (size_t)col * BS + cc) - __ldg(sp + (size_t)col * BS + cc);
+                            x[h][cc] = pre ? __ldg(dlt + (size_t)col * BS + cc)
+                                           : __ldg(s + (size_t)col * BS + cc) - __ldg(sp + (size_t)col * BS + cc);
                     }
             }
             B1S_WAIT()

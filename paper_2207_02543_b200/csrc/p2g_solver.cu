@@ -131,6 +131,7 @@ struct p2g_handle {
     bool has_state = false;  // a solve ran since the last setup (Krylov state valid)
     double* s_final = nullptr;  // buffer holding B r after the post-smoother
     double* s_prol = nullptr;   // prolongated s' (Kp recurrence)
+    const double* dlt_of = nullptr;  // the sweep output whose s - s' the last backward sweep left in d_t
 
     // graph
     cudaGraphExec_t loop_exec = nullptr;
@@ -642,8 +643,13 @@ struct Run {
                               : (last ? k_gs_backward_b1h<3, true> : k_gs_backward_b1h<3, false>);
                 const size_t smem = stg ? kB1sSmem : 0;
                 dim3 g = blk1_grid(h, (maxc + 1) / 2, (const void*)fn, true, smem);
+                // out-of-place last sweep (D9): also store s - s' for the recurrence's gathers
+                // (d_t is free between the restriction and the next residual)
+                const bool dl = last && xlo != s && h->d_t && !std::getenv("P2G_NO_DLT");
+                h->dlt_of = dl ? s : (h->dlt_of == s ? nullptr : h->dlt_of);
                 fn<<<g, kBlock, smem, h->stream>>>(A, ntab(h), f, xlo, s, h->d_active, nb, ne,
-                                                last ? h->d_part_rs : nullptr, first_phase ? 0 : 1);
+                                                last ? h->d_part_rs : nullptr, first_phase ? 0 : 1,
+                                                dl ? h->d_t : nullptr);
                 if (last) *rs_rows = g.x / kCluster;
                 count_launch(h, KC_BWD);
                 CU(cudaGetLastError());
@@ -728,14 +734,15 @@ struct Run {
         bool done = false;
         if constexpr (Sh::W == 1) {
             if (blk1_hw(h)) {
+                const double* dlt = h->dlt_of == s_new ? h->d_t : nullptr;
                 if (blk1_stg(h, 4))
                     k_kp_update_b1s<3><<<g, kBlock, kB1sSmem, h->stream>>>(
                         A, ntab(h), h->d_r, s_new, s_prol, h->d_Kp, h->d_p, h->d_beta, h->d_active,
-                        h->d_part_dot);
+                        h->d_part_dot, dlt);
                 else
                     k_kp_update_b1h<3><<<g, kBlock, 0, h->stream>>>(A, ntab(h), h->d_r, s_new, s_prol,
                                                                      h->d_Kp, h->d_p, h->d_beta,
-                                                                     h->d_active, h->d_part_dot);
+                                                                     h->d_active, h->d_part_dot, dlt);
                 done = true;
             } else if (blk1_half(h)) {
                 P2G_BS_SWITCH(h->pat.bs, {
