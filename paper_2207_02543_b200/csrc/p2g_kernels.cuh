@@ -2758,6 +2758,312 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_RESTRICT2_MINB)
     cl.sync();
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised bulk-copy restriction for large systems (c3 / c4 shapes).
+// The register-fed kernels keep every warp on the chain global load -> DMMA
+// and re-read each Phi row once per 16 instances; the first staged form
+// (k_restrict_mma) released its stages with a CTA barrier, which stalled the
+// DMMA warps behind the slowest one.  Here:
+//  * one PRODUCER warp (warp kWarps) streams RT-row tiles of T (one bulk copy
+//    per row into a padded row stride: conflict-free 16-byte fragment reads)
+//    and of the padded Phi (one copy) into an NS-stage ring; a stage is handed
+//    over by a FULL mbarrier (expect_tx) and handed back by an EMPTY mbarrier
+//    on which each consumer warp arrives once -- no CTA-wide barrier in the loop;
+//  * 8 CONSUMER warps; a warp owns 32 instances (four 8-instance n-blocks fed
+//    by two 16-byte shared loads: .x / .y are the even / odd instances) and
+//    every m-block, so a Phi fragment is used four times and the CTA tile
+//    spans TBW = 64 / 128 / 256 instances (at TBW = Bp, Phi is read from DRAM
+//    once).  Warps split a stage's k-steps KSPLIT = 8 / (TBW / 32) ways.
+//  * epilogue as k_restrict_reg2: fixed-order k-split sum in shared memory,
+//    fixed-order cluster sum into the cluster's partial row (deterministic).
+constexpr int kWsBlock = kBlock + 32;
+template <int TBW, int KMAX>
+struct WsTile {
+    static constexpr int NG = TBW / 32, KSPLIT = kWarps / NG;
+    static constexpr int QW = 4;                // k-steps per consumer warp and stage
+    static constexpr int RT = 4 * QW * KSPLIT;  // rows per stage
+    // A stage holds its rows as four QUARTERS of QR consecutive rows; the four
+    // rows of a k-step are row q of each quarter (lane%4 picks the quarter).
+    // Each quarter is padded by 32 bytes, so the four lanes of a fragment
+    // column read different bank groups (data: 16-byte loads; Phi: 8-byte
+    // loads, each bank hit twice), and a quarter is ONE bulk copy whenever its
+    // rows are contiguous in global memory (Phi always; the data when TBW = Bp).
+    static constexpr int QR = RT / 4;
+    static constexpr int KS = phi_stride(KMAX);
+    static constexpr int QT = QR * TBW + 4;  // data quarter stride (doubles)
+    static constexpr int QP = QR * KS + 4;   // Phi quarter stride
+    static constexpr int T_DBL = 4 * QT;
+    static constexpr int STAGE = T_DBL + 4 * QP;  // doubles (a multiple of 4: 32-byte aligned)
+    static constexpr int NSMAX = (227 * 1024 - 256) / (STAGE * 8);
+    static constexpr int NS = NSMAX < 4 ? NSMAX : 4;
+    static constexpr size_t SMEM = sizeof(double) * (size_t)NS * STAGE + 128;
+    static_assert(TBW % 32 == 0 && kWarps % NG == 0 && NS >= 2, "tile geometry");
+    static_assert((size_t)KMAX * TBW <= (size_t)NS * STAGE, "epilogue buffer fits the ring");
+};
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int TBW, int KMAX, bool MASK>
+__device__ __forceinline__ void ws_stage_mma(const double* Ts, const double* Ps, int ks, int mb,
+                                             int nr, int ig, int kp, int g, int tg,
+                                             double (&acc)[(KMAX + 7) / 8][4][2]) {
+    using WT = WsTile<TBW, KMAX>;
+    constexpr int MBX = (KMAX + 7) / 8;
+#pragma unroll
+    for (int j = 0; j < WT::QW; ++j) {
+        const int q = kp * WT::QW + j;  // row q of quarter tg
+        const bool ok = !MASK || tg * WT::QR + q < nr;
+        const double* tr = Ts + tg * WT::QT + q * TBW + 32 * ig + 2 * g;
+        double2 b0 = *reinterpret_cast<const double2*>(tr);
+        double2 b1 = *reinterpret_cast<const double2*>(tr + 16);
+        if (MASK && !ok) b0 = b1 = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int m = 0; m < MBX; ++m)
+            if (m < mb) {
+                double a = Ps[tg * WT::QP + q * ks + 8 * m + g];
+                if (MASK && !ok) a = 0.0;
+                dmma(acc[m][0][0], acc[m][0][1], a, b0.x);
+                dmma(acc[m][1][0], acc[m][1][1], a, b0.y);
+                dmma(acc[m][2][0], acc[m][2][1], a, b1.x);
+                dmma(acc[m][3][0], acc[m][3][1], a, b1.y);
+            }
+    }
+}
+
+template <int TBW, int KMAX>
+__global__ void P2G_CLUSTER __launch_bounds__(kWsBlock, 1)
+    k_restrict_ws(int n, int Bp, const double* __restrict__ t, const double* __restrict__ phit,
+                  int k, int ks, double* part) {
+    using WT = WsTile<TBW, KMAX>;
+    constexpr int MBX = (KMAX + 7) / 8;
+    extern __shared__ __align__(128) double dsm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm + (size_t)WT::NS * WT::STAGE);
+    uint64_t* empty = full + WT::NS;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, tg = lane & 3;
+    const int bt0 = blockIdx.y * TBW;
+    const int ntiles = (n + WT::RT - 1) / WT::RT;
+    const int mb = (k + 7) / 8;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < WT::NS; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], kWarps);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int ig = warp % WT::NG, kp = warp / WT::NG;
+    double acc[MBX][4][2];
+#pragma unroll
+    for (int m = 0; m < MBX; ++m)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[m][j][0] = acc[m][j][1] = 0.0;
+    if (warp == kWarps) {  // producer
+        const uint64_t pol = l2_evict_first_policy();
+        int it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int st = it % WT::NS;
+            if (it >= WT::NS) mbar_wait(&empty[st], ((it / WT::NS) - 1) & 1);
+            double* stage = dsm + (size_t)st * WT::STAGE;
+            const int r0 = tile * WT::RT, nr = min(WT::RT, n - r0);
+            if (lane == 0)
+                mbar_arrive_tx(&full[st], static_cast<uint32_t>(nr) * (ks + TBW) * 8u);
+            __syncwarp();
+            if (lane < 4) {  // Phi: one copy per quarter
+                const int q0 = lane * WT::QR, qn = min(WT::QR, nr - q0);
+                if (qn > 0)
+                    bulk_g2s(stage + WT::T_DBL + lane * WT::QP, phit + (size_t)(r0 + q0) * ks,
+                             static_cast<uint32_t>(qn * ks) * 8u, &full[st]);
+            }
+            if (Bp == TBW) {  // contiguous rows: one copy per quarter
+                if (lane >= 4 && lane < 8) {
+                    const int c = lane - 4, q0 = c * WT::QR, qn = min(WT::QR, nr - q0);
+                    if (qn > 0)
+                        bulk_g2s_hint(stage + c * WT::QT, t + (size_t)(r0 + q0) * Bp,
+                                      static_cast<uint32_t>(qn) * TBW * 8u, &full[st], pol);
+                }
+            } else {
+                for (int r = lane; r < nr; r += 32)
+                    bulk_g2s_hint(stage + (r / WT::QR) * WT::QT + (r % WT::QR) * TBW,
+                                  t + (size_t)(r0 + r) * Bp + bt0, TBW * 8u, &full[st], pol);
+            }
+        }
+    } else {  // consumers
+        int it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int st = it % WT::NS;
+            const double* Ts = dsm + (size_t)st * WT::STAGE;
+            const double* Ps = Ts + WT::T_DBL;
+            mbar_wait(&full[st], (it / WT::NS) & 1);
+            const int nr = min(WT::RT, n - tile * WT::RT);
+            if (nr == WT::RT)
+                ws_stage_mma<TBW, KMAX, false>(Ts, Ps, ks, mb, nr, ig, kp, g, tg, acc);
+            else
+                ws_stage_mma<TBW, KMAX, true>(Ts, Ps, ks, mb, nr, ig, kp, g, tg, acc);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+        }
+    }
+    __syncthreads();  // every issued stage has been consumed: the ring is free
+    // lane holds C[8m + g][32 ig + 16 h + 4 tg + {0 (even .0), 1 (odd .0), 2 (even .1), 3 (odd .1)}]
+    double* tot = dsm;  // [k][TBW]
+    for (int kq = WT::KSPLIT - 1; kq >= 0; --kq) {  // fixed-order k-split sum
+        if (warp < kWarps && kp == kq) {
+#pragma unroll
+            for (int m = 0; m < MBX; ++m)
+                if (8 * m + g < k) {
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        double* d = tot + (size_t)(8 * m + g) * TBW + 32 * ig + 16 * hh + 4 * tg;
+                        const double v0 = acc[m][2 * hh][0], v1 = acc[m][2 * hh + 1][0];
+                        const double v2 = acc[m][2 * hh][1], v3 = acc[m][2 * hh + 1][1];
+                        if (kq == WT::KSPLIT - 1) {
+                            d[0] = v0; d[1] = v1; d[2] = v2; d[3] = v3;
+                        } else {
+                            d[0] = d[0] + v0; d[1] = d[1] + v1; d[2] = d[2] + v2; d[3] = d[3] + v3;
+                        }
+                    }
+                }
+        }
+        __syncthreads();
+    }
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    {  // every CTA of the cluster sums its share of the entries (same rank order)
+        double* prow = part + (size_t)(blockIdx.x / kCluster) * k * Bp + bt0;
+        for (int q = threadIdx.x + (int)cl.block_rank() * kWsBlock; q < k * TBW; q += kWsBlock * kCluster) {
+            double tt = 0.0;
+#pragma unroll
+            for (int r = 0; r < kCluster; ++r) tt += cl.map_shared_rank(tot, r)[q];
+            prow[(size_t)(q / TBW) * Bp + q % TBW] = tt;
+        }
+    }
+    cl.sync();
+}
+
+// Warp-specialised bulk-copy prolongation S (+)= Phi E, the same ring as
+// k_restrict_ws: the producer warp streams RT-row tiles of Phi (and, unless
+// ASSIGN, of S into a row stride of 64 bytes mod 128: conflict-free C-fragment
+// reads); a consumer warp owns 32 instances (four 8-instance n-blocks, E's B
+// fragments in registers) and MPW 8-row m-blocks of each stage, forms the
+// correction, adds it to S (u += 1.0 * lift(e), pod.hpp:201-202) and stores
+// straight to global memory (masked for inactive instances).  With TBW = Bp
+// a Phi row is read once for the whole batch.
+template <int TBW, int KMAX>
+struct WsPTile {
+    static constexpr int NG = TBW / 32, MSPLIT = kWarps / NG;
+    static constexpr int MPW = 2;                 // m-blocks per consumer warp and stage
+    static constexpr int RT = 8 * MPW * MSPLIT;   // rows per stage
+    static constexpr int TS = TBW + 8;            // data-row stride: 64 bytes mod 128
+    static constexpr int KS = phi_stride(KMAX);
+    static constexpr int T_DBL = RT * TS;
+    static constexpr int STAGE = T_DBL + RT * KS;
+    static constexpr int NSMAX = (227 * 1024 - 256) / (STAGE * 8);
+    static constexpr int NS = NSMAX < 4 ? NSMAX : 4;
+    static constexpr size_t SMEM = sizeof(double) * (size_t)NS * STAGE + 128;
+    static_assert(TBW % 32 == 0 && kWarps % NG == 0 && NS >= 2, "tile geometry");
+};
+
+template <int TBW, int KMAX, bool ASSIGN>
+__global__ void __launch_bounds__(kWsBlock, 1)
+    k_prolong_ws(int n, int Bp, double* s, const double* __restrict__ phit, int k, int ks,
+                 const double* __restrict__ e, const int* active) {
+    using WT = WsPTile<TBW, KMAX>;
+    constexpr int KQ = (KMAX + 3) / 4;
+    extern __shared__ __align__(128) double dsm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm + (size_t)WT::NS * WT::STAGE);
+    uint64_t* empty = full + WT::NS;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, tg = lane & 3;
+    const int bt0 = blockIdx.y * TBW;
+    const int ntiles = (n + WT::RT - 1) / WT::RT;
+    const int kq = (k + 3) / 4;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < WT::NS; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], kWarps);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (warp == kWarps) {  // producer
+        int it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int st = it % WT::NS;
+            if (it >= WT::NS) mbar_wait(&empty[st], ((it / WT::NS) - 1) & 1);
+            double* stage = dsm + (size_t)st * WT::STAGE;
+            const int r0 = tile * WT::RT, nr = min(WT::RT, n - r0);
+            const uint32_t pbytes = static_cast<uint32_t>(nr * ks) * 8u;
+            const uint32_t tbytes = ASSIGN ? 0u : static_cast<uint32_t>(nr) * TBW * 8u;
+            if (lane == 0) mbar_arrive_tx(&full[st], pbytes + tbytes);
+            __syncwarp();
+            if (lane == 0) bulk_g2s(stage + WT::T_DBL, phit + (size_t)r0 * ks, pbytes, &full[st]);
+            if constexpr (!ASSIGN)
+                for (int r = lane; r < nr; r += 32)
+                    bulk_g2s(stage + r * WT::TS, s + (size_t)(r0 + r) * Bp + bt0, TBW * 8u, &full[st]);
+        }
+        return;
+    }
+    const int ig = warp % WT::NG, mp = warp / WT::NG;
+    double be[KQ][4];
+    bool act0[4], act1[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+        for (int q = 0; q < KQ; ++q) {
+            const int a = 4 * q + tg;
+            be[q][j] = a < k ? e[(size_t)a * Bp + bt0 + 32 * ig + 8 * j + g] : 0.0;
+        }
+        const int col = bt0 + 32 * ig + 8 * j + 2 * tg;
+        act0[j] = active[col] != 0;
+        act1[j] = active[col + 1] != 0;
+    }
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int st = it % WT::NS;
+        const double* Ss = dsm + (size_t)st * WT::STAGE;
+        const double* Ps = Ss + WT::T_DBL;
+        mbar_wait(&full[st], (it / WT::NS) & 1);
+        const int r0 = tile * WT::RT, nr = min(WT::RT, n - r0);
+#pragma unroll
+        for (int u = 0; u < WT::MPW; ++u) {
+            const int row = 8 * (mp * WT::MPW + u) + g;
+            double c[4][2];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) c[j][0] = c[j][1] = 0.0;
+#pragma unroll
+            for (int q = 0; q < KQ; ++q)
+                if (q < kq) {
+                    const double a = Ps[row * ks + 4 * q + tg];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) dmma(c[j][0], c[j][1], a, be[q][j]);
+                }
+            if (row < nr) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int cl = 32 * ig + 8 * j + 2 * tg;
+                    double o0 = c[j][0], o1 = c[j][1];
+                    if constexpr (!ASSIGN) {
+                        const double2 sv = *reinterpret_cast<const double2*>(Ss + row * WT::TS + cl);
+                        o0 = __dadd_rn(sv.x, o0);
+                        o1 = __dadd_rn(sv.y, o1);
+                    }
+                    double* dst = s + (size_t)(r0 + row) * Bp + bt0 + cl;
+                    if (act0[j] && act1[j])
+                        *reinterpret_cast<double2*>(dst) = make_double2(o0, o1);
+                    else {
+                        if (act0[j]) dst[0] = o0;
+                        if (act1[j]) dst[1] = o1;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+    }
+}
+
 // the CTA's warps share 8-row m-blocks (NB n-blocks each; with TB = 32 two
 // m-blocks per step); U steps of S / Phi loads issued before their MMAs
 #ifndef P2G_PROLONG_U_WIDE

@@ -262,6 +262,19 @@ constexpr int kProlongTmaRows = 1 << 18;  // rows from which the prolongation is
 
 // the wide tensor-core restriction (k_restrict_reg2); P2G_RESTRICT_WIDE=0
 // selects k_restrict_reg (A/B)
+// the warp-specialised bulk-copy restriction (k_restrict_ws) from this many
+// rows on (P2G_RESTRICT_WS=0 disables it, =1 forces it at any size)
+constexpr int kRestrictWsRows = 1 << 18;
+int restrict_ws_mode() {
+    const char* v = std::getenv("P2G_RESTRICT_WS");
+    return v ? (v[0] == '0' ? 0 : 2) : 1;
+}
+
+int prolong_ws_mode() {  // k_prolong_ws, same convention (P2G_PROLONG_WS)
+    const char* v = std::getenv("P2G_PROLONG_WS");
+    return v ? (v[0] == '0' ? 0 : 2) : 1;
+}
+
 bool restrict_wide() {
     static const bool w = [] {
         const char* v = std::getenv("P2G_RESTRICT_WIDE");
@@ -269,6 +282,9 @@ bool restrict_wide() {
     }();
     return w;
 }
+
+template <int KM>
+struct KTag {};
 
 int kbucket(int k) {
     if (k <= 8) return 8;
@@ -347,7 +363,7 @@ void count_launch(p2g_handle* h, int kclass) {
 // Resident CTAs per kernel (one full wave), cached per function.  For the
 // cluster kernels this is the number of co-resident CLUSTERS x kCluster, so
 // the grid never spills into a partial second wave.
-int resident_ctas(p2g_handle* h, const void* fn, bool cluster, size_t smem = 0) {
+int resident_ctas(p2g_handle* h, const void* fn, bool cluster, size_t smem = 0, int block = kBlock) {
     for (auto& e : h->occ_cache)
         if (e.first == fn) return e.second;
     int ctas = 0;
@@ -356,7 +372,7 @@ int resident_ctas(p2g_handle* h, const void* fn, bool cluster, size_t smem = 0) 
     if (cluster) {
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3(kCluster * 1024, 1, 1);
-        lc.blockDim = dim3(kBlock, 1, 1);
+        lc.blockDim = dim3(block, 1, 1);
         lc.dynamicSmemBytes = smem;
         int ncl = 0;
         if (cudaOccupancyMaxActiveClusters(&ncl, fn, &lc) != cudaSuccess || ncl <= 0) {
@@ -366,7 +382,7 @@ int resident_ctas(p2g_handle* h, const void* fn, bool cluster, size_t smem = 0) 
         ctas = ncl * kCluster;
     } else {
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, smem);
         ctas = std::max(occ, 1) * h->num_sms;
     }
     h->occ_cache.emplace_back(fn, ctas);
@@ -793,6 +809,23 @@ struct Run {
         return P2G_OK;
     }
 
+    template <int TBW, int KM>
+    static int restrict_ws(p2g_handle* h, const double* t, int* nb_out, KTag<KM>) {
+        using WT = WsTile<TBW, KM>;
+        auto fn = k_restrict_ws<TBW, KM>;
+        const int n = static_cast<int>(h->pat.n);
+        const int64_t need = (n + WT::RT - 1) / WT::RT;
+        const int64_t tiles = h->Bp / TBW;
+        int64_t gx = std::min<int64_t>(
+            need, std::max<int64_t>(resident_ctas(h, (const void*)fn, true, WT::SMEM, kWsBlock) / tiles, kCluster));
+        gx = std::min<int64_t>(std::max<int64_t>(gx, 1), h->nb_cap);
+        gx = (gx + kCluster - 1) / kCluster * kCluster;
+        dim3 g((unsigned)gx, (unsigned)tiles);
+        fn<<<g, kWsBlock, WT::SMEM, h->stream>>>(n, h->Bp, t, h->d_phit, h->k, h->phi_ks, h->d_part_c);
+        *nb_out = g.x / kCluster;
+        return P2G_OK;
+    }
+
     // c = Phi^T t with t = FORM(f, s) (RES_VECTOR: t = f).  The residual goes
     // to its own buffer d_t (Kp must survive the iteration for the recurrence).
     static int restrict_(p2g_handle* h, int form, const double* f, const double* s, int* nb_out) {
@@ -845,6 +878,18 @@ struct Run {
         const int n = static_cast<int>(h->pat.n);
         if constexpr (Sh::S == 1) {  // batched tiles: tensor-core restriction
             constexpr int TB = Sh::T;
+            const int wsm = restrict_ws_mode();
+            if (h->Bp % 64 == 0 && std::getenv("P2G_TMA") == nullptr &&
+                (wsm == 2 || (wsm == 1 && n >= kRestrictWsRows))) {
+                KSWITCH(k, {
+                    if (h->Bp % 256 == 0) restrict_ws<256>(h, t, nb_out, KTag<KM>{});
+                    else if (h->Bp % 128 == 0) restrict_ws<128>(h, t, nb_out, KTag<KM>{});
+                    else restrict_ws<64>(h, t, nb_out, KTag<KM>{});
+                });
+                count_launch(h, KC_RESTRICT);
+                CU(cudaGetLastError());
+                return P2G_OK;
+            }
             KSWITCH(k, {
                 const bool tma = std::getenv("P2G_TMA") != nullptr;
                 const bool wide = TB % 16 == 0 && !tma && restrict_wide();
@@ -894,11 +939,36 @@ struct Run {
         return P2G_OK;
     }
 
+    template <int TBW, int KM>
+    static void prolong_ws(p2g_handle* h, double* s, int n, bool assign, KTag<KM>) {
+        using WT = WsPTile<TBW, KM>;
+        auto fn = assign ? k_prolong_ws<TBW, KM, true> : k_prolong_ws<TBW, KM, false>;
+        const int64_t need = (n + WT::RT - 1) / WT::RT;
+        const int64_t tiles = h->Bp / TBW;
+        int64_t gx = std::min<int64_t>(
+            need, std::max<int64_t>(resident_ctas(h, (const void*)fn, false, WT::SMEM, kWsBlock) / tiles, 1));
+        dim3 g((unsigned)std::max<int64_t>(gx, 1), (unsigned)tiles);
+        fn<<<g, kWsBlock, WT::SMEM, h->stream>>>(n, h->Bp, s, h->d_phit, h->k, h->phi_ks, h->d_e,
+                                                 h->d_active);
+    }
+
     static int prolong(p2g_handle* h, double* s, bool assign) {
         const int k = h->k;
         const int n = static_cast<int>(h->pat.n + h->n_ghost);  // ghosts too (partitioned)
         if constexpr (Sh::S == 1) {  // batched tiles: bulk-copy pipelined prolongation
             constexpr int TB = Sh::T;
+            const int wsm = prolong_ws_mode();
+            if (h->Bp % 64 == 0 && std::getenv("P2G_TMA") == nullptr &&
+                (wsm == 2 || (wsm == 1 && n >= kProlongTmaRows))) {
+                KSWITCH(k, {
+                    if (h->Bp % 256 == 0) prolong_ws<256>(h, s, n, assign, KTag<KM>{});
+                    else if (h->Bp % 128 == 0) prolong_ws<128>(h, s, n, assign, KTag<KM>{});
+                    else prolong_ws<64>(h, s, n, assign, KTag<KM>{});
+                });
+                count_launch(h, KC_PROLONG);
+                CU(cudaGetLastError());
+                return P2G_OK;
+            }
             KSWITCH(k, {
                 // the TMA-staged (bulk copy + mbarrier) form pays on large systems
                 // (c3 975 vs 1100 us, c4 190 vs 201), not on c2 (21 vs 18.5 us)

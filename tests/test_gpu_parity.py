@@ -343,6 +343,44 @@ def test_tma_staged_restriction_prolongation_variant(gpu, monkeypatch):
     s.close()
 
 
+@pytest.mark.parametrize("dim,B,k", [(2, 40, 12), (2, 128, 30), (2, 256, 30), (2, 320, 20),
+                                     (3, 64, 30), (2, 64, 48)])
+def test_warp_specialised_projections(gpu, monkeypatch, dim, B, k):
+    """k_restrict_ws / k_prolong_ws (producer warp + full / empty mbarrier ring; the
+    large-system projections, forced here with P2G_RESTRICT_WS=1 P2G_PROLONG_WS=1)
+    at CTA tiles of 64 / 128 / 256
+    instances, with a partial last row tile: the preconditioner agrees with the
+    register-fed restriction's to rounding and with the oracle; solves match."""
+    if dim == 2:
+        m, rp, ci, f, V, phi = small_problem(B=B, k=k, nx=34, ny=17)
+    else:
+        m, rp, ci, f, V, phi = small_problem(dim=3, nx=7, ny=6, nz=5, Lx=1.4, Ly=1.2, Lz=1.0, B=B, k=k)
+    R = np.random.default_rng(11).standard_normal((B, m.n))
+    F = np.broadcast_to(f, (B, m.n)).copy()
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("P2G_RESTRICT_WS", mode)
+        monkeypatch.setenv("P2G_PROLONG_WS", mode)
+        s = make_solver(m, rp, ci, V, phi)
+        S = s.precond_apply(R)
+        x, it, conv, status, hist = s.solve(F, None, 1e-8, 3000, x0_mode=L.X0_REDUCED)
+        assert np.all(conv) and np.all(status == 0)
+        out[mode] = (S, x, it)
+        if mode == "1":
+            perm, prp, pci, pV, pf, pphi = perm_system(s, rp, ci, V, f, phi)
+            for b in (0, B // 2, B - 1):
+                s_ref = _oracle_apply(prp, pci, pV[b], pphi, R[b][perm])
+                assert np.linalg.norm(S[b][perm] - s_ref) <= 1e-11 * np.linalg.norm(s_ref)
+            x0_ref, _, _ = ORC.reduced_solve(prp, pci, pV[B - 1], pf, pphi)
+            ref = ORC.pcg_pod2g(prp, pci, pV[B - 1], pf, pphi, x0_ref, 1e-8, 3000)
+            _check_solve(x[B - 1], it[B - 1], conv[B - 1], status[B - 1], hist[B - 1], None, ref, 1e-8)
+        s.close()
+    S0, x0, it0 = out["0"]
+    S1, x1, it1 = out["1"]
+    assert np.max(np.linalg.norm(S1 - S0, axis=1) / np.linalg.norm(S0, axis=1)) <= 1e-12
+    assert np.max(np.abs(it1.astype(int) - it0.astype(int))) <= 1
+
+
 def test_two_instance_tiles(gpu):
     """B = 70: two 64-instance tiles (grid.y = 2) through every kernel,
     including the tensor-core restriction / prolongation and the coarse solve."""
