@@ -155,6 +155,31 @@ def hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+# FP64 tensor-core (DMMA m8n8k4) peak measured on this pool's B200s with
+# tools/dmma_lab.cu (profiles/r02_dmma_peak.txt): 128 flop / clk / SM.
+FP64_TENSOR_TFLOPS = 37.0
+
+
+def class_table(prof, peak, n, k, B):
+    """Per kernel class: event-bracketed ms, algorithmic bytes and the HBM
+    fraction; the two projections (DMMA kernels) also carry their tensor-core
+    work (k padded to the m-block / k-step the kernels run) against the measured
+    FP64 tensor peak -- the restriction at k = 30 is tensor-bound (7 flop/B
+    against a machine balance of 5.7)."""
+    out = {}
+    for name, (ms, by) in prof.items():
+        e = {"ms": ms, "bytes": by}
+        if ms > 0 and by > 0:
+            e["hbm_frac"] = by / (ms * 1e-3) / 1e9 / peak
+        if ms > 0 and B > 1 and name in ("restrict", "prolong"):
+            kp = (k + 7) // 8 * 8 if name == "restrict" else (k + 3) // 4 * 4
+            fl = 2.0 * n * kp * ((B + 31) // 32 * 32)
+            e["tensor_tflops"] = fl / (ms * 1e-3) / 1e12
+            e["tensor_frac"] = e["tensor_tflops"] / FP64_TENSOR_TFLOPS
+        out[name] = e
+    return out
+
+
 def ncu_traffic(config, kclass):
     """dram bytes per iteration of kernel class `kclass` on `config`, from the
     committed ncu --set full capture of THAT config (profiles/ncu_traffic.json,
@@ -452,7 +477,7 @@ def main():
                          "loop_note": f"captured WHILE loop, {LOOP_ITERS} iterations, all instances "
                                       "active (tol 0); iteration_ms is the sum of the event-bracketed "
                                       "class times",
-                         "classes": {k: {"ms": v[0], "bytes": v[1]} for k, v in prof.items()}},
+                         "classes": class_table(prof, peak, n, int(prob.phi.shape[1]), B)},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
@@ -585,7 +610,7 @@ def c5_arm(args, cfg, ws, rank, local):
                          "algorithmic_bytes_per_iteration": iter_bytes,
                          "iteration_ms": iter_ms,
                          "iteration_frac": iter_bytes / (iter_ms * 1e-3) / 1e9 / peak,
-                         "classes": {k: {"ms": v[0], "bytes": v[1]} for k, v in prof.items()},
+                         "classes": class_table(prof, peak, 0, 0, 1),
                          "note": "rank 0's partition"},
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(l1 - l0), "launches_per_iteration": int(per_iter),

@@ -2776,7 +2776,12 @@ __global__ void P2G_CLUSTER __launch_bounds__(kBlock, P2G_RESTRICT2_MINB)
 //    once).  Warps split a stage's k-steps KSPLIT = 8 / (TBW / 32) ways.
 //  * epilogue as k_restrict_reg2: fixed-order k-split sum in shared memory,
 //    fixed-order cluster sum into the cluster's partial row (deterministic).
+//  * clusters of kWsCluster = 2 CTAs (an SM pair), not kCluster = 8: with one
+//    CTA per SM only 15 clusters of 8 fit the 148 SMs (120 CTAs: ncu
+//    launch__cluster_max_active), and this kernel is FP64-tensor-pipe bound
+//    (93 % DMMA pipe active), so idle SMs cost time one for one.
 constexpr int kWsBlock = kBlock + 32;
+constexpr int kWsCluster = 2;
 template <int TBW, int KMAX>
 struct WsTile {
     static constexpr int NG = TBW / 32, KSPLIT = kWarps / NG;
@@ -2832,7 +2837,7 @@ __device__ __forceinline__ void ws_stage_mma(const double* Ts, const double* Ps,
 }
 
 template <int TBW, int KMAX>
-__global__ void P2G_CLUSTER __launch_bounds__(kWsBlock, 1)
+__global__ void __cluster_dims__(kWsCluster, 1, 1) __launch_bounds__(kWsBlock, 1)
     k_restrict_ws(int n, int Bp, const double* __restrict__ t, const double* __restrict__ phit,
                   int k, int ks, double* part) {
     using WT = WsTile<TBW, KMAX>;
@@ -2931,11 +2936,11 @@ __global__ void P2G_CLUSTER __launch_bounds__(kWsBlock, 1)
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();
     {  // every CTA of the cluster sums its share of the entries (same rank order)
-        double* prow = part + (size_t)(blockIdx.x / kCluster) * k * Bp + bt0;
-        for (int q = threadIdx.x + (int)cl.block_rank() * kWsBlock; q < k * TBW; q += kWsBlock * kCluster) {
+        double* prow = part + (size_t)(blockIdx.x / kWsCluster) * k * Bp + bt0;
+        for (int q = threadIdx.x + (int)cl.block_rank() * kWsBlock; q < k * TBW; q += kWsBlock * kWsCluster) {
             double tt = 0.0;
 #pragma unroll
-            for (int r = 0; r < kCluster; ++r) tt += cl.map_shared_rank(tot, r)[q];
+            for (int r = 0; r < kWsCluster; ++r) tt += cl.map_shared_rank(tot, r)[q];
             prow[(size_t)(q / TBW) * Bp + q % TBW] = tt;
         }
     }

@@ -263,8 +263,9 @@ constexpr int kProlongTmaRows = 1 << 18;  // rows from which the prolongation is
 // the wide tensor-core restriction (k_restrict_reg2); P2G_RESTRICT_WIDE=0
 // selects k_restrict_reg (A/B)
 // the warp-specialised bulk-copy restriction (k_restrict_ws) from this many
-// rows on (P2G_RESTRICT_WS=0 disables it, =1 forces it at any size)
-constexpr int kRestrictWsRows = 1 << 18;
+// rows on (P2G_RESTRICT_WS=0 disables it, =1 forces it at any size); c2
+// (66,048 rows): 16.4 vs 18.8 us, c4 119 vs 152 us, c3 534 vs 1091 us
+constexpr int kRestrictWsRows = 1 << 16;
 int restrict_ws_mode() {
     const char* v = std::getenv("P2G_RESTRICT_WS");
     return v ? (v[0] == '0' ? 0 : 2) : 1;
@@ -363,7 +364,8 @@ void count_launch(p2g_handle* h, int kclass) {
 // Resident CTAs per kernel (one full wave), cached per function.  For the
 // cluster kernels this is the number of co-resident CLUSTERS x kCluster, so
 // the grid never spills into a partial second wave.
-int resident_ctas(p2g_handle* h, const void* fn, bool cluster, size_t smem = 0, int block = kBlock) {
+int resident_ctas(p2g_handle* h, const void* fn, bool cluster, size_t smem = 0, int block = kBlock,
+                  int csize = kCluster) {
     for (auto& e : h->occ_cache)
         if (e.first == fn) return e.second;
     int ctas = 0;
@@ -371,15 +373,15 @@ int resident_ctas(p2g_handle* h, const void* fn, bool cluster, size_t smem = 0, 
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cluster) {
         cudaLaunchConfig_t lc = {};
-        lc.gridDim = dim3(kCluster * 1024, 1, 1);
+        lc.gridDim = dim3(csize * 1024, 1, 1);
         lc.blockDim = dim3(block, 1, 1);
         lc.dynamicSmemBytes = smem;
         int ncl = 0;
         if (cudaOccupancyMaxActiveClusters(&ncl, fn, &lc) != cudaSuccess || ncl <= 0) {
             cudaGetLastError();
-            ncl = h->num_sms / kCluster;
+            ncl = h->num_sms / csize;
         }
-        ctas = ncl * kCluster;
+        ctas = ncl * csize;
     } else {
         int occ = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, smem);
@@ -817,12 +819,13 @@ struct Run {
         const int64_t need = (n + WT::RT - 1) / WT::RT;
         const int64_t tiles = h->Bp / TBW;
         int64_t gx = std::min<int64_t>(
-            need, std::max<int64_t>(resident_ctas(h, (const void*)fn, true, WT::SMEM, kWsBlock) / tiles, kCluster));
-        gx = std::min<int64_t>(std::max<int64_t>(gx, 1), h->nb_cap);
-        gx = (gx + kCluster - 1) / kCluster * kCluster;
+            need, std::max<int64_t>(resident_ctas(h, (const void*)fn, true, WT::SMEM, kWsBlock, kWsCluster) / tiles,
+                                    kWsCluster));
+        gx = std::min<int64_t>(std::max<int64_t>(gx, 1), (int64_t)h->nb_cap * kWsCluster);
+        gx = (gx + kWsCluster - 1) / kWsCluster * kWsCluster;
         dim3 g((unsigned)gx, (unsigned)tiles);
         fn<<<g, kWsBlock, WT::SMEM, h->stream>>>(n, h->Bp, t, h->d_phit, h->k, h->phi_ks, h->d_part_c);
-        *nb_out = g.x / kCluster;
+        *nb_out = g.x / kWsCluster;
         return P2G_OK;
     }
 
