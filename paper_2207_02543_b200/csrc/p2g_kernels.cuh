@@ -2949,25 +2949,33 @@ __global__ void __cluster_dims__(kWsCluster, 1, 1) __launch_bounds__(kWsBlock, 1
 
 // Warp-specialised bulk-copy prolongation S (+)= Phi E, the same ring as
 // k_restrict_ws: the producer warp streams RT-row tiles of Phi (and, unless
-// ASSIGN, of S into a row stride of 64 bytes mod 128: conflict-free C-fragment
-// reads); a consumer warp owns 32 instances (four 8-instance n-blocks, E's B
-// fragments in registers) and MPW 8-row m-blocks of each stage, forms the
-// correction, adds it to S (u += 1.0 * lift(e), pod.hpp:201-202) and stores
-// straight to global memory (masked for inactive instances).  With TBW = Bp
-// a Phi row is read once for the whole batch.
+// ASSIGN, of S); a consumer warp owns 32 instances (four 8-instance n-blocks,
+// E's B fragments in registers) and MPW 8-row m-blocks of each stage, forms
+// the correction, adds it to S (u += 1.0 * lift(e), pod.hpp:201-202) and
+// stores straight to global memory (masked for inactive instances).  With
+// TBW = Bp a Phi row is read once for the whole batch.
+// A stage holds its rows as EIGHTHS of ER consecutive rows; m-block i is row
+// i of each eighth (lane/4 picks the eighth), so an eighth is ONE bulk copy
+// when its rows are contiguous (Phi always; S when TBW = Bp: 16 copies per
+// stage, not one per row -- 512-byte copies are bound by the per-SM TMA
+// operation rate).  Eighth strides: S 64 bytes mod 128 (conflict-free 16-byte
+// C-fragment reads), Phi 4 doubles mod 16 (each bank hit twice by the 8-byte
+// A-fragment reads, the minimum).
 template <int TBW, int KMAX>
 struct WsPTile {
     static constexpr int NG = TBW / 32, MSPLIT = kWarps / NG;
-    static constexpr int MPW = 2;                 // m-blocks per consumer warp and stage
-    static constexpr int RT = 8 * MPW * MSPLIT;   // rows per stage
-    static constexpr int TS = TBW + 8;            // data-row stride: 64 bytes mod 128
+    static constexpr int MPW = 2;                // m-blocks per consumer warp and stage
+    static constexpr int ER = MPW * MSPLIT;      // rows per eighth
+    static constexpr int RT = 8 * ER;            // rows per stage
     static constexpr int KS = phi_stride(KMAX);
-    static constexpr int T_DBL = RT * TS;
-    static constexpr int STAGE = T_DBL + RT * KS;
+    static constexpr int ES = ER * TBW + 8;      // S eighth stride (doubles)
+    static constexpr int EP = ER * KS + ((4 - ER * KS % 16) + 16) % 16;  // Phi eighth stride
+    static constexpr int T_DBL = 8 * ES;
+    static constexpr int STAGE = T_DBL + 8 * EP;
     static constexpr int NSMAX = (227 * 1024 - 256) / (STAGE * 8);
     static constexpr int NS = NSMAX < 4 ? NSMAX : 4;
     static constexpr size_t SMEM = sizeof(double) * (size_t)NS * STAGE + 128;
-    static_assert(TBW % 32 == 0 && kWarps % NG == 0 && NS >= 2, "tile geometry");
+    static_assert(TBW % 32 == 0 && kWarps % NG == 0 && NS >= 2 && EP % 2 == 0, "tile geometry");
 };
 
 template <int TBW, int KMAX, bool ASSIGN>
@@ -2999,14 +3007,29 @@ __global__ void __launch_bounds__(kWsBlock, 1)
             if (it >= WT::NS) mbar_wait(&empty[st], ((it / WT::NS) - 1) & 1);
             double* stage = dsm + (size_t)st * WT::STAGE;
             const int r0 = tile * WT::RT, nr = min(WT::RT, n - r0);
-            const uint32_t pbytes = static_cast<uint32_t>(nr * ks) * 8u;
-            const uint32_t tbytes = ASSIGN ? 0u : static_cast<uint32_t>(nr) * TBW * 8u;
-            if (lane == 0) mbar_arrive_tx(&full[st], pbytes + tbytes);
+            if (lane == 0)
+                mbar_arrive_tx(&full[st], static_cast<uint32_t>(nr) * (ks + (ASSIGN ? 0 : TBW)) * 8u);
             __syncwarp();
-            if (lane == 0) bulk_g2s(stage + WT::T_DBL, phit + (size_t)r0 * ks, pbytes, &full[st]);
-            if constexpr (!ASSIGN)
-                for (int r = lane; r < nr; r += 32)
-                    bulk_g2s(stage + r * WT::TS, s + (size_t)(r0 + r) * Bp + bt0, TBW * 8u, &full[st]);
+            if (lane < 8) {  // Phi: one copy per eighth
+                const int q0 = lane * WT::ER, qn = min(WT::ER, nr - q0);
+                if (qn > 0)
+                    bulk_g2s(stage + WT::T_DBL + lane * WT::EP, phit + (size_t)(r0 + q0) * ks,
+                             static_cast<uint32_t>(qn * ks) * 8u, &full[st]);
+            }
+            if constexpr (!ASSIGN) {
+                if (Bp == TBW) {  // contiguous rows: one copy per eighth
+                    if (lane >= 8 && lane < 16) {
+                        const int c = lane - 8, q0 = c * WT::ER, qn = min(WT::ER, nr - q0);
+                        if (qn > 0)
+                            bulk_g2s(stage + c * WT::ES, s + (size_t)(r0 + q0) * Bp,
+                                     static_cast<uint32_t>(qn) * TBW * 8u, &full[st]);
+                    }
+                } else {
+                    for (int r = lane; r < nr; r += 32)
+                        bulk_g2s(stage + (r / WT::ER) * WT::ES + (r % WT::ER) * TBW,
+                                 s + (size_t)(r0 + r) * Bp + bt0, TBW * 8u, &full[st]);
+                }
+            }
         }
         return;
     }
@@ -3033,14 +3056,15 @@ __global__ void __launch_bounds__(kWsBlock, 1)
         const int r0 = tile * WT::RT, nr = min(WT::RT, n - r0);
 #pragma unroll
         for (int u = 0; u < WT::MPW; ++u) {
-            const int row = 8 * (mp * WT::MPW + u) + g;
+            const int i = mp * WT::MPW + u;    // row i of eighth g
+            const int row = g * WT::ER + i;    // row within the tile
             double c[4][2];
 #pragma unroll
             for (int j = 0; j < 4; ++j) c[j][0] = c[j][1] = 0.0;
 #pragma unroll
             for (int q = 0; q < KQ; ++q)
                 if (q < kq) {
-                    const double a = Ps[row * ks + 4 * q + tg];
+                    const double a = Ps[g * WT::EP + i * ks + 4 * q + tg];
 #pragma unroll
                     for (int j = 0; j < 4; ++j) dmma(c[j][0], c[j][1], a, be[q][j]);
                 }
@@ -3050,7 +3074,8 @@ __global__ void __launch_bounds__(kWsBlock, 1)
                     const int cl = 32 * ig + 8 * j + 2 * tg;
                     double o0 = c[j][0], o1 = c[j][1];
                     if constexpr (!ASSIGN) {
-                        const double2 sv = *reinterpret_cast<const double2*>(Ss + row * WT::TS + cl);
+                        const double2 sv =
+                            *reinterpret_cast<const double2*>(Ss + g * WT::ES + i * TBW + cl);
                         o0 = __dadd_rn(sv.x, o0);
                         o1 = __dadd_rn(sv.y, o1);
                     }

@@ -258,7 +258,10 @@ int ensure(p2g_handle* h, T*& p, size_t count) {
     return P2G_OK;
 }
 
-constexpr int kProlongTmaRows = 1 << 18;  // rows from which the prolongation is TMA-staged
+constexpr int kProlongTmaRows = 1 << 18;  // rows from which k_prolong_mma is used when k_prolong_ws is off
+// the warp-specialised prolongation (k_prolong_ws) from this many rows on: c2
+// (66,048 rows) 16.4 vs 18.5 us, c4 173 vs 190 us, c3 725 vs 969 us
+constexpr int kProlongWsRows = 1 << 16;
 
 // the wide tensor-core restriction (k_restrict_reg2); P2G_RESTRICT_WIDE=0
 // selects k_restrict_reg (A/B)
@@ -962,7 +965,7 @@ struct Run {
             constexpr int TB = Sh::T;
             const int wsm = prolong_ws_mode();
             if (h->Bp % 64 == 0 && std::getenv("P2G_TMA") == nullptr &&
-                (wsm == 2 || (wsm == 1 && n >= kProlongTmaRows))) {
+                (wsm == 2 || (wsm == 1 && n >= kProlongWsRows))) {
                 KSWITCH(k, {
                     if (h->Bp % 256 == 0) prolong_ws<256>(h, s, n, assign, KTag<KM>{});
                     else if (h->Bp % 128 == 0) prolong_ws<128>(h, s, n, assign, KTag<KM>{});
