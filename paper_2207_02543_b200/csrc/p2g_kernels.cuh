@@ -46,7 +46,10 @@ constexpr int kBlock = kWarps * 32;
 // Reduction-producing kernels run in thread-block clusters of kCluster CTAs:
 // the per-CTA partials are combined over DSMEM, so each cluster writes ONE
 // partial row (8x fewer rows for the per-instance scalar reductions).
-constexpr int kCluster = 8;
+#ifndef P2G_KCLUSTER
+#define P2G_KCLUSTER 8
+#endif
+constexpr int kCluster = P2G_KCLUSTER;
 #define P2G_CLUSTER __cluster_dims__(kCluster, 1, 1)
 // Streaming row kernels are latency bound unless the SM is full: cap them at
 // 32 registers so 8 CTAs x 8 warps (100% occupancy) stay resident (the

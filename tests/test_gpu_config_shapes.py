@@ -165,6 +165,19 @@ def test_c3_shape_four_tiles(gpu):
 @pytest.mark.parametrize("dim,world,B", [(2, 2, 1), (2, 3, 1), (2, 4, 8), (3, 2, 1), (3, 4, 1),
                                          (3, 3, 4)])
 def test_partitioned_matches_oracle(gpu, dim, world, B):
+    _partitioned_vs_oracle(dim, world, B)
+
+
+def test_partitioned_with_warp_specialised_projections(gpu, monkeypatch):
+    """A batched row-partitioned solve (B = 40 -> one 64-instance tile, 3
+    partitions) with k_restrict_ws / k_prolong_ws forced: the prolongation
+    covers the ghost rows, the restriction the owned rows only."""
+    monkeypatch.setenv("P2G_RESTRICT_WS", "1")
+    monkeypatch.setenv("P2G_PROLONG_WS", "1")
+    _partitioned_vs_oracle(2, 3, 40)
+
+
+def _partitioned_vs_oracle(dim, world, B):
     """The row-partitioned path (p2g_part_*, in-process transport) against the
     oracle directly.  All partitions share the global node colouring, so the
     partitioned sweep is natural-order GS on the globally colour-permuted

@@ -22,9 +22,9 @@ CLASSES = [
     ("update_presmooth", r"^(void )?(p2g::)?k_(update_pre|update_rows|jacobi)\b"),
     ("gs_forward", r"^(void )?(p2g::)?k_gs_forward\w*\b"),
     ("residual", r"^(void )?(p2g::)?k_residual\w*\b"),
-    ("restrict", r"^(void )?(p2g::)?k_restrict_(vec|tiled|reg2?|mma)\b"),
+    ("restrict", r"^(void )?(p2g::)?k_restrict_(vec|tiled|reg2?|mma|ws)\b"),
     ("coarse_solve", r"^(void )?(p2g::)?k_coarse\b"),
-    ("prolong", r"^(void )?(p2g::)?k_prolong(_tiled|_reg|_mma)?\b"),
+    ("prolong", r"^(void )?(p2g::)?k_prolong(_tiled|_reg|_mma|_ws)?\b"),
     ("gs_backward", r"^(void )?(p2g::)?k_gs_backward\w*\b"),
     ("scalar_reduce", r"^(void )?(p2g::)?k_(alpha|finalize|set_cond|reduce_rows|sum_parts)\b"),
     ("p_update", r"^(void )?(p2g::)?k_pupdate\b"),
