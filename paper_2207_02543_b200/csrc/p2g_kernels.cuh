@@ -45,9 +45,14 @@ constexpr int kWarps = 8;
 constexpr int kBlock = kWarps * 32;
 // Reduction-producing kernels run in thread-block clusters of kCluster CTAs:
 // the per-CTA partials are combined over DSMEM, so each cluster writes ONE
-// partial row (8x fewer rows for the per-instance scalar reductions).
+// partial row.  kCluster = 2 (an SM pair, which always fits): clusters of 8
+// leave SM slots idle -- at 2 CTAs/SM only 33 clusters (264 of 296 CTA slots)
+// are co-resident, at 1 CTA/SM 15 (120 of 148), ncu launch__cluster_max_active
+// -- which cost the hex8 backward sweep 3 % (c4 iteration 15.78 -> 15.61 ms,
+// c2 loop 404.1 -> 401.9 us; 4: 15.68 ms / 402.6 us) for 4x the partial rows
+// of the per-instance scalar reductions.
 #ifndef P2G_KCLUSTER
-#define P2G_KCLUSTER 8
+#define P2G_KCLUSTER 2
 #endif
 constexpr int kCluster = P2G_KCLUSTER;
 #define P2G_CLUSTER __cluster_dims__(kCluster, 1, 1)
