@@ -344,7 +344,7 @@ def test_tma_staged_restriction_prolongation_variant(gpu, monkeypatch):
 
 
 @pytest.mark.parametrize("dim,B,k", [(2, 40, 12), (2, 128, 30), (2, 256, 30), (2, 320, 20),
-                                     (3, 64, 30), (2, 64, 48)])
+                                     (3, 64, 30), (2, 64, 48), (2, 100, 8), (3, 65, 37)])
 def test_warp_specialised_projections(gpu, monkeypatch, dim, B, k):
     """k_restrict_ws / k_prolong_ws (producer warp + full / empty mbarrier ring; the
     large-system projections, forced here with P2G_RESTRICT_WS=1 P2G_PROLONG_WS=1)
