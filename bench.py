@@ -316,7 +316,7 @@ def main():
     b_d = torch.from_numpy(F).to(dev)
     x_d = torch.empty_like(b_d)
     s = BatchSolver(local)
-    s.set_pattern(prob.rp, prob.ci, prob.mesh.block_size)
+    s.set_pattern(prob.rp, prob.ci, prob.mesh.block_size, batch_hint=B)
     stream = torch.cuda.ExternalStream(s.stream(), device=dev)
 
     s.set_basis(prob.phi)  # the offline basis, shared by every batch (pod.hpp:261-263)
@@ -459,7 +459,8 @@ def main():
                        "n_dofs": n, "nnz": nnz, "pod_rank": int(prob.phi.shape[1]),
                        "instances_per_gpu": B, "instances_total": total_solves // args.steps,
                        "tol": cfg.tol, "x0": "reduced_solve",
-                       "smoother": "multicolour symmetric GS (node colours, D1)",
+                       "smoother": "multicolour symmetric GS (%d node colour classes, D1)"
+                                   % (len(s.permutation()[1]) - 1),
                        "l2": "inputs larger than L2 (values %.0f MB per GPU)" % (values.nbytes / 1e6),
                        "parallelism": f"instance-sharded x{ws}",
                        "iterations_mean": float(np.mean(iters)),

@@ -117,6 +117,16 @@ const char* p2g_status_string(int status);
 int p2g_abi_version(void);
 
 /* ---- data -------------------------------------------------------------- */
+/* Optional, BEFORE p2g_set_pattern: the number of instances the handle will be
+ * solved with (0 = unknown, the default).  The reference builds one
+ * Pod2gPreconditioner per instance (bench.hpp:315-330, inside parallel_for,
+ * core/parallel.hpp:16-43), so it has no such notion; here the batch shares one
+ * pattern analysis, and a large batch on a large pattern (nnz x batch >= 2^31)
+ * is coloured with the 64-class wavefront colouring instead of the greedy one
+ * (fewer PCG iterations, D1).  Results are valid for any later batch
+ * size; only the iteration count / speed trade-off depends on the hint. */
+int p2g_set_batch_hint(p2g_handle* h, int64_t batch);
+
 /* Square CSR pattern (CsrMatrix::validate invariants, csr.hpp:33-46: offsets
  * non-decreasing from 0 to nnz, columns strictly increasing and < n, every
  * row holding its diagonal).  block_size = dofs per node (rows

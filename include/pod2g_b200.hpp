@@ -196,6 +196,7 @@ std::vector<std::pair<std::vector<double>, SolveReport>> pcg_solve_batch(
         throw std::invalid_argument("pcg_solve_batch: empty or mismatched batch");
     const std::size_t n = Ks[0]->nrows, nnz = Ks[0]->values.size(), B = Ks.size();
     Handle h(device);
+    h.check(p2g_set_batch_hint(h.get(), static_cast<int64_t>(B)), "set_batch_hint");
     upload_pattern(h, *Ks[0], block_size);
     std::vector<double> vals(B * nnz), F(B * n);
     for (std::size_t b = 0; b < B; ++b) {

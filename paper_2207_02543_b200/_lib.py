@@ -54,6 +54,7 @@ SIGNATURES = [
     ("p2g_smooth", C.c_int, [H, C.c_int32, D, D]),
     ("p2g_coarse_operator", C.c_int, [H, D]),
     ("p2g_get_permutation", C.c_int, [H, I64, I32, I64, C.c_int32]),
+    ("p2g_set_batch_hint", C.c_int, [H, C.c_int64]),
     ("p2g_analyze_node_blocking", C.c_int, [C.c_int64, U64, U64, C.c_int32, I32, I32]),
     ("p2g_analyze_pattern", C.c_int, [C.c_int64, U64, U64, C.c_int32, I64, I32, I64, C.c_int32,
                                       C.c_char_p, C.c_int32]),

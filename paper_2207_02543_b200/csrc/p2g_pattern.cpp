@@ -55,7 +55,7 @@ std::vector<int32_t> order_colours(int ncol, const std::vector<double>& W) {
 }
 
 std::string build_coloured_pattern(int64_t n, const uint64_t* rp, const uint64_t* ci, int bs,
-                                   ColouredPattern& out) {
+                                   ColouredPattern& out, int wave_colours) {
     if (n <= 0) return "p2g_set_pattern: n must be positive";
     if (bs < 1 || bs > 8) return "p2g_set_pattern: block_size outside [1,8]";
     if (n % bs != 0) return "p2g_set_pattern: n not a multiple of block_size";
@@ -130,12 +130,16 @@ std::string build_coloured_pattern(int64_t n, const uint64_t* rp, const uint64_t
     }
     if (ncol > 64) return "p2g_set_pattern: more than 64 node colours";
 
-    // wavefront colouring (experiment: P2G_WAVE_COLOURS=C): colour = level mod C
+    // wavefront colouring (wave_colours = C; P2G_WAVE_COLOURS=C): colour = level mod C
     // with level = the node's level in natural-order Gauss-Seidel's dependency
     // DAG, classes run in level order -- as C grows, natural order.
     bool wave = false;
-    if (const char* w = std::getenv("P2G_WAVE_COLOURS")) {
-        const int C = std::atoi(w);
+    if (wave_colours < 0) {
+        const char* w = std::getenv("P2G_WAVE_COLOURS");
+        wave_colours = w ? std::atoi(w) : 0;
+    }
+    {
+        const int C = wave_colours;
         if (C >= 2 && C <= 64) {
             std::vector<int64_t> lev(nn, 0);
             for (int64_t a = 0; a < nn; ++a)

@@ -35,8 +35,12 @@ std::vector<int32_t> order_colours(int ncol, const std::vector<double>& W);
 // Returns "" on success, else the require()-style message.  Validates the
 // reference invariants, the presence of every diagonal, the int32 range, the
 // node blocking (n % bs == 0) and structural symmetry of the node graph.
+// wave_colours: C >= 2 selects the wavefront colouring (colour = level in
+// natural-order GS's dependency DAG mod C; D1) when it is a proper
+// colouring of this graph, 0 the greedy colouring, -1 reads P2G_WAVE_COLOURS.
 std::string build_coloured_pattern(int64_t n, const uint64_t* row_offsets,
-                                   const uint64_t* col_indices, int bs, ColouredPattern& out);
+                                   const uint64_t* col_indices, int bs, ColouredPattern& out,
+                                   int wave_colours = -1);
 
 // Node-blocked view of a (coloured) local pattern for the node-blocked row
 // kernels (NodeTab, p2g_kernels.cuh).  Returns false unless every node's bs

@@ -131,6 +131,7 @@ struct p2g_handle {
     bool has_state = false;  // a solve ran since the last setup (Krylov state valid)
     double* s_final = nullptr;  // buffer holding B r after the post-smoother
     double* s_prol = nullptr;   // prolongated s' (Kp recurrence)
+    int64_t batch_hint = 0;  // p2g_set_batch_hint: the batch the handle will be used with (0: unknown)
     const double* dlt_of = nullptr;  // the sweep output whose s - s' the last backward sweep left in d_t
 
     // graph
@@ -153,9 +154,10 @@ struct p2g_handle {
     bool capturing = false;
     // profiling
     bool profiling = false;
-    cudaEvent_t kev[64];
+    static constexpr int kMaxKev = 192;  // > 15 + 2 x 64 colour phases
+    cudaEvent_t kev[kMaxKev];
     int kev_n = 0;
-    int kev_class[64];
+    int kev_class[kMaxKev];
 };
 
 namespace {
@@ -348,7 +350,7 @@ cudaError_t prof_record(p2g_handle* h, cudaEvent_t e, cudaStream_t st) {
 }
 
 void prof_mark(p2g_handle* h, int kclass) {
-    if (h->profiling && h->kev_n < 63) {
+    if (h->profiling && h->kev_n < p2g_handle::kMaxKev - 1) {
         h->kev_class[h->kev_n] = kclass;
         prof_record(h, h->kev[h->kev_n + 1], h->stream);
         ++h->kev_n;
@@ -1873,12 +1875,35 @@ int upload_node_table(p2g_handle* h) {
     return P2G_OK;
 }
 
+int p2g_set_batch_hint(p2g_handle* h, int64_t batch) {
+    if (!h || batch < 0) return P2G_EINVAL;
+    h->batch_hint = batch;
+    return P2G_OK;
+}
+
+// Colouring policy (D1).  P2G_WAVE_COLOURS decides when set (-1:
+// build_coloured_pattern reads it).  Otherwise the 64-class wavefront colouring
+// is used when the caller announced a batch (p2g_set_batch_hint) large enough
+// that an iteration streams >= ~50 GB (nnz x padded batch >= 2^31, override:
+// P2G_WAVE_MIN_WORK): there its 14-17 % fewer iterations outweigh its 120
+// extra colour phases per iteration and its less local gathers (c3 +7.7 %,
+// c4 +5.6 % solves/s); on c2-sized work it loses 10-50 %.
+static int wave_colours_for(const p2g_handle* h, int64_t n, const uint64_t* row_offsets) {
+    if (std::getenv("P2G_WAVE_COLOURS")) return -1;
+    if (h->batch_hint < 9 || n <= 0 || !row_offsets) return 0;  // lane-per-instance batches only
+    double min_work = 2147483648.0;
+    if (const char* v = std::getenv("P2G_WAVE_MIN_WORK")) min_work = std::atof(v);
+    const double work = (double)row_offsets[n] * (double)((h->batch_hint + 31) / 32 * 32);
+    return work >= min_work ? 64 : 0;
+}
+
 int p2g_set_pattern(p2g_handle* h, int64_t n, const uint64_t* row_offsets,
                     const uint64_t* col_indices, int32_t block_size) {
     if (!h) return P2G_EINVAL;
     CU(cudaSetDevice(h->device));
     ColouredPattern pat;
-    const std::string msg = build_coloured_pattern(n, row_offsets, col_indices, block_size, pat);
+    const std::string msg = build_coloured_pattern(n, row_offsets, col_indices, block_size, pat,
+                                                   wave_colours_for(h, n, row_offsets));
     REQ(msg.empty(), P2G_EINVAL, msg);
     destroy_graph(h);
     if (h->cstream) CU(cudaStreamSynchronize(h->cstream));

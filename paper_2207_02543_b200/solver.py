@@ -121,10 +121,14 @@ class BatchSolver:
             _raise(st, f"{what}: {msg}" if what else msg)
 
     # -- data
-    def set_pattern(self, row_offsets, col_indices, block_size: int = 1):
+    def set_pattern(self, row_offsets, col_indices, block_size: int = 1, batch_hint: int = 0):
+        """batch_hint: the number of instances the handle will be solved with (0 =
+        unknown); large batches on large patterns get the wavefront colouring
+        (p2g_set_batch_hint, D1)."""
         rp = np.ascontiguousarray(row_offsets, dtype=np.uint64)
         ci = np.ascontiguousarray(col_indices, dtype=np.uint64)
         n = len(rp) - 1
+        self._check(self._L.p2g_set_batch_hint(self._h, int(batch_hint)), "set_batch_hint")
         self._check(self._L.p2g_set_pattern(self._h, n, rp.ctypes.data_as(L.U64),
                                             ci.ctypes.data_as(L.U64), block_size),
                     "set_pattern")

@@ -40,9 +40,9 @@ def small_problem(dim=2, nx=64, ny=32, nz=1, Lx=2.0, Ly=1.0, Lz=1.0, B=1, k=10, 
     return m, rp, ci, f, V, phi
 
 
-def make_solver(m, rp, ci, V, phi, **setup):
+def make_solver(m, rp, ci, V, phi, batch_hint=0, **setup):
     s = BatchSolver(0)
-    s.set_pattern(rp, ci, m.block_size)
+    s.set_pattern(rp, ci, m.block_size, batch_hint=batch_hint)
     s.set_values(V)
     s.set_basis(phi)
     st = s.setup(**setup)
@@ -379,6 +379,50 @@ def test_warp_specialised_projections(gpu, monkeypatch, dim, B, k):
     S1, x1, it1 = out["1"]
     assert np.max(np.linalg.norm(S1 - S0, axis=1) / np.linalg.norm(S0, axis=1)) <= 1e-12
     assert np.max(np.abs(it1.astype(int) - it0.astype(int))) <= 1
+
+
+@pytest.mark.parametrize("dim,B,C", [(2, 40, 8), (2, 40, 16), (3, 33, 12), (2, 40, 0), (3, 33, 0)])
+def test_wavefront_colouring_matches_oracle(gpu, monkeypatch, dim, B, C):
+    """P2G_WAVE_COLOURS=C (colour = level in natural-order GS's dependency DAG mod C;
+    the large-system default candidate measured in DESIGN.md): the sweeps are still
+    natural-order GS on the colour-permuted system, so the oracle on P K P^T applies
+    unchanged -- bit-exact sweeps, iterations within 1, x within 1e-8."""
+    if C:
+        monkeypatch.setenv("P2G_WAVE_COLOURS", str(C))
+    else:  # C = 0: the policy of p2g_set_batch_hint (64 classes for large work), threshold lowered
+        monkeypatch.delenv("P2G_WAVE_COLOURS", raising=False)
+        monkeypatch.setenv("P2G_WAVE_MIN_WORK", "1")
+    if dim == 2:
+        m, rp, ci, f, V, phi = small_problem(B=B, k=10, nx=40, ny=20)
+    else:
+        m, rp, ci, f, V, phi = small_problem(dim=3, nx=8, ny=8, nz=8, Lx=1, Ly=1, Lz=1, B=B, k=8)
+    s = make_solver(m, rp, ci, V, phi, batch_hint=0 if C else B)
+    perm, offs = s.permutation()
+    assert len(offs) - 1 > (4 if dim == 2 else 8)  # more classes than the parity colouring
+    if not C:  # without the hint the same handle setup keeps the greedy colouring
+        s0 = make_solver(m, rp, ci, V, phi)
+        assert len(s0.permutation()[1]) - 1 == (4 if dim == 2 else 8)
+        s0.close()
+    perm, prp, pci, pV, pf, pphi = perm_system(s, rp, ci, V, f, phi)
+    rng = np.random.default_rng(21)
+    Fr = rng.standard_normal((B, m.n))
+    U0 = rng.standard_normal((B, m.n))
+    for direction in (0, 1):
+        U = s.smooth(direction, Fr, U0)
+        for b in (0, B - 1):
+            u_ref, st = ORC.gauss_seidel(prp, pci, pV[b], Fr[b][perm], U0[b][perm], 1,
+                                         backward=bool(direction))
+            assert np.array_equal(U[b][perm], u_ref)
+    F = np.broadcast_to(f, (B, m.n)).copy()
+    x, it, conv, status, hist = s.solve(F, None, 1e-8, 3000, x0_mode=L.X0_REDUCED)
+    assert np.all(conv) and np.all(status == 0)
+    for b in (0, B - 1):
+        x0_ref, _, _ = ORC.reduced_solve(prp, pci, pV[b], pf, pphi)
+        ref = ORC.pcg_pod2g(prp, pci, pV[b], pf, pphi, x0_ref, 1e-8, 3000)
+        _check_solve(x[b], it[b], conv[b], status[b], hist[b], None, ref, 1e-8)
+        ref_m = ORC.pcg_pod2g(prp, pci, pV[b], pf, pphi, x0_ref, 0.0, int(it[b]))
+        assert np.linalg.norm(x[b][perm] - ref_m.u) <= X_RTOL * np.linalg.norm(ref_m.u)
+    s.close()
 
 
 def test_two_instance_tiles(gpu):
