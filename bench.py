@@ -58,6 +58,9 @@ def parse():
                     help="c5 offline stage: snapshot solves behind the k = 40 basis")
     ap.add_argument("--c5-cpu-iters", type=int, default=2,
                     help="c5 CPU baseline: reference PCG iterations timed (1 core)")
+    ap.add_argument("--instances", type=int, default=0,
+                    help="solve only the first N instances of this rank's shard (what a rank of a "
+                         "larger job holds; threshold calibration, not a BASELINE workload)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-instances", type=int, default=0,
@@ -306,6 +309,8 @@ def main():
     t0 = time.perf_counter()
     prob = PR.build_problem(cfg, device=local)
     B, seeds, strong = PR.shard(cfg, ws, rank)
+    if args.instances and args.instances < B:
+        B, seeds = args.instances, seeds[:args.instances]
     values = prob.values(seeds)                 # [B][nnz] natural order (host)
     n, nnz = prob.mesh.n, prob.mesh.nnz
     F = np.ascontiguousarray(np.broadcast_to(prob.f, (B, n)))

@@ -1884,14 +1884,15 @@ int p2g_set_batch_hint(p2g_handle* h, int64_t batch) {
 // Colouring policy (D1).  P2G_WAVE_COLOURS decides when set (-1:
 // build_coloured_pattern reads it).  Otherwise the 64-class wavefront colouring
 // is used when the caller announced a batch (p2g_set_batch_hint) large enough
-// that an iteration streams >= ~50 GB (nnz x padded batch >= 2^31, override:
-// P2G_WAVE_MIN_WORK): there its 14-17 % fewer iterations outweigh its 120
-// extra colour phases per iteration and its less local gathers (c3 +7.7 %,
-// c4 +5.6 % solves/s); on c2-sized work it loses 10-50 %.
+// that an iteration lasts several ms (nnz x padded batch >= 2^30, override:
+// P2G_WAVE_MIN_WORK): there its 11-17 % fewer iterations outweigh its 120
+// extra colour phases per iteration (~3 us each) and its less local gathers
+// (solves/s: c3 +7.7 %, c3 shards of 128 / 64 instances +6.0 / +12.5 %, c4
+// +5.6 %, c4 shard of 32 +5.0 %); on c2-sized work (7.5e7) it loses 10-50 %.
 static int wave_colours_for(const p2g_handle* h, int64_t n, const uint64_t* row_offsets) {
     if (std::getenv("P2G_WAVE_COLOURS")) return -1;
     if (h->batch_hint < 9 || n <= 0 || !row_offsets) return 0;  // lane-per-instance batches only
-    double min_work = 2147483648.0;
+    double min_work = 1073741824.0;
     if (const char* v = std::getenv("P2G_WAVE_MIN_WORK")) min_work = std::atof(v);
     const double work = (double)row_offsets[n] * (double)((h->batch_hint + 31) / 32 * 32);
     return work >= min_work ? 64 : 0;
