@@ -121,7 +121,7 @@ int p2g_abi_version(void);
  * solved with (0 = unknown, the default).  The reference builds one
  * Pod2gPreconditioner per instance (bench.hpp:315-330, inside parallel_for,
  * core/parallel.hpp:16-43), so it has no such notion; here the batch shares one
- * pattern analysis, and a large batch on a large pattern (nnz x batch >= 2^30)
+ * pattern analysis, and a large batch on a large pattern (nnz x batch >= 2^29 for 2 dofs per node, 1.5 x 2^30 otherwise)
  * is coloured with the 64-class wavefront colouring instead of the greedy one
  * (fewer PCG iterations, D1).  Results are valid for any later batch
  * size; only the iteration count / speed trade-off depends on the hint. */

@@ -1884,15 +1884,20 @@ int p2g_set_batch_hint(p2g_handle* h, int64_t batch) {
 // Colouring policy (D1).  P2G_WAVE_COLOURS decides when set (-1:
 // build_coloured_pattern reads it).  Otherwise the 64-class wavefront colouring
 // is used when the caller announced a batch (p2g_set_batch_hint) large enough
-// that an iteration lasts several ms (nnz x padded batch >= 2^30, override:
-// P2G_WAVE_MIN_WORK): there its 11-17 % fewer iterations outweigh its 120
-// extra colour phases per iteration (~3 us each) and its less local gathers
-// (solves/s: c3 +7.7 %, c3 shards of 128 / 64 instances +6.0 / +12.5 %, c4
-// +5.6 %, c4 shard of 32 +5.0 %); on c2-sized work (7.5e7) it loses 10-50 %.
-static int wave_colours_for(const p2g_handle* h, int64_t n, const uint64_t* row_offsets) {
+// that an iteration lasts several ms: there its 11-17 % fewer iterations
+// outweigh its 120 extra colour phases per iteration (~3 us each) and its less
+// local gathers.  Measured (solves/s, work = nnz x padded batch):
+//   Q4 (2 dofs per node): c3 mesh x 256 / 128 / 64 / 32 instances (4.8e9 ..
+//     6.0e8) +7.7 / +6.0 / +12.5 / +13.8 %; c2 (7.5e7) -10..-50 %  -> 2^29
+//   hex8 (3 dofs per node; neighbours spread over 14 classes, not 6): c4 mesh
+//     x 64 / 32 (4.0e9 / 2.0e9) +5.6 / +5.0 %, x 16 / 8 (1.0e9 / 5.0e8)
+//     -2.9 / -4.3 %  -> 1.5 x 2^30
+// P2G_WAVE_MIN_WORK overrides the threshold.
+static int wave_colours_for(const p2g_handle* h, int64_t n, const uint64_t* row_offsets,
+                            int block_size) {
     if (std::getenv("P2G_WAVE_COLOURS")) return -1;
     if (h->batch_hint < 9 || n <= 0 || !row_offsets) return 0;  // lane-per-instance batches only
-    double min_work = 1073741824.0;
+    double min_work = block_size == 2 ? 536870912.0 : 1610612736.0;
     if (const char* v = std::getenv("P2G_WAVE_MIN_WORK")) min_work = std::atof(v);
     const double work = (double)row_offsets[n] * (double)((h->batch_hint + 31) / 32 * 32);
     return work >= min_work ? 64 : 0;
@@ -1904,7 +1909,7 @@ int p2g_set_pattern(p2g_handle* h, int64_t n, const uint64_t* row_offsets,
     CU(cudaSetDevice(h->device));
     ColouredPattern pat;
     const std::string msg = build_coloured_pattern(n, row_offsets, col_indices, block_size, pat,
-                                                   wave_colours_for(h, n, row_offsets));
+                                                   wave_colours_for(h, n, row_offsets, block_size));
     REQ(msg.empty(), P2G_EINVAL, msg);
     destroy_graph(h);
     if (h->cstream) CU(cudaStreamSynchronize(h->cstream));
