@@ -1886,7 +1886,7 @@ int p2g_set_batch_hint(p2g_handle* h, int64_t batch) {
 // is used when the caller announced a batch (p2g_set_batch_hint) large enough
 // that an iteration lasts several ms: there its 11-17 % fewer iterations
 // outweigh its 120 extra colour phases per iteration (~3 us each) and its less
-// local gathers.  Measured (solves/s, work = nnz x padded batch):
+// local gathers.  Measured (solves/s, work = nnz x batch):
 //   Q4 (2 dofs per node): c3 mesh x 256 / 128 / 64 / 32 instances (4.8e9 ..
 //     6.0e8) +7.7 / +6.0 / +12.5 / +13.8 %; c2 (7.5e7) -10..-50 %  -> 2^29
 //   hex8 (3 dofs per node; neighbours spread over 14 classes, not 6): c4 mesh
@@ -1899,7 +1899,7 @@ static int wave_colours_for(const p2g_handle* h, int64_t n, const uint64_t* row_
     if (h->batch_hint < 9 || n <= 0 || !row_offsets) return 0;  // lane-per-instance batches only
     double min_work = block_size == 2 ? 536870912.0 : 1610612736.0;
     if (const char* v = std::getenv("P2G_WAVE_MIN_WORK")) min_work = std::atof(v);
-    const double work = (double)row_offsets[n] * (double)((h->batch_hint + 31) / 32 * 32);
+    const double work = (double)row_offsets[n] * (double)h->batch_hint;
     return work >= min_work ? 64 : 0;
 }
 
