@@ -121,8 +121,9 @@ int p2g_abi_version(void);
  * solved with (0 = unknown, the default).  The reference builds one
  * Pod2gPreconditioner per instance (bench.hpp:315-330, inside parallel_for,
  * core/parallel.hpp:16-43), so it has no such notion; here the batch shares one
- * pattern analysis, and a large batch on a large pattern (nnz x batch >= 2^29 for 2 dofs per node, 1.5 x 2^30 otherwise)
- * is coloured with the 64-class wavefront colouring instead of the greedy one
+ * pattern analysis, and a large batch on a large pattern (nnz x batch >= 2^29
+ * for 2 dofs per node, >= 1.5 x 2^30 otherwise; at least 9 instances) is
+ * coloured with the 64-class wavefront colouring instead of the greedy one
  * (fewer PCG iterations, D1).  Results are valid for any later batch
  * size; only the iteration count / speed trade-off depends on the hint. */
 int p2g_set_batch_hint(p2g_handle* h, int64_t batch);
@@ -131,7 +132,8 @@ int p2g_set_batch_hint(p2g_handle* h, int64_t batch);
  * non-decreasing from 0 to nnz, columns strictly increasing and < n, every
  * row holding its diagonal).  block_size = dofs per node (rows
  * node*bs .. node*bs+bs-1 belong to one node; 1 = point colouring).  The
- * node graph is coloured greedily in natural order. */
+ * node graph is coloured greedily in natural order (or by wavefronts, see
+ * p2g_set_batch_hint). */
 int p2g_set_pattern(p2g_handle* h, int64_t n, const uint64_t* row_offsets,
                     const uint64_t* col_indices, int32_t block_size);
 
